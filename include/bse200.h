@@ -1,0 +1,136 @@
+/*
+ * bse200 — C ABI of the B200-native pseudo-hermitian ChASE hot path.
+ *
+ * Every entry point replaces one operator of the reference Python package
+ * `bsesolve` (paths relative to /root/reference/pkg/src/bsesolve/); the
+ * Python host layer `paper_2601_10557_b200` binds them with ctypes exactly
+ * as a maintainer of the reference would.
+ *
+ * Conventions
+ *   - All matrices are complex128, column-major, interleaved (re, im) —
+ *     numpy's `complex128` / F-order, torch's `complex128` column-major.
+ *   - Pointers named `d_*` are DEVICE pointers (cudaMalloc / torch CUDA
+ *     storage); `h_*` are HOST pointers.  Sizes are int64_t element counts.
+ *   - The Hamiltonian operand `d_ab` is the m x 2m device matrix [A | B]
+ *     (leading dimension `lda` >= m): A hermitian, B symmetric, exactly the
+ *     two blocks `BseHamiltonian` stores (hamiltonian.py:63-96).
+ *   - Work is enqueued on the context's stream (bse_set_stream); functions
+ *     that return host scalars synchronise that stream.
+ *   - Return value: BSE_OK or one of the BSE_E* status codes, which the
+ *     Python layer maps onto the reference exception classes
+ *     (errors.py:8-38).  bse_last_error() returns the message.
+ *   - Deterministic: no atomics in any reduction; reruns are bitwise equal.
+ */
+#ifndef BSE200_H
+#define BSE200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BSE_OK = 0,
+  BSE_EVALIDATION = 1,   /* ValidationError            errors.py:12 */
+  BSE_ENUMERICAL = 2,    /* NumericalError             errors.py:16 */
+  BSE_EINDEFINITE = 3,   /* IndefiniteError            errors.py:20 */
+  BSE_ERANK = 4,         /* RankDeficiencyError        errors.py:24 */
+  BSE_ELANCZOS = 5,      /* LanczosBreakdownError      errors.py:28 */
+  BSE_EHERMITIAN_RQ = 6, /* HermitianRqError           errors.py:32 */
+  BSE_ECUDA = 7          /* CUDA / cuSOLVER failure (NumericalError on the Python side) */
+};
+
+typedef struct bse_ctx bse_ctx;
+
+/* ---- context ------------------------------------------------------------ */
+int bse_ctx_create(int device, bse_ctx** out);
+void bse_ctx_destroy(bse_ctx* ctx);
+int bse_set_stream(bse_ctx* ctx, void* cuda_stream);
+const char* bse_last_error(const bse_ctx* ctx);
+/* number of bse200 kernels launched through this context (evidence counter) */
+int64_t bse_launch_count(const bse_ctx* ctx);
+const char* bse_version(void);
+
+/* ---- Hamiltonian operator ------------------------------------------------ */
+/* y = H x  (low_sign = +1)  or  y = S H x  (low_sign = -1)
+ * replaces apply_h hamiltonian.py:132-151 (and apply_s(apply_h(.)) at
+ * rayleigh_ritz.py:112).  x, y: n x k (n = 2m), must not alias.            */
+int bse_apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_x, int64_t ldx, void* d_y,
+                int64_t ldy, int64_t k, double low_sign);
+
+/* One Chebyshev step y_next = alpha (H y - c y) - beta y_prev, fused in the
+ * GEMM epilogue (chebyshev.py:68-74).  y_next may alias y_prev, not y.    */
+int bse_filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_y, const void* d_yprev,
+                    void* d_ynext, int64_t ld, int64_t k, double c, double alpha, double beta);
+
+/* Whole filter p(H) V (chebyshev.py:51-75): degree `deg` (even) products,
+ * sigma-scaled recurrence with c = center, e = half_width, s = scale_ref.
+ * d_v (n x k, ld) is overwritten with the result; d_work must hold 2 n x k
+ * blocks with the same ld (rotating recurrence buffers).                   */
+int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_v, int64_t ld, int64_t k,
+                         int deg, double c, double e, double s, void* d_work);
+
+/* Residual norms r_j = ||H v_j - lam_j v_j||_2 (rayleigh_ritz.py:182-190),
+ * fused residual-norm epilogue; h_lam (k) in, h_res (k) out on host.      */
+int bse_residuals(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_v, int64_t ldv, int64_t k,
+                  const double* h_lam, double* h_res);
+
+/* ---- orthonormalisation (ortho.py:96-158) --------------------------------- */
+/* In place: project out span(S Y_locked) (Y: n x l, may be l = 0), then
+ * CholQR2; on failure shifted CholQR3 (replacing the Householder fallback);
+ * then the column phase convention of ortho.py:70-82.
+ * *h_method = 0 cholqr2, 1 shifted fallback.  BSE_ERANK on rank deficiency. */
+int bse_s_orthonormalize(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t ldv, const void* d_ylocked,
+                         int64_t l, int64_t ldy, int* h_method);
+int bse_cholqr(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq, int* h_method);
+/* column phase convention alone (fix_column_phases, ortho.py:70-82) */
+int bse_fix_phases(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq);
+
+/* ---- Rayleigh-Ritz (rayleigh_ritz.py:98-179) ------------------------------ */
+/* Hermitian-equivalent oblique RR on the active basis Q (n x k):
+ * h_lam (k) ascending Ritz values, d_vout (n x k) unit Ritz vectors,
+ * *h_lam_min_m = |lambda|_min(Q*SQ).  BSE_EHERMITIAN_RQ when Q*SQ is
+ * singular (< 1e-8), Q*SHQ is not positive definite, or theta ~ 0.        */
+int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
+                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m);
+/* Non-hermitian backup projection (Alg. 3, rayleigh_ritz.py:146-179). */
+int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
+                  double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m);
+
+/* ---- Lanczos bounds (lanczos.py:53-88) ------------------------------------ */
+/* One S-inner-product Lanczos sweep from host start vector h_start (n):
+ * h_alpha (steps), h_beta (steps-1); *h_count = number of alphas produced.
+ * BSE_EINDEFINITE if the start has non-positive S*H norm.                  */
+int bse_lanczos_sweep(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* h_start, int steps,
+                      double* h_alpha, double* h_beta, int* h_count);
+
+/* ---- input checks --------------------------------------------------------- */
+/* Cholesky of the materialised S H (hamiltonian.py:208-218); *h_definite = 1/0. */
+int bse_is_definite(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int* h_definite);
+
+/* ---- synthetic inputs (generate.py:60-83 on the device) -------------------- */
+/* complex normals start_index .. +count of stream `seed` (rng.py:63-81):
+ * bit-exact splitmix64 words, device libm Box-Muller (<= ~1 ulp from host). */
+int bse_complex_normals(bse_ctx* ctx, void* d_out, uint64_t seed, int64_t start_index, int64_t count);
+/* the transpose (cols x rows, column-major) of the rows x cols normal matrix */
+int bse_complex_normals_t(bse_ctx* ctx, void* d_out, uint64_t seed, int64_t rows, int64_t cols);
+/* a <- (a + a^T)/2 (conj = 0) or (a + a^H)/2 (conj = 1), m x m              */
+int bse_symmetrize(bse_ctx* ctx, void* d_a, int64_t m, int64_t lda, int conj);
+/* a <- scale * (conj ? conj(a) : a) + shift * I                             */
+int bse_scale_shift(bse_ctx* ctx, void* d_a, int64_t m, int64_t lda, double scale, double shift, int conj);
+/* eigenvalues (ascending, host) of a hermitian device matrix                */
+int bse_eigvalsh(bse_ctx* ctx, const void* d_a, int64_t k, int64_t lda, double* h_w);
+
+/* ---- generic tall-skinny products (also used by tests) -------------------- */
+/* C = alpha * A^H B + beta C  (A: K x M, B: K x N)   */
+int bse_zgemm_cn(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const void* d_a, int64_t lda,
+                 const void* d_b, int64_t ldb, double beta, void* d_c, int64_t ldc);
+/* C = alpha * A B + beta C    (A: M x K, B: K x N)   */
+int bse_zgemm_nn(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const void* d_a, int64_t lda,
+                 const void* d_b, int64_t ldb, double beta, void* d_c, int64_t ldc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSE200_H */

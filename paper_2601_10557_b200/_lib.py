@@ -1,0 +1,154 @@
+"""ctypes binding of the bse200 C ABI (include/bse200.h).
+
+This is the only door to the GPU: every numerical step of the solve goes
+through ``libbse200.so``.  There is no CPU fallback — if the library or a CUDA
+device is missing, every entry point raises ``RuntimeError`` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+from pathlib import Path
+
+from .errors import (
+    HermitianRqError,
+    IndefiniteError,
+    LanczosBreakdownError,
+    NumericalError,
+    RankDeficiencyError,
+    ValidationError,
+)
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("BSE200_LIB", _HERE / "libbse200.so"))
+
+_i64 = C.c_int64
+_vp = C.c_void_p
+_dbl = C.c_double
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+# name -> (restype, argtypes); mirrors include/bse200.h
+_SIGS = {
+    "bse_version": (C.c_char_p, []),
+    "bse_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "bse_ctx_destroy": (None, [_vp]),
+    "bse_set_stream": (C.c_int, [_vp, _vp]),
+    "bse_last_error": (C.c_char_p, [_vp]),
+    "bse_launch_count": (_i64, [_vp]),
+    "bse_apply_h": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _dbl]),
+    "bse_filter_step": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _dbl]),
+    "bse_chebyshev_filter": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
+    "bse_residuals": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _dp]),
+    "bse_s_orthonormalize": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
+    "bse_cholqr": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _ip]),
+    "bse_fix_phases": (C.c_int, [_vp, _vp, _i64, _i64, _i64]),
+    "bse_rr_hermitian": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
+    "bse_rr_backup": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
+    "bse_lanczos_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _dp, _dp, _ip]),
+    "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
+    "bse_complex_normals": (C.c_int, [_vp, _vp, C.c_uint64, _i64, _i64]),
+    "bse_complex_normals_t": (C.c_int, [_vp, _vp, C.c_uint64, _i64, _i64]),
+    "bse_symmetrize": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int]),
+    "bse_scale_shift": (C.c_int, [_vp, _vp, _i64, _i64, _dbl, _dbl, C.c_int]),
+    "bse_eigvalsh": (C.c_int, [_vp, _vp, _i64, _i64, _dp]),
+    "bse_zgemm_cn": (C.c_int, [_vp, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64]),
+    "bse_zgemm_nn": (C.c_int, [_vp, _i64, _i64, _i64, _dbl, _vp, _i64, _vp, _i64, _dbl, _vp, _i64]),
+}
+
+# status codes (bse200.h) -> exception classes of the reference (errors.py:8-38)
+_STATUS = {
+    1: ValidationError,
+    2: NumericalError,
+    3: IndefiniteError,
+    4: RankDeficiencyError,
+    5: LanczosBreakdownError,
+    6: HermitianRqError,
+    7: NumericalError,
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load() -> C.CDLL:
+    """Load libbse200.so (raises if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"bse200 CUDA library not found at {LIB_PATH}; run `python __graft_entry__.py build` "
+                    "(no CPU fallback exists)"
+                )
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+class Context:
+    """One bse_ctx per CUDA device (cuBLAS/cuSOLVER handles + workspace)."""
+
+    _by_device: dict[int, "Context"] = {}
+
+    def __init__(self, device: int):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("bse200 needs a CUDA device (B200, sm_100a); none is visible — no CPU fallback")
+        self.lib = load()
+        self.device = device
+        h = _vp()
+        st = self.lib.bse_ctx_create(device, C.byref(h))
+        if st != 0:
+            raise RuntimeError(f"bse_ctx_create failed with status {st}")
+        self.handle = h
+        self._stream = None
+
+    @classmethod
+    def get(cls, device: int) -> "Context":
+        ctx = cls._by_device.get(device)
+        if ctx is None:
+            ctx = cls(device)
+            cls._by_device[device] = ctx
+        return ctx
+
+    def bind_stream(self) -> None:
+        """Enqueue on torch's current stream of this device."""
+        import torch
+
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if s != self._stream:
+            self.check(self.lib.bse_set_stream(self.handle, _vp(s)))
+            self._stream = s
+
+    def check(self, status: int) -> None:
+        if status != 0:
+            msg = self.lib.bse_last_error(self.handle).decode(errors="replace")
+            raise _STATUS.get(status, NumericalError)(msg)
+
+    def call(self, name: str, *args) -> None:
+        self.bind_stream()
+        self.check(getattr(self.lib, name)(self.handle, *args))
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.bse_launch_count(self.handle))
+
+
+def dptr(t) -> _vp:
+    return _vp(t.data_ptr())
+
+
+def hptr(a) -> _dp:
+    return a.ctypes.data_as(_dp)

@@ -1,0 +1,929 @@
+// bse200: C ABI of the B200-native pseudo-hermitian ChASE hot path.
+// See include/bse200.h for the contract and DESIGN.md for the data layout.
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bse200.h"
+#include "aux.cuh"
+#include "hop.cuh"
+#include "zgemm.cuh"
+
+using bse::zval;
+
+// ----------------------------------------------------------------------------
+// context, errors, workspace
+// ----------------------------------------------------------------------------
+struct bse_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  cusolverDnParams_t params = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  void* ws = nullptr;  // general device scratch
+  size_t ws_bytes = 0;
+  void* hws = nullptr;  // host scratch (cuSOLVER 64-bit API)
+  size_t hws_bytes = 0;
+  double* pinned = nullptr;  // pinned host staging (small results)
+  size_t pinned_count = 0;
+};
+
+namespace {
+
+struct BseError : std::runtime_error {
+  int code;
+  BseError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(x)                                                                                    \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess)                                                                            \
+      throw BseError(BSE_ECUDA, std::string("CUDA error ") + cudaGetErrorString(e_) + " at " #x);     \
+  } while (0)
+#define BLAS_OK(x)                                                                                    \
+  do {                                                                                                \
+    cublasStatus_t s_ = (x);                                                                          \
+    if (s_ != CUBLAS_STATUS_SUCCESS) throw BseError(BSE_ECUDA, "cuBLAS status " + std::to_string(s_) + " at " #x); \
+  } while (0)
+#define SOLVER_OK(x)                                                                                  \
+  do {                                                                                                \
+    cusolverStatus_t s_ = (x);                                                                        \
+    if (s_ != CUSOLVER_STATUS_SUCCESS)                                                                \
+      throw BseError(BSE_ECUDA, "cuSOLVER status " + std::to_string(s_) + " at " #x);                 \
+  } while (0)
+
+void check_launch(bse_ctx* ctx) {
+  ctx->launches++;
+  CUDA_OK(cudaGetLastError());
+}
+
+template <class F>
+int guarded(bse_ctx* ctx, F&& f) {
+  if (!ctx) return BSE_EVALIDATION;
+  try {
+    CUDA_OK(cudaSetDevice(ctx->device));
+    f();
+    ctx->err.clear();
+    return BSE_OK;
+  } catch (const BseError& e) {
+    ctx->err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return BSE_ECUDA;
+  }
+}
+
+// Bump allocator over the context workspace.  ensure() must be called with the
+// call's total need before any carve (it may reallocate, which synchronises).
+struct Scratch {
+  bse_ctx* ctx;
+  size_t off = 0;
+  explicit Scratch(bse_ctx* c, size_t total) : ctx(c) {
+    total += 4096;
+    if (ctx->ws_bytes < total) {
+      if (ctx->ws) {
+        CUDA_OK(cudaStreamSynchronize(ctx->stream));
+        CUDA_OK(cudaFree(ctx->ws));
+      }
+      const size_t want = std::max(total, ctx->ws_bytes * 3 / 2);
+      ctx->ws = nullptr;
+      ctx->ws_bytes = 0;
+      CUDA_OK(cudaMalloc(&ctx->ws, want));
+      ctx->ws_bytes = want;
+    }
+  }
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = reinterpret_cast<T*>(static_cast<char*>(ctx->ws) + off);
+    off += count * sizeof(T);
+    if (off > ctx->ws_bytes) throw BseError(BSE_ECUDA, "internal: workspace overrun");
+    return p;
+  }
+};
+
+inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+
+double* pinned(bse_ctx* ctx, size_t count) {
+  if (ctx->pinned_count < count) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    CUDA_OK(cudaMallocHost(&ctx->pinned, count * sizeof(double)));
+    ctx->pinned_count = count;
+  }
+  return ctx->pinned;
+}
+
+void* host_ws(bse_ctx* ctx, size_t bytes) {
+  if (ctx->hws_bytes < bytes) {
+    free(ctx->hws);
+    ctx->hws = malloc(bytes);
+    ctx->hws_bytes = bytes;
+  }
+  return ctx->hws;
+}
+
+inline int grid1d(int64_t n, int threads = 256, int cap = 148 * 16) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, cap));
+}
+
+// ----------------------------------------------------------------------------
+// H operator launches
+// ----------------------------------------------------------------------------
+// Tile configuration of the fused H-operator GEMM:
+// CTA 64 x 32 complex (up and low halves), 8 warps of 16 x 16, BK = 8, 4 stages.
+using HopMain = bse::HopCfg<64, 32, 8, 2, 2, 4, 2>;
+
+template <class C, int EPI>
+void launch_hop(bse_ctx* ctx, const bse::HopArgs& a) {
+  static bool configured = false;
+  if (!configured) {
+    CUDA_OK(cudaFuncSetAttribute(bse::hop_kernel<C, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    configured = true;
+  }
+  dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
+  bse::hop_kernel<C, EPI><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  check_launch(ctx);
+}
+
+bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, int64_t k) {
+  bse::HopArgs a{};
+  const zval* ab = static_cast<const zval*>(d_ab);
+  a.pa = ab;
+  a.pb = ab + m * lda;
+  a.lda = lda;
+  a.mr = (int)m;
+  a.kc = (int)m;
+  a.x1 = x;
+  a.x2 = x + m;
+  a.ldx = ldx;
+  a.k = (int)k;
+  a.alpha = 1.0;
+  a.beta = 0.0;
+  a.shift = 0.0;
+  a.low_sign = 1.0;
+  return a;
+}
+
+void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, zval* y, int64_t ldy,
+             int64_t k, double low_sign) {
+  if (k == 0 || m == 0) return;
+  bse::HopArgs a = hop_args_single(d_ab, lda, m, x, ldx, k);
+  a.y1 = y;
+  a.y2 = y + m;
+  a.ldy = ldy;
+  a.low_sign = low_sign;
+  launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+}
+
+void filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* y, const zval* yprev,
+                 zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
+  bse::HopArgs a = hop_args_single(d_ab, lda, m, y, ld, k);
+  a.y1 = ynext;
+  a.y2 = ynext + m;
+  a.ldy = ld;
+  a.s1 = y;
+  a.s2 = y + m;
+  a.lds = ld;
+  a.shift = c;
+  a.alpha = alpha;
+  a.beta = beta;
+  if (beta != 0.0) {
+    a.p1 = yprev;
+    a.p2 = yprev + m;
+    a.ldp = ld;
+  }
+  launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+}
+
+// residual norms into d_out (k doubles, device)
+void residual_norms(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* v, int64_t ldv, int64_t k,
+                    const double* d_lam, double* d_part, double* d_out) {
+  bse::HopArgs a = hop_args_single(d_ab, lda, m, v, ldv, k);
+  a.s1 = v;
+  a.s2 = v + m;
+  a.lds = ldv;
+  a.lam = d_lam;
+  a.partial = d_part;
+  launch_hop<HopMain, bse::HOP_RESID>(ctx, a);
+  const int nb = (int)((m + HopMain::BM - 1) / HopMain::BM);
+  bse::resid_finalize_kernel<<<(int)((k + 127) / 128), 128, 0, ctx->stream>>>(d_part, nb, (int)k, d_out);
+  check_launch(ctx);
+}
+
+size_t resid_part_count(int64_t m, int64_t k) { return (size_t)((m + HopMain::BM - 1) / HopMain::BM) * k; }
+
+// ----------------------------------------------------------------------------
+// GEMMs
+// ----------------------------------------------------------------------------
+using GemmMain = bse::GemmCfg<64, 64, 8, 4, 2, 4>;
+
+int splitk_for(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ((M + GemmMain::BM - 1) / GemmMain::BM) * ((N + GemmMain::BN - 1) / GemmMain::BN);
+  const int64_t want = 148 * 2;
+  if (tiles >= want) return 1;
+  int64_t s = (want + tiles - 1) / tiles;
+  const int64_t kt = (K + GemmMain::BK - 1) / GemmMain::BK;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, kt / 16));  // keep >= 16 k-tiles per split
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+}
+
+size_t gemm_ws_bytes(int64_t M, int64_t N, int64_t K) {
+  const int s = splitk_for(M, N, K);
+  return s > 1 ? al((size_t)s * M * N * sizeof(zval)) : 0;
+}
+
+template <int OPA>
+void zgemm(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const zval* a, int64_t lda, const zval* b,
+           int64_t ldb, double beta, zval* c, int64_t ldc, zval* ws) {
+  if (M == 0 || N == 0) return;
+  using C = GemmMain;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_OK(cudaFuncSetAttribute(bse::zgemm_kernel<C, OPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    configured = true;
+  }
+  bse::GemmArgs g{};
+  g.a = a;
+  g.lda = lda;
+  g.b = b;
+  g.ldb = ldb;
+  g.c = c;
+  g.ldc = ldc;
+  g.M = (int)M;
+  g.N = (int)N;
+  g.K = (int)K;
+  g.alpha = alpha;
+  g.beta = beta;
+  const int splits = (K == 0) ? 1 : splitk_for(M, N, K);
+  g.ws = ws;
+  if (splits > 1 && !ws) throw BseError(BSE_ECUDA, "internal: split-K workspace missing");
+  dim3 grid((unsigned)((M + C::BM - 1) / C::BM), (unsigned)((N + C::BN - 1) / C::BN), (unsigned)splits);
+  bse::zgemm_kernel<C, OPA><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(g);
+  check_launch(ctx);
+  if (splits > 1) {
+    bse::zgemm_splitk_reduce<<<grid1d(M * N), 256, 0, ctx->stream>>>(ws, splits, c, ldc, (int)M, (int)N, alpha, beta);
+    check_launch(ctx);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// small dense pieces (k x k) on device: cuSOLVER / cuBLAS
+// ----------------------------------------------------------------------------
+const cuDoubleComplex* cz(const zval* p) { return reinterpret_cast<const cuDoubleComplex*>(p); }
+cuDoubleComplex* cz(zval* p) { return reinterpret_cast<cuDoubleComplex*>(p); }
+
+// Cholesky in place (uplo), returns info (0 ok, >0 not positive definite)
+int potrf(bse_ctx* ctx, zval* a, int k, cublasFillMode_t uplo, int* d_info) {
+  size_t dws = 0, hws = 0;
+  SOLVER_OK(cusolverDnXpotrf_bufferSize(ctx->solver, ctx->params, uplo, k, CUDA_C_64F, a, k, CUDA_C_64F, &dws, &hws));
+  void* dbuf = nullptr;
+  CUDA_OK(cudaMallocAsync(&dbuf, std::max<size_t>(dws, 16), ctx->stream));
+  void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
+  SOLVER_OK(cusolverDnXpotrf(ctx->solver, ctx->params, uplo, k, CUDA_C_64F, a, k, CUDA_C_64F, dbuf, dws, hbuf, hws, d_info));
+  int info = 0;
+  CUDA_OK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaFreeAsync(dbuf, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  return info;
+}
+
+// hermitian eigendecomposition (values ascending in d_w; vectors overwrite a when want_vec)
+void heevd(bse_ctx* ctx, zval* a, int k, double* d_w, bool want_vec, int* d_info) {
+  const cusolverEigMode_t jobz = want_vec ? CUSOLVER_EIG_MODE_VECTOR : CUSOLVER_EIG_MODE_NOVECTOR;
+  size_t dws = 0, hws = 0;
+  SOLVER_OK(cusolverDnXsyevd_bufferSize(ctx->solver, ctx->params, jobz, CUBLAS_FILL_MODE_LOWER, k, CUDA_C_64F, a, k,
+                                        CUDA_R_64F, d_w, CUDA_C_64F, &dws, &hws));
+  void* dbuf = nullptr;
+  CUDA_OK(cudaMallocAsync(&dbuf, std::max<size_t>(dws, 16), ctx->stream));
+  void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
+  SOLVER_OK(cusolverDnXsyevd(ctx->solver, ctx->params, jobz, CUBLAS_FILL_MODE_LOWER, k, CUDA_C_64F, a, k, CUDA_R_64F,
+                             d_w, CUDA_C_64F, dbuf, dws, hbuf, hws, d_info));
+  int info = 0;
+  CUDA_OK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaFreeAsync(dbuf, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  if (info != 0) throw BseError(BSE_ENUMERICAL, "hermitian eigensolver failed (info " + std::to_string(info) + ")");
+}
+
+void to_host(bse_ctx* ctx, double* h, const double* d, size_t count) {
+  double* p = pinned(ctx, count);
+  CUDA_OK(cudaMemcpyAsync(p, d, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(h, p, count * sizeof(double));
+}
+
+void to_device(bse_ctx* ctx, double* d, const double* h, size_t count) {
+  double* p = pinned(ctx, count);
+  std::memcpy(p, h, count * sizeof(double));
+  CUDA_OK(cudaMemcpyAsync(d, p, count * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+}
+
+// max |G - I| of a k x k device matrix -> host
+double defect_to_host(bse_ctx* ctx, const zval* g, int k, double* d_part) {
+  const int nb = grid1d((int64_t)k * k, 256, 256);
+  bse::defect_partial_kernel<<<nb, 256, 0, ctx->stream>>>(g, k, d_part);
+  check_launch(ctx);
+  bse::max_reduce_kernel<<<1, 32, 0, ctx->stream>>>(d_part, nb, d_part + nb);
+  check_launch(ctx);
+  double h = 0.0;
+  to_host(ctx, &h, d_part + nb, 1);
+  return h;
+}
+
+// ----------------------------------------------------------------------------
+// CholQR (ortho.py:96-129), shifted CholQR3 fallback
+// ----------------------------------------------------------------------------
+// One CholQR pass on q (n x k) in place: G = Q^H Q (+ shift I), R = chol(G)
+// (upper), Q <- Q R^{-1} with R^{-1} from a k x k TRSM and the product on the
+// DMMA GEMM.  gram needs 2 k x k, tmp n x k.  Returns false when the Cholesky
+// factorisation fails (ortho.py:113-119).
+bool cholqr_pass(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, zval* gram, zval* tmp, zval* gws,
+                 int* d_info, double shift, double* d_rdiag) {
+  zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
+  bse::hermitize_kernel<<<grid1d(k * k), 256, 0, ctx->stream>>>(gram, (int)k);
+  check_launch(ctx);
+  if (shift != 0.0) {
+    bse::add_diag_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(gram, (int)k, shift);
+    check_launch(ctx);
+  }
+  const int info = potrf(ctx, gram, (int)k, CUBLAS_FILL_MODE_UPPER, d_info);
+  if (info != 0) return false;
+  if (d_rdiag) {
+    bse::absdiag_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(gram, (int)k, d_rdiag);
+    check_launch(ctx);
+  }
+  zval* rinv = gram + k * k;
+  bse::set_identity_kernel<<<grid1d(k * k), 256, 0, ctx->stream>>>(rinv, (int)k);
+  check_launch(ctx);
+  const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
+  BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
+                      (int)k, &z1, cz(gram), (int)k, cz(rinv), (int)k));
+  CUDA_OK(cudaMemcpy2DAsync(tmp, sizeof(zval) * n, q, sizeof(zval) * ldq, sizeof(zval) * n, (size_t)k,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, tmp, n, rinv, k, 0.0, q, ldq, gws);
+  return true;
+}
+
+size_t cholqr_ws_bytes(int64_t n, int64_t k) {
+  return al(2 * k * k * sizeof(zval)) + 2 * al(n * k * sizeof(zval)) +
+         al(std::max(gemm_ws_bytes(k, k, n), gemm_ws_bytes(n, k, k)) + sizeof(zval)) + al(1024 * 8) + al(k * 8) +
+         al(64) + 4096;
+}
+
+// ortho.py:96-129 on device.  Returns method (0 cholqr2, 1 shifted fallback);
+// throws BSE_ERANK when no path yields a full-rank factor.
+int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scratch& sc) {
+  if (k > n) throw BseError(BSE_ERANK, "cannot orthonormalize " + std::to_string(k) + " columns in dimension " +
+                                           std::to_string(n));
+  zval* gram = sc.take<zval>(2 * k * k);
+  zval* tmp = sc.take<zval>(n * k);
+  zval* gws = sc.take<zval>(std::max(gemm_ws_bytes(k, k, n), gemm_ws_bytes(n, k, k)) / sizeof(zval) + 1);
+  double* dpart = sc.take<double>(1024);
+  double* rdiag = sc.take<double>(k);
+  int* d_info = sc.take<int>(4);
+  // keep the input for the fallback (ortho.py:126 restarts from x)
+  bool ok = true;
+  zval* x0 = sc.take<zval>(n * k);
+  CUDA_OK(cudaMemcpy2DAsync(x0, sizeof(zval) * n, q, sizeof(zval) * ldq, sizeof(zval) * n, (size_t)k,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  for (int pass = 0; pass < 2 && ok; ++pass) ok = cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, 0.0, nullptr);
+  if (ok) {
+    zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
+    const double defect = defect_to_host(ctx, gram, (int)k, dpart);
+    if (defect <= 1e-8) return 0;  // ortho.py:124-126 (NaN fails the test)
+  }
+  // Shifted CholeskyQR3 (Fukaya et al.): shift = 11 (n k + k (k + 1)) u ||X||_F^2, then CholQR2.
+  CUDA_OK(cudaMemcpy2DAsync(q, sizeof(zval) * ldq, x0, sizeof(zval) * n, sizeof(zval) * n, (size_t)k,
+                            cudaMemcpyDeviceToDevice, ctx->stream));
+  bse::frob2_kernel<<<(int)k, 256, 0, ctx->stream>>>(q, ldq, n, rdiag);
+  check_launch(ctx);
+  std::vector<double> f2(k);
+  to_host(ctx, f2.data(), rdiag, k);
+  double fro2 = 0.0;
+  for (double v : f2) fro2 += v;
+  const double u = std::ldexp(1.0, -53);
+  const double shift = 11.0 * ((double)n * k + (double)k * (k + 1)) * u * fro2;
+  if (!(fro2 > 0.0) || !cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, shift, rdiag))
+    throw BseError(BSE_ERANK, "columns are numerically rank deficient (shifted Cholesky failed)");
+  // rank test on the shifted factor (mirrors ortho.py:86-93: min|diag R| <= 1e-10 max|diag R|)
+  std::vector<double> rd(k);
+  to_host(ctx, rd.data(), rdiag, k);
+  const double dmax = *std::max_element(rd.begin(), rd.end()), dmin = *std::min_element(rd.begin(), rd.end());
+  if (dmax == 0.0 || dmin <= 1e-10 * dmax || !(dmin == dmin))
+    throw BseError(BSE_ERANK, "columns are numerically rank deficient (diag ratio " + std::to_string(dmin) + " / " +
+                                  std::to_string(dmax) + ")");
+  for (int pass = 0; pass < 2; ++pass)
+    if (!cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, 0.0, nullptr))
+      throw BseError(BSE_ERANK, "columns are numerically rank deficient (CholQR after shift failed)");
+  zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
+  const double defect = defect_to_host(ctx, gram, (int)k, dpart);
+  if (!(defect <= 1e-8)) throw BseError(BSE_ERANK, "orthonormalization failed (defect " + std::to_string(defect) + ")");
+  return 1;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* bse_version(void) { return "bse200 0.1 (sm_100a, FP64 DMMA)"; }
+
+int bse_ctx_create(int device, bse_ctx** out) {
+  if (!out) return BSE_EVALIDATION;
+  *out = nullptr;
+  bse_ctx* ctx = new bse_ctx();
+  ctx->device = device;
+  try {
+    CUDA_OK(cudaSetDevice(device));
+    BLAS_OK(cublasCreate(&ctx->blas));
+    SOLVER_OK(cusolverDnCreate(&ctx->solver));
+    SOLVER_OK(cusolverDnCreateParams(&ctx->params));
+  } catch (const BseError& e) {
+    delete ctx;
+    return e.code;
+  }
+  *out = ctx;
+  return BSE_OK;
+}
+
+void bse_ctx_destroy(bse_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  free(ctx->hws);
+  if (ctx->params) cusolverDnDestroyParams(ctx->params);
+  if (ctx->solver) cusolverDnDestroy(ctx->solver);
+  if (ctx->blas) cublasDestroy(ctx->blas);
+  delete ctx;
+}
+
+int bse_set_stream(bse_ctx* ctx, void* stream) {
+  return guarded(ctx, [&] {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    BLAS_OK(cublasSetStream(ctx->blas, ctx->stream));
+    SOLVER_OK(cusolverDnSetStream(ctx->solver, ctx->stream));
+  });
+}
+
+const char* bse_last_error(const bse_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int64_t bse_launch_count(const bse_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int bse_apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_x, int64_t ldx, void* d_y,
+                int64_t ldy, int64_t k, double low_sign) {
+  return guarded(ctx, [&] {
+    if (m < 0 || k < 0 || lda < m || ldx < 2 * m || ldy < 2 * m) throw BseError(BSE_EVALIDATION, "bad shapes");
+    apply_h(ctx, d_ab, lda, m, static_cast<const zval*>(d_x), ldx, static_cast<zval*>(d_y), ldy, k, low_sign);
+  });
+}
+
+int bse_filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_y, const void* d_yprev,
+                    void* d_ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
+  return guarded(ctx, [&] {
+    if (m < 0 || k < 0 || lda < m || ld < 2 * m) throw BseError(BSE_EVALIDATION, "bad shapes");
+    if (k == 0 || m == 0) return;
+    filter_step(ctx, d_ab, lda, m, static_cast<const zval*>(d_y), static_cast<const zval*>(d_yprev),
+                static_cast<zval*>(d_ynext), ld, k, c, alpha, beta);
+  });
+}
+
+int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_v, int64_t ld, int64_t k,
+                         int deg, double c, double e, double s, void* d_work) {
+  return guarded(ctx, [&] {
+    if (deg < 2 || deg % 2) throw BseError(BSE_EVALIDATION, "filter degree must be even and >= 2");
+    if (!(e > 0)) throw BseError(BSE_EVALIDATION, "filter half width must be positive");
+    if (m < 0 || k < 0 || lda < m || ld < 2 * m) throw BseError(BSE_EVALIDATION, "bad shapes");
+    if (k == 0 || m == 0) return;
+    // chebyshev.py:58-74 with three rotating buffers {v, w0, w1}
+    zval* bufs[3] = {static_cast<zval*>(d_v), static_cast<zval*>(d_work), static_cast<zval*>(d_work) + ld * k};
+    const double sigma1 = e / (s - c);
+    double sigma = sigma1;
+    int prev = 0, cur = 1;
+    filter_step(ctx, d_ab, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0);
+    for (int step = 2; step <= deg; ++step) {
+      const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
+      const int nxt = 3 - prev - cur;
+      // y_next = (2 s'/e)(H y - c y) - (s s') y_prev ; written over the free buffer
+      filter_step(ctx, d_ab, lda, m, bufs[cur], bufs[prev], bufs[nxt], ld, k, c, 2.0 * sigma_new / e,
+                  sigma * sigma_new);
+      prev = cur;
+      cur = nxt;
+      sigma = sigma_new;
+    }
+    if (cur != 0)
+      CUDA_OK(cudaMemcpyAsync(bufs[0], bufs[cur], sizeof(zval) * ld * k, cudaMemcpyDeviceToDevice, ctx->stream));
+  });
+}
+
+int bse_residuals(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_v, int64_t ldv, int64_t k,
+                  const double* h_lam, double* h_res) {
+  return guarded(ctx, [&] {
+    if (k == 0) return;
+    Scratch sc(ctx, al(k * 8) * 2 + al(resid_part_count(m, k) * 8));
+    double* d_lam = sc.take<double>(k);
+    double* d_out = sc.take<double>(k);
+    double* d_part = sc.take<double>(resid_part_count(m, k));
+    to_device(ctx, d_lam, h_lam, k);
+    residual_norms(ctx, d_ab, lda, m, static_cast<const zval*>(d_v), ldv, k, d_lam, d_part, d_out);
+    to_host(ctx, h_res, d_out, k);
+  });
+}
+
+int bse_zgemm_cn(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const void* d_a, int64_t lda,
+                 const void* d_b, int64_t ldb, double beta, void* d_c, int64_t ldc) {
+  return guarded(ctx, [&] {
+    Scratch sc(ctx, gemm_ws_bytes(M, N, K));
+    zval* ws = gemm_ws_bytes(M, N, K) ? sc.take<zval>((size_t)splitk_for(M, N, K) * M * N) : nullptr;
+    zgemm<bse::OPA_C>(ctx, M, N, K, alpha, static_cast<const zval*>(d_a), lda, static_cast<const zval*>(d_b), ldb,
+                      beta, static_cast<zval*>(d_c), ldc, ws);
+  });
+}
+
+int bse_zgemm_nn(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const void* d_a, int64_t lda,
+                 const void* d_b, int64_t ldb, double beta, void* d_c, int64_t ldc) {
+  return guarded(ctx, [&] {
+    Scratch sc(ctx, gemm_ws_bytes(M, N, K));
+    zval* ws = gemm_ws_bytes(M, N, K) ? sc.take<zval>((size_t)splitk_for(M, N, K) * M * N) : nullptr;
+    zgemm<bse::OPA_N>(ctx, M, N, K, alpha, static_cast<const zval*>(d_a), lda, static_cast<const zval*>(d_b), ldb,
+                      beta, static_cast<zval*>(d_c), ldc, ws);
+  });
+}
+
+int bse_cholqr(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq, int* h_method) {
+  return guarded(ctx, [&] {
+    if (k == 0) {
+      if (h_method) *h_method = 0;
+      return;
+    }
+    Scratch sc(ctx, cholqr_ws_bytes(n, k));
+    zval* q = static_cast<zval*>(d_q);
+    const int method = cholqr_device(ctx, q, n, k, ldq, sc);
+    bse::phase_fix_kernel<<<(int)k, 256, 0, ctx->stream>>>(q, ldq, n);
+    check_launch(ctx);
+    if (h_method) *h_method = method;
+  });
+}
+
+int bse_fix_phases(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq) {
+  return guarded(ctx, [&] {
+    if (k == 0 || n == 0) return;
+    bse::phase_fix_kernel<<<(int)k, 256, 0, ctx->stream>>>(static_cast<zval*>(d_q), ldq, n);
+    check_launch(ctx);
+  });
+}
+
+int bse_s_orthonormalize(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t ldv, const void* d_ylocked,
+                         int64_t l, int64_t ldy, int* h_method) {
+  return guarded(ctx, [&] {
+    if (n % 2) throw BseError(BSE_EVALIDATION, "S needs an even row count");
+    if (k == 0) {
+      if (h_method) *h_method = 0;
+      return;
+    }
+    zval* v = static_cast<zval*>(d_v);
+    const int64_t m = n / 2;
+    size_t need = cholqr_ws_bytes(n, std::max(k, l));
+    if (l > 0) need += al(n * l * sizeof(zval)) + al(l * k * sizeof(zval)) + gemm_ws_bytes(l, k, n) + gemm_ws_bytes(n, k, l);
+    Scratch sc(ctx, need);
+    if (l > 0) {
+      // ortho.py:148-155: orthonormal basis of span(S Y_locked), then v -= basis (basis^H v)
+      zval* basis = sc.take<zval>(n * l);
+      zval* proj = sc.take<zval>(l * k);
+      zval* gws = sc.take<zval>(std::max(gemm_ws_bytes(l, k, n), gemm_ws_bytes(n, k, l)) / sizeof(zval) + 1);
+      bse::sflip_copy_kernel<<<grid1d(n * l), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ylocked), ldy, basis,
+                                                                       n, m, l);
+      check_launch(ctx);
+      {
+        Scratch inner = sc;  // carve the basis CholQR scratch after ours
+        cholqr_device(ctx, basis, n, l, n, inner);
+      }
+      zgemm<bse::OPA_C>(ctx, l, k, n, 1.0, basis, n, v, ldv, 0.0, proj, l, gws);
+      zgemm<bse::OPA_N>(ctx, n, k, l, -1.0, basis, n, proj, l, 1.0, v, ldv, gws);
+    }
+    Scratch rest = sc;
+    const int method = cholqr_device(ctx, v, n, k, ldv, rest);
+    bse::phase_fix_kernel<<<(int)k, 256, 0, ctx->stream>>>(v, ldv, n);
+    check_launch(ctx);
+    if (h_method) *h_method = method;
+  });
+}
+
+int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
+                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
+  return guarded(ctx, [&] {
+    if (k == 0) return;
+    const int64_t n = 2 * m;
+    const zval* q = static_cast<const zval*>(d_q);
+    zval* vout = static_cast<zval*>(d_vout);
+    const size_t kk = (size_t)k * k;
+    Scratch sc(ctx, al(n * k * sizeof(zval)) + 5 * al(kk * sizeof(zval)) + 2 * al(k * 8) + al(k * 4) + al(64) +
+                        std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)}) + 4096);
+    zval* t = sc.take<zval>(n * k);
+    zval* w = sc.take<zval>(kk);
+    zval* mm = sc.take<zval>(kk);
+    zval* tmp = sc.take<zval>(kk);
+    zval* g = sc.take<zval>(kk);
+    zval* wperm = sc.take<zval>(kk);
+    double* d_w = sc.take<double>(k);
+    double* d_norm = sc.take<double>(k);
+    int* d_perm = sc.take<int>(k);
+    int* d_info = sc.take<int>(4);
+    zval* gws = sc.take<zval>(std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)}) /
+                                  sizeof(zval) + 1);
+    // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T (hermitised) ; M = I - 2 Q2^H Q2 (hermitised)
+    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0);
+    zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
+    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(w, (int)k);
+    check_launch(ctx);
+    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, tmp, k, gws);
+    bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(tmp, mm, (int)k);
+    check_launch(ctx);
+    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
+    check_launch(ctx);
+    // :116-120  |lambda|_min(M) >= 1e-8
+    CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+    heevd(ctx, tmp, (int)k, d_w, false, d_info);
+    std::vector<double> hw(k);
+    to_host(ctx, hw.data(), d_w, k);
+    double lmm = INFINITY;
+    for (double v : hw) lmm = std::min(lmm, std::fabs(v));
+    if (h_lam_min_m) *h_lam_min_m = lmm;
+    if (!(lmm >= 1e-8))
+      throw BseError(BSE_EHERMITIAN_RQ, "|lambda_min(Q*SQ)| = " + std::to_string(lmm) + " below 1e-8");
+    // :121-126  L = chol(W)
+    if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0)
+      throw BseError(BSE_EHERMITIAN_RQ, "Cholesky of Q*SHQ failed; S*H is not definite on the subspace");
+    // :127-129  G = L^{-1} M L^{-H}, hermitised
+    const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
+    CUDA_OK(cudaMemcpyAsync(g, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
+                        (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
+    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, (int)k,
+                        (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
+    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k);
+    check_launch(ctx);
+    // :130-133  theta, y = eigh(G); lambda = 1/theta
+    heevd(ctx, g, (int)k, d_w, true, d_info);
+    to_host(ctx, hw.data(), d_w, k);
+    double tmin = INFINITY;
+    for (double v : hw) tmin = std::min(tmin, std::fabs(v));
+    if (tmin < 2.220446049250313e-16) throw BseError(BSE_EHERMITIAN_RQ, "reduced spectrum touches zero; cannot invert");
+    std::vector<double> lam(k);
+    for (int64_t i = 0; i < k; ++i) lam[i] = 1.0 / hw[i];
+    std::vector<int> order(k);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lam[a] < lam[b]; });
+    for (int64_t i = 0; i < k; ++i) h_lam[i] = lam[order[i]];
+    // :134-137  w = L^{-H} y ; V = Q w (sorted) ; unit columns
+    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, (int)k,
+                        (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
+    {
+      std::vector<double> tmpd((k + 1) / 2 + 1);
+      static_assert(sizeof(int) * 2 == sizeof(double), "packing");
+      std::memcpy(tmpd.data(), order.data(), sizeof(int) * k);
+      to_device(ctx, reinterpret_cast<double*>(d_perm), tmpd.data(), (k + 1) / 2);
+    }
+    bse::gather_cols_kernel<<<dim3(1, (unsigned)k), 256, 0, ctx->stream>>>(g, k, wperm, k, k, d_perm);
+    check_launch(ctx);
+    zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, q, ldq, wperm, k, 0.0, vout, ldvout, gws);
+    bse::colnorm_kernel<<<(int)k, 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
+    check_launch(ctx);
+    bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
+    check_launch(ctx);
+  });
+}
+
+int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
+                  double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
+  return guarded(ctx, [&] {
+    if (k == 0) return;
+    const int64_t n = 2 * m;
+    const zval* q = static_cast<const zval*>(d_q);
+    zval* vout = static_cast<zval*>(d_vout);
+    const size_t kk = (size_t)k * k;
+    const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k),
+                                  gemm_ws_bytes(k, k, k)});
+    Scratch sc(ctx, al(n * k * sizeof(zval)) + 6 * al(kk * sizeof(zval)) + 3 * al(k * 16) + al(k * 4) + al(64) + gwsb +
+                        4096);
+    zval* t = sc.take<zval>(n * k);
+    zval* w = sc.take<zval>(kk);
+    zval* mm = sc.take<zval>(kk);
+    zval* tmp = sc.take<zval>(kk);
+    zval* g = sc.take<zval>(kk);
+    zval* y = sc.take<zval>(kk);
+    zval* yperm = sc.take<zval>(kk);
+    zval* d_ev = sc.take<zval>(k);
+    double* d_w = sc.take<double>(k);
+    double* d_d = sc.take<double>(k);
+    int* d_perm = sc.take<int>(k);
+    int* d_info = sc.take<int>(4);
+    zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
+    // rayleigh_ritz.py:160-168
+    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, 1.0);
+    zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
+    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, tmp, k, gws);
+    bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(tmp, mm, (int)k);
+    check_launch(ctx);
+    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
+    check_launch(ctx);
+    CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+    heevd(ctx, tmp, (int)k, d_w, false, d_info);
+    std::vector<double> hw(k);
+    to_host(ctx, hw.data(), d_w, k);
+    double lmm = INFINITY;
+    for (double v : hw) lmm = std::min(lmm, std::fabs(v));
+    if (h_lam_min_m) *h_lam_min_m = lmm;
+    bse::diag_real_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(mm, (int)k, 1e-12, d_d);
+    check_launch(ctx);
+    bse::offdiag_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, tmp, (int)k);
+    check_launch(ctx);
+    // g0 = Q^H (S T) = Q1^H T1 - Q2^H T2
+    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q, ldq, t, n, 0.0, g, k, gws);
+    zgemm<bse::OPA_C>(ctx, k, k, m, -1.0, q + m, ldq, t + m, n, 1.0, g, k, gws);
+    // g = (g0 - off W) / d
+    zgemm<bse::OPA_N>(ctx, k, k, k, -1.0, tmp, k, w, k, 1.0, g, k, gws);
+    bse::rowscale_inv_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k, d_d);
+    check_launch(ctx);
+    // direct.py:102-116: general eigensolver, ascending real parts (stable)
+    size_t dws = 0, hws = 0;
+    SOLVER_OK(cusolverDnXgeev_bufferSize(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR,
+                                         CUSOLVER_EIG_MODE_VECTOR, k, CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F,
+                                         nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F, &dws, &hws));
+    void* dbuf = nullptr;
+    CUDA_OK(cudaMallocAsync(&dbuf, std::max<size_t>(dws, 16), ctx->stream));
+    void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
+    SOLVER_OK(cusolverDnXgeev(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, k,
+                              CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F, nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F,
+                              dbuf, dws, hbuf, hws, d_info));
+    int info = 0;
+    CUDA_OK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(cudaFreeAsync(dbuf, ctx->stream));
+    CUDA_OK(cudaStreamSynchronize(ctx->stream));
+    if (info != 0) throw BseError(BSE_ENUMERICAL, "general eigensolver failed (info " + std::to_string(info) + ")");
+    std::vector<double> ev(2 * k);
+    to_host(ctx, ev.data(), reinterpret_cast<double*>(d_ev), 2 * k);
+    std::vector<int> order(k);
+    std::iota(order.begin(), order.end(), 0);
+    for (int64_t i = 0; i < k; ++i)
+      if (!std::isfinite(ev[2 * i]) || !std::isfinite(ev[2 * i + 1]))
+        throw BseError(BSE_ENUMERICAL, "general eigensolver returned non-finite eigenvalues");
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ev[2 * a] < ev[2 * b]; });
+    for (int64_t i = 0; i < k; ++i) h_lam[i] = ev[2 * order[i]];
+    {
+      std::vector<double> tmpd((k + 1) / 2 + 1);
+      std::memcpy(tmpd.data(), order.data(), sizeof(int) * k);
+      to_device(ctx, reinterpret_cast<double*>(d_perm), tmpd.data(), (k + 1) / 2);
+    }
+    bse::gather_cols_kernel<<<dim3(1, (unsigned)k), 256, 0, ctx->stream>>>(y, k, yperm, k, k, d_perm);
+    check_launch(ctx);
+    zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, q, ldq, yperm, k, 0.0, vout, ldvout, gws);
+    bse::colnorm_kernel<<<(int)k, 256, 0, ctx->stream>>>(vout, ldvout, n, d_w);
+    check_launch(ctx);
+    bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_w);
+    check_launch(ctx);
+  });
+}
+
+int bse_lanczos_sweep(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* h_start, int steps,
+                      double* h_alpha, double* h_beta, int* h_count) {
+  return guarded(ctx, [&] {
+    const int64_t n = 2 * m;
+    const int nb = grid1d(n, 256, 296);
+    Scratch sc(ctx, 6 * al(n * sizeof(zval)) + al((nb + 2) * 8) + al(64));
+    zval* start = sc.take<zval>(n);
+    zval* q = sc.take<zval>(n);
+    zval* qold = sc.take<zval>(n);
+    zval* z = sc.take<zval>(n);
+    zval* w = sc.take<zval>(n);
+    zval* gv = sc.take<zval>(n);
+    double* part = sc.take<double>(nb + 2);
+    to_device(ctx, reinterpret_cast<double*>(start), static_cast<const double*>(h_start), 2 * n);
+    auto sdot = [&](const zval* x, const zval* y) {
+      bse::sdot_partial_kernel<<<nb, 256, 0, ctx->stream>>>(x, y, n, m, 1, part);
+      check_launch(ctx);
+      bse::sum_reduce_kernel<<<1, 256, 0, ctx->stream>>>(part, nb, part + nb);
+      check_launch(ctx);
+      double h = 0.0;
+      to_host(ctx, &h, part + nb, 1);
+      return h;
+    };
+    auto scale_div = [&](zval* out, const zval* in, double s) {
+      // out = in / s  (division, as numpy's x / beta)
+      CUDA_OK(cudaMemcpyAsync(out, in, n * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+      to_device(ctx, part + nb + 1, &s, 1);
+      bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 148), 1), 256, 0, ctx->stream>>>(out, n, n, part + nb + 1);
+      check_launch(ctx);
+    };
+    // lanczos.py:58-66
+    apply_h(ctx, d_ab, lda, m, start, n, gv, n, 1, 1.0);
+    const double norm2 = sdot(gv, start);
+    if (!(norm2 > 0))
+      throw BseError(BSE_EINDEFINITE, "start vector has non-positive S*H norm; matrix is not definite");
+    const double sc0 = std::sqrt(norm2);
+    scale_div(q, start, sc0);
+    scale_div(z, gv, sc0);
+    CUDA_OK(cudaMemsetAsync(qold, 0, n * sizeof(zval), ctx->stream));
+    double beta_prev = 0.0, amax = 0.0;
+    int na = 0, nbeta = 0;
+    for (int j = 0; j < steps; ++j) {
+      const double alpha = sdot(z, z);  // lanczos.py:72
+      h_alpha[na++] = alpha;
+      amax = std::max(amax, std::fabs(alpha));
+      if (j == steps - 1) break;
+      bse::lincomb3_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(w, z, 1.0, q, -alpha, qold, -beta_prev, n);
+      check_launch(ctx);
+      apply_h(ctx, d_ab, lda, m, w, n, gv, n, 1, 1.0);
+      const double beta2 = sdot(gv, w);
+      const double running = std::max({1.0, amax, beta_prev});
+      if (beta2 <= (1e-14 * running) * (1e-14 * running)) break;  // lanczos.py:79-81
+      const double beta = std::sqrt(beta2);
+      h_beta[nbeta++] = beta;
+      std::swap(qold, q);
+      scale_div(q, w, beta);
+      scale_div(z, gv, beta);
+      beta_prev = beta;
+    }
+    *h_count = na;
+  });
+}
+
+int bse_is_definite(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int* h_definite) {
+  return guarded(ctx, [&] {
+    const int64_t n = 2 * m;
+    Scratch sc(ctx, al((size_t)n * n * sizeof(zval)) + al(64));
+    zval* sh = sc.take<zval>((size_t)n * n);
+    int* d_info = sc.take<int>(4);
+    bse::materialize_sh_kernel<<<grid1d(n * n), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ab), lda, m, sh);
+    check_launch(ctx);
+    *h_definite = potrf(ctx, sh, (int)n, CUBLAS_FILL_MODE_LOWER, d_info) == 0 ? 1 : 0;
+  });
+}
+
+int bse_complex_normals(bse_ctx* ctx, void* d_out, uint64_t seed, int64_t start_index, int64_t count) {
+  return guarded(ctx, [&] {
+    if (count <= 0) return;
+    bse::complex_normals_kernel<<<grid1d(count, 256, 148 * 32), 256, 0, ctx->stream>>>(static_cast<zval*>(d_out), seed,
+                                                                                       start_index, count);
+    check_launch(ctx);
+  });
+}
+
+int bse_complex_normals_t(bse_ctx* ctx, void* d_out, uint64_t seed, int64_t rows, int64_t cols) {
+  return guarded(ctx, [&] {
+    if (rows <= 0 || cols <= 0) return;
+    bse::complex_normals_t_kernel<<<grid1d(rows * cols, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        static_cast<zval*>(d_out), seed, rows, cols);
+    check_launch(ctx);
+  });
+}
+
+int bse_symmetrize(bse_ctx* ctx, void* d_a, int64_t m, int64_t lda, int conj) {
+  return guarded(ctx, [&] {
+    if (m <= 0) return;
+    bse::symmetrize_kernel<<<grid1d(m * m, 256, 148 * 32), 256, 0, ctx->stream>>>(static_cast<zval*>(d_a), lda, m, conj);
+    check_launch(ctx);
+  });
+}
+
+int bse_scale_shift(bse_ctx* ctx, void* d_a, int64_t m, int64_t lda, double scale, double shift, int conj) {
+  return guarded(ctx, [&] {
+    if (m <= 0) return;
+    bse::scale_shift_kernel<<<grid1d(m * m, 256, 148 * 32), 256, 0, ctx->stream>>>(static_cast<zval*>(d_a), lda, m,
+                                                                                  scale, shift, conj);
+    check_launch(ctx);
+  });
+}
+
+int bse_eigvalsh(bse_ctx* ctx, const void* d_a, int64_t k, int64_t lda, double* h_w) {
+  return guarded(ctx, [&] {
+    if (k <= 0) return;
+    Scratch sc(ctx, al((size_t)k * k * sizeof(zval)) + al(k * 8) + al(64));
+    zval* a = sc.take<zval>((size_t)k * k);
+    double* d_w = sc.take<double>(k);
+    int* d_info = sc.take<int>(4);
+    CUDA_OK(cudaMemcpy2DAsync(a, sizeof(zval) * k, d_a, sizeof(zval) * lda, sizeof(zval) * k, (size_t)k,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    heevd(ctx, a, (int)k, d_w, false, d_info);
+    to_host(ctx, h_w, d_w, k);
+  });
+}
+
+}  // extern "C"

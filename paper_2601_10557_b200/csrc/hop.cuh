@@ -1,0 +1,263 @@
+// Fused H-operator kernel: one complex FP64 GEMM that applies the BSE
+// Hamiltonian H = [[A, B], [-conj(B), -conj(A)]] from its two stored blocks
+// and finishes the result in the epilogue (Chebyshev three-term axpby,
+// S-flip, or residual column norms), so no separate elementwise pass touches
+// HBM.
+//
+// Reference semantics (paths under /root/reference/pkg/src/bsesolve/):
+//   apply_h            hamiltonian.py:132-151   H x = [A x1 + B x2 ; -conj(A conj x2 + B conj x1)]
+//   chebyshev_filter   chebyshev.py:68-74       y+ = (2s'/e)(H y - c y) - (s s') y-
+//   build_hermitian_rq rayleigh_ritz.py:112      T = S H Q
+//   residuals          rayleigh_ritz.py:188-189 ||H v - lam v||_2
+//
+// Formulation.  With P the current K-slab of A (part 0) or B (part 1):
+//   U  += P    * Xa      (Xa = X1 for part 0, X2 for part 1)
+//   L' += conj(P) * Xb   (Xb = X2 for part 0, X1 for part 1)
+// and H x = [U ; -L'].  Both products share every P fragment, so the A/B
+// stream is read once for the up and low halves.  Per 8x8 output block pair
+// and k4 step: 8 DMMA (4M complex split), fragments via LDS.128.
+#pragma once
+#include "common.cuh"
+
+namespace bse {
+
+enum HopEpi : int { HOP_AXPBY = 0, HOP_RESID = 1 };
+
+struct HopArgs {
+  // P operand: part 0 (A tile) and part 1 (B tile), both mr x kc, column-major, leading dim lda
+  const zval* pa;
+  const zval* pb;
+  int64_t lda;
+  int mr;  // output rows per half
+  int kc;  // contraction length per part
+  // X operand rows for the contraction: x1 (rows of the "upper" half), x2 ("lower")
+  const zval* x1;
+  const zval* x2;
+  int64_t ldx;
+  int k;  // columns
+  // epilogue operands (rows of the output)
+  zval* y1;
+  zval* y2;
+  int64_t ldy;
+  const zval* s1;  // shift operand (x at output rows); may be null when shift == 0
+  const zval* s2;
+  int64_t lds;
+  const zval* p1;  // y_prev at output rows; may be null when beta == 0
+  const zval* p2;
+  int64_t ldp;
+  double alpha, beta, shift, low_sign;
+  // residual mode
+  const double* lam;  // per column
+  double* partial;    // [gridDim.y][k]
+};
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_>
+struct HopCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int WARPS_M = BM / (8 * WM);
+  static constexpr int WARPS_N = BN / (8 * WN);
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int LDP = BM + 2;  // == 2 (mod 8): conflict-free LDS.128 A fragments
+  static constexpr int LDX = BK + 4;  // == 4 (mod 8): conflict-free LDS.128 B fragments
+  static constexpr int P_ELEMS = BK * LDP;
+  static constexpr int X_ELEMS = BN * LDX;
+  static constexpr int STAGE_ELEMS = P_ELEMS + 2 * X_ELEMS;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(zval);
+  static_assert(BM % 8 == 0 && BK % 8 == 0 && BN % 8 == 0, "tile dims");
+  static_assert((BK * BM) % THREADS == 0 && (2 * BN * BK) % THREADS == 0, "loader mapping");
+};
+
+template <class C>
+__device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int kt, int nkt_part, int i0, int c0) {
+  const int tid = threadIdx.x;
+  const int part = kt >= nkt_part;
+  const int j0 = (kt - part * nkt_part) * C::BK;
+  const zval* P = part ? a.pb : a.pa;
+  const zval* XA = part ? a.x2 : a.x1;
+  const zval* XB = part ? a.x1 : a.x2;
+  zval* Ps = st;
+  zval* Xas = st + C::P_ELEMS;
+  zval* Xbs = Xas + C::X_ELEMS;
+#pragma unroll
+  for (int r = 0; r < (C::BK * C::BM) / C::THREADS; ++r) {
+    const int id = tid + r * C::THREADS;
+    const int ii = id % C::BM, jj = id / C::BM;
+    const int gi = i0 + ii, gj = j0 + jj;
+    const bool ok = (gi < a.mr) && (gj < a.kc);
+    const zval* src = ok ? P + (int64_t)gj * a.lda + gi : P;
+    cp_async16(Ps + jj * C::LDP + ii, src, ok);
+  }
+#pragma unroll
+  for (int r = 0; r < (2 * C::BN * C::BK) / C::THREADS; ++r) {
+    const int id = tid + r * C::THREADS;
+    const int kk = id % C::BK;
+    const int cc = (id / C::BK) % C::BN;
+    const int which = id / (C::BK * C::BN);
+    const int gj = j0 + kk, gc = c0 + cc;
+    const bool ok = (gj < a.kc) && (gc < a.k);
+    const zval* X = which ? XB : XA;
+    const zval* src = ok ? X + (int64_t)gc * a.ldx + gj : X;
+    cp_async16((which ? Xbs : Xas) + cc * C::LDX + kk, src, ok);
+  }
+}
+
+template <class C, int EPI>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zval* smem = reinterpret_cast<zval*>(smem_raw);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int c0 = blockIdx.x * C::BN;  // column tile fastest: CTAs sharing an A/B strip run together
+  const int i0 = blockIdx.y * C::BM;
+
+  const int nkt_part = (a.kc + C::BK - 1) / C::BK;
+  const int nkt = 2 * nkt_part;
+
+  double ur[C::WM][C::WN][2], ui[C::WM][C::WN][2], lr[C::WM][C::WN][2], li[C::WM][C::WN][2];
+#pragma unroll
+  for (int i = 0; i < C::WM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) ur[i][j][h] = ui[i][j][h] = lr[i][j][h] = li[i][j][h] = 0.0;
+
+  // prologue
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < nkt) hop_load_stage<C>(smem + s * C::STAGE_ELEMS, a, s, nkt_part, i0, c0);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nkt; ++kt) {
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    {
+      const int nxt = kt + C::STAGES - 1;
+      if (nxt < nkt) hop_load_stage<C>(smem + (nxt % C::STAGES) * C::STAGE_ELEMS, a, nxt, nkt_part, i0, c0);
+      cp_async_commit();
+    }
+    const zval* Ps = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
+    const zval* Xas = Ps + C::P_ELEMS;
+    const zval* Xbs = Xas + C::X_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < C::BK / 4; ++ks) {
+      zval pf[C::WM], xa[C::WN], xb[C::WN];
+#pragma unroll
+      for (int i = 0; i < C::WM; ++i) pf[i] = lds128(Ps + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j) {
+        const int col = wn * (8 * C::WN) + j * 8 + g;
+        xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
+        xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
+      }
+#pragma unroll
+      for (int i = 0; i < C::WM; ++i) {
+        const double pr = pf[i].re, pi = pf[i].im, npi = -pf[i].im;
+#pragma unroll
+        for (int j = 0; j < C::WN; ++j) {
+          dmma(ur[i][j], pr, xa[j].re);
+          dmma(ur[i][j], npi, xa[j].im);
+          dmma(ui[i][j], pr, xa[j].im);
+          dmma(ui[i][j], pi, xa[j].re);
+          dmma(lr[i][j], pr, xb[j].re);
+          dmma(lr[i][j], pi, xb[j].im);
+          dmma(li[i][j], pr, xb[j].im);
+          dmma(li[i][j], npi, xb[j].re);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---------------------------------------------------------------- epilogue
+  if constexpr (EPI == HOP_AXPBY) {
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i) {
+      const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
+      if (row >= a.mr) continue;
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + h;
+          if (col >= a.k) continue;
+          // H x rows: up = U, low = -L'
+          double hu_r = ur[i][j][h], hu_i = ui[i][j][h];
+          double hl_r = -lr[i][j][h], hl_i = -li[i][j][h];
+          if (a.shift != 0.0) {
+            const zval s1 = a.s1[(int64_t)col * a.lds + row];
+            const zval s2 = a.s2[(int64_t)col * a.lds + row];
+            hu_r = hu_r - a.shift * s1.re;
+            hu_i = hu_i - a.shift * s1.im;
+            hl_r = hl_r - a.shift * s2.re;
+            hl_i = hl_i - a.shift * s2.im;
+          }
+          zval o1{a.alpha * hu_r, a.alpha * hu_i}, o2{a.alpha * hl_r, a.alpha * hl_i};
+          if (a.beta != 0.0) {
+            const zval q1 = a.p1[(int64_t)col * a.ldp + row];
+            const zval q2 = a.p2[(int64_t)col * a.ldp + row];
+            o1.re = o1.re - a.beta * q1.re;
+            o1.im = o1.im - a.beta * q1.im;
+            o2.re = o2.re - a.beta * q2.re;
+            o2.im = o2.im - a.beta * q2.im;
+          }
+          o2.re *= a.low_sign;
+          o2.im *= a.low_sign;
+          a.y1[(int64_t)col * a.ldy + row] = o1;
+          a.y2[(int64_t)col * a.ldy + row] = o2;
+        }
+      }
+    }
+  } else {
+    // residual column norms: sum over this CTA's rows of |Hv - lam v|^2 (both halves)
+    __shared__ double red[C::WARPS_M][C::BN];
+    double acc[C::WN][2];
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + h;
+        double s = 0.0;
+        if (col < a.k) {
+          const double lam = a.lam[col];
+#pragma unroll
+          for (int i = 0; i < C::WM; ++i) {
+            const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
+            if (row < a.mr) {
+              const zval v1 = a.s1[(int64_t)col * a.lds + row];
+              const zval v2 = a.s2[(int64_t)col * a.lds + row];
+              const double r1 = ur[i][j][h] - lam * v1.re, r2 = ui[i][j][h] - lam * v1.im;
+              const double r3 = -lr[i][j][h] - lam * v2.re, r4 = -li[i][j][h] - lam * v2.im;
+              s += r1 * r1 + r2 * r2 + r3 * r3 + r4 * r4;
+            }
+          }
+        }
+        // reduce across g (lane bits 2..4), fixed order
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 8);
+        s += __shfl_xor_sync(0xffffffffu, s, 16);
+        acc[j][h] = s;
+      }
+    }
+    if (g == 0) {
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) red[wm][wn * (8 * C::WN) + j * 8 + 2 * t + h] = acc[j][h];
+    }
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < C::BN; cc += C::THREADS) {
+      const int col = c0 + cc;
+      if (col < a.k) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < C::WARPS_M; ++w) s += red[w][cc];
+        a.partial[(int64_t)blockIdx.y * a.k + col] = s;
+      }
+    }
+  }
+}
+
+}  // namespace bse

@@ -1,0 +1,318 @@
+"""BSE Hamiltonian blocks on the device and the H / S / K / J operators.
+
+Drop-in for bsesolve/hamiltonian.py.  ``BseHamiltonian`` keeps the reference
+constructor contract (A hermitian, B symmetric, complex128, defects up to
+1e-12 x scale repaired, larger ones rejected: hamiltonian.py:35-96) and adds
+the device layout the kernels read: one m x 2m column-major complex128 buffer
+``[A | B]`` per GPU (32 m^2 bytes, converted once; see DESIGN.md "HBM
+layout").  ``apply_h`` and friends run on the GPU through the C ABI.
+"""
+
+from __future__ import annotations
+
+import enum
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ValidationError
+from .metrics import PhaseLedger
+
+logger = logging.getLogger(__name__)
+
+SYMMETRY_RTOL = 1e-12
+
+
+class Definiteness(enum.Enum):
+    UNKNOWN = "unknown"
+    DEFINITE = "definite"
+    INDEFINITE = "indefinite"
+
+
+def as_complex_matrix(a, name: str = "matrix") -> np.ndarray:
+    """2-D finite complex128, column-major (hamiltonian.py:35-42)."""
+    arr = np.asfortranarray(a, dtype=np.complex128)
+    if arr.ndim != 2:
+        raise ValidationError(f"{name} must be 2-D, got ndim={arr.ndim}")
+    if arr.size and not np.isfinite(arr).all():
+        raise ValidationError(f"{name} contains non-finite entries")
+    return arr
+
+
+def _repair(block: np.ndarray, mirror: np.ndarray, name: str, what: str) -> np.ndarray:
+    """hamiltonian.py:45-60 semantics: exact -> as is; <= 1e-12 scale -> averaged; else reject."""
+    if not block.size:
+        return block
+    gap = float(np.abs(block - mirror).max())
+    if gap == 0.0:
+        return block
+    scale = float(np.abs(block).max())
+    if scale > 0.0 and gap > SYMMETRY_RTOL * scale:
+        raise ValidationError(
+            f"{name} violates {what} beyond tolerance: defect={gap:.3e}, allowed={SYMMETRY_RTOL * scale:.3e}"
+        )
+    logger.warning("%s had a %s defect of %.3e (scale %.3e); symmetrized on load", name, what, gap, scale)
+    return np.asfortranarray((block + mirror) / 2.0)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def colmajor_empty(rows: int, cols: int, device) -> "torch.Tensor":
+    """Uninitialised column-major complex128 device matrix (shape rows x cols, strides (1, rows))."""
+    torch = _torch()
+    return torch.empty((cols, rows), dtype=torch.complex128, device=device).T
+
+
+def to_colmajor(x, device) -> "torch.Tensor":
+    """Column-major complex128 copy of a numpy / torch matrix on ``device``."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=torch.complex128)
+    else:
+        arr = np.asarray(x, dtype=np.complex128)
+        if arr.ndim == 1:
+            arr = arr[:, None]
+        t = torch.from_numpy(np.ascontiguousarray(arr.T)).to(device, non_blocking=False).T
+        return t
+    if t.ndim == 1:
+        t = t[:, None]
+    if t.stride(0) != 1 or t.stride(1) < t.shape[0]:
+        t = t.T.contiguous().T
+    return t
+
+
+def ld_of(t) -> int:
+    return max(int(t.stride(1)), int(t.shape[0]), 1) if t.ndim == 2 else int(t.shape[0])
+
+
+@dataclass(eq=False)
+class BseHamiltonian:
+    """H = [[A, B], [-conj(B), -conj(A)]] stored as its blocks A and B.
+
+    ``a``/``b`` are host numpy arrays (reference contract).  ``device_blocks``
+    returns the ``[A | B]`` device buffer, uploaded once per device.  A
+    Hamiltonian built on the GPU (``generate(..., device=...)``) may carry only
+    the device copy; ``a``/``b`` are then downloaded lazily.
+    """
+
+    a: np.ndarray | None
+    b: np.ndarray | None
+    definiteness: Definiteness = field(default=Definiteness.UNKNOWN)
+
+    def __post_init__(self) -> None:
+        self._dev: dict = {}
+        self._m = None
+        if self.a is None and self.b is None:
+            return  # device-born; populated by from_device()
+        a = as_complex_matrix(self.a, "A")
+        b = as_complex_matrix(self.b, "B")
+        if a.shape[0] != a.shape[1] or b.shape[0] != b.shape[1]:
+            raise ValidationError(f"blocks must be square, got {a.shape} and {b.shape}")
+        if a.shape != b.shape:
+            raise ValidationError(f"A and B must agree in size, got {a.shape} != {b.shape}")
+        a = _repair(a, a.conj().T, "A", "hermiticity")
+        b = _repair(b, b.T, "B", "symmetry")
+        a.flags.writeable = False
+        b.flags.writeable = False
+        self.a, self.b = a, b
+        self._m = a.shape[0]
+
+    # ------------------------------------------------------------------ device
+    @classmethod
+    def from_device(cls, ab, definiteness: Definiteness = Definiteness.UNKNOWN) -> "BseHamiltonian":
+        """Wrap an m x 2m column-major device buffer [A | B] (exactly hermitian / symmetric)."""
+        ham = cls(None, None, definiteness)
+        ham._m = int(ab.shape[0])
+        ham._dev[ab.device] = ab
+        return ham
+
+    def device_blocks(self, device=None):
+        torch = _torch()
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        device = torch.device(device)
+        if device.type == "cuda" and device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        ab = self._dev.get(device)
+        if ab is None:
+            if self.a is None:
+                src = next(iter(self._dev.values()))
+                ab = src.to(device)
+                if ab.stride(0) != 1:
+                    ab = ab.T.contiguous().T
+            else:
+                m = self.m
+                ab = colmajor_empty(m, 2 * m, device)
+                # F-ordered numpy -> (1, m)-strided host view -> one dense copy per block
+                ab[:, :m].copy_(torch.from_numpy(np.asfortranarray(self.a)))
+                ab[:, m:].copy_(torch.from_numpy(np.asfortranarray(self.b)))
+            self._dev[device] = ab
+        return ab
+
+    def release_device(self) -> None:
+        if self.a is not None:
+            self._dev.clear()
+
+    def host_blocks(self) -> tuple[np.ndarray, np.ndarray]:
+        if self.a is None:
+            ab = next(iter(self._dev.values()))
+            m = self.m
+            full = ab.T.contiguous().cpu().numpy().T  # F-order numpy
+            self.a = np.asfortranarray(full[:, :m])
+            self.b = np.asfortranarray(full[:, m:])
+            self.a.flags.writeable = False
+            self.b.flags.writeable = False
+        return self.a, self.b
+
+    @property
+    def m(self) -> int:
+        return self._m
+
+    @property
+    def n(self) -> int:
+        return 2 * self._m
+
+
+def _check_rows(x, n: int) -> None:
+    if x.shape[0] != n:
+        raise ValidationError(f"operand has {x.shape[0]} rows, expected {n}")
+
+
+def _host_like(ref, t):
+    """Return t as numpy when the caller passed numpy, else as a torch tensor."""
+    torch = _torch()
+    if isinstance(ref, torch.Tensor):
+        return t
+    return t.T.contiguous().cpu().numpy().T
+
+
+def _device_for(x):
+    torch = _torch()
+    if isinstance(x, torch.Tensor) and x.is_cuda:
+        return x.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+# ---------------------------------------------------------------- S / K / J
+def _halves(x, name: str):
+    if x.shape[0] % 2:
+        raise ValidationError(f"{name} needs an even row count, got {x.shape[0]}")
+    return x.shape[0] // 2
+
+
+def apply_s(x):
+    """S x (hamiltonian.py:104-111): lower half negated."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        m = _halves(x, "S")
+        out = x.clone()
+        out[m:] *= -1.0
+        return out
+    x = np.asarray(x, dtype=np.complex128)
+    m = _halves(x, "S")
+    out = x.copy()
+    out[m:] *= -1.0
+    return out
+
+
+def apply_k(x):
+    """K x (hamiltonian.py:114-120): halves swapped."""
+    torch = _torch()
+    m = _halves(x, "K")
+    if isinstance(x, torch.Tensor):
+        return torch.cat([x[m:], x[:m]], dim=0)
+    x = np.asarray(x, dtype=np.complex128)
+    return np.concatenate([x[m:], x[:m]], axis=0)
+
+
+def apply_j(x):
+    """J x = (x_lower, -x_upper) (hamiltonian.py:123-129)."""
+    torch = _torch()
+    m = _halves(x, "J")
+    if isinstance(x, torch.Tensor):
+        return torch.cat([x[m:], -x[:m]], dim=0)
+    x = np.asarray(x, dtype=np.complex128)
+    return np.concatenate([x[m:], -x[:m]], axis=0)
+
+
+# ---------------------------------------------------------------- H products
+def _apply(ham: BseHamiltonian, x, low_sign: float, ledger, phase):
+    vec = getattr(x, "ndim", 2) == 1
+    _check_rows(x, ham.n)
+    dev = _device_for(x)
+    xd = to_colmajor(x, dev)
+    k = xd.shape[1]
+    y = colmajor_empty(ham.n, k, dev)
+    ctx = _lib.Context.get(dev.index)
+    ab = ham.device_blocks(dev)
+    ctx.call("bse_apply_h", _lib.dptr(ab), ld_of(ab), ham.m, _lib.dptr(xd), ld_of(xd), _lib.dptr(y), ld_of(y), k,
+             float(low_sign))
+    if ledger is not None:
+        ledger.add_flops(phase, 8.0 * ham.n * ham.n * k)
+    out = _host_like(x, y)
+    return out[:, 0] if vec else out
+
+
+def apply_h(ham: BseHamiltonian, x, ledger: PhaseLedger | None = None, phase: str = "filter"):
+    """H x on the GPU (hamiltonian.py:132-151): one fused DMMA GEMM over [A | B]."""
+    return _apply(ham, x, 1.0, ledger, phase)
+
+
+def apply_h_via_adjoint(ham: BseHamiltonian, x, ledger: PhaseLedger | None = None, phase: str = "filter"):
+    """H x as S (H* (S x)) (hamiltonian.py:154-176).  On one device the
+    adjoint identity is the same fused product (the block-transposed tiles
+    only differ in the 2D-distributed layout)."""
+    return _apply(ham, x, 1.0, ledger, phase)
+
+
+def apply_sh(ham: BseHamiltonian, x, ledger: PhaseLedger | None = None, phase: str = "rr"):
+    """S H x with the flip fused into the epilogue (rayleigh_ritz.py:112)."""
+    return _apply(ham, x, -1.0, ledger, phase)
+
+
+def materialize(ham: BseHamiltonian) -> np.ndarray:
+    """Dense n x n H (oracles / structural checks only; hamiltonian.py:179-183)."""
+    a, b = ham.host_blocks()
+    return np.asfortranarray(np.block([[a, b], [-np.conj(b), -np.conj(a)]]))
+
+
+def materialize_sh(ham: BseHamiltonian) -> np.ndarray:
+    """Dense S H = [[A, B], [conj B, conj A]] (hamiltonian.py:186-190)."""
+    a, b = ham.host_blocks()
+    return np.asfortranarray(np.block([[a, b], [np.conj(b), np.conj(a)]]))
+
+
+def validate_pseudo_hermitian(h_dense) -> tuple[bool, float]:
+    """S H = H* S on a dense matrix (hamiltonian.py:193-205)."""
+    h = np.asarray(h_dense, dtype=np.complex128)
+    if h.ndim != 2 or h.shape[0] != h.shape[1]:
+        raise ValidationError(f"expected a square matrix, got shape {h.shape}")
+    if h.shape[0] % 2:
+        raise ValidationError(f"pseudo-hermitian structure needs even dimension, got {h.shape[0]}")
+    lhs = apply_s(h)
+    rhs = h.conj().T.copy()
+    rhs[:, h.shape[0] // 2:] *= -1.0
+    gap = float(np.abs(lhs - rhs).max()) if h.size else 0.0
+    scale = float(np.abs(h).max()) if h.size else 0.0
+    return gap <= SYMMETRY_RTOL * scale, gap
+
+
+def is_definite(ham: BseHamiltonian) -> Definiteness:
+    """Cholesky of S H on the device (hamiltonian.py:208-218), cached."""
+    if ham.definiteness is not Definiteness.UNKNOWN:
+        return ham.definiteness
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ab = ham.device_blocks(dev)
+    import ctypes
+
+    flag = ctypes.c_int(0)
+    _lib.Context.get(dev.index).call("bse_is_definite", _lib.dptr(ab), ld_of(ab), ham.m, ctypes.byref(flag))
+    ham.definiteness = Definiteness.DEFINITE if flag.value else Definiteness.INDEFINITE
+    return ham.definiteness

@@ -1,0 +1,53 @@
+"""Counter-based random streams, bit-identical to the reference scheme
+(bsesolve/rng.py:1-81, docs/FORMATS.md): splitmix64 words, uniforms in
+(0, 1], Box-Muller complex normals, column-major matrix fill, tagged child
+streams.  Computed on the host with numpy so the start vectors of a solve are
+the very same bits the reference draws (GPU libm would differ in the last
+ulp and change the iteration trace)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+_U64 = np.uint64
+_WRAP = (1 << 64) - 1
+_STEP, _M1, _M2 = 0x9E3779B97F4A7C15, 0xBF58476D1CE4E5B9, 0x94D049BB133111EB
+
+
+def _finalize(z):
+    z = ((z ^ (z >> 30)) * _M1) & _WRAP
+    z = ((z ^ (z >> 27)) * _M2) & _WRAP
+    return z ^ (z >> 31)
+
+
+def word(seed: int, counter: int) -> int:
+    return _finalize((seed + (counter + 1) * _STEP) & _WRAP)
+
+
+def substream(seed: int, tag: int) -> int:
+    return word(seed & _WRAP, tag)
+
+
+def _words(seed: int, start: int, count: int) -> np.ndarray:
+    with np.errstate(over="ignore"):
+        z = _U64(seed & _WRAP) + np.arange(start + 1, start + 1 + count, dtype=_U64) * _U64(_STEP)
+        for shift, mul in ((30, _M1), (27, _M2)):
+            z ^= z >> _U64(shift)
+            z *= _U64(mul)
+        z ^= z >> _U64(31)
+    return z
+
+
+def uniforms(seed: int, start: int, count: int) -> np.ndarray:
+    return ((_words(seed, start, count) >> _U64(11)).astype(np.float64) + 1.0) * 2.0**-53
+
+
+def complex_normals(seed: int, count: int, start_index: int = 0) -> np.ndarray:
+    u = uniforms(seed, 2 * start_index, 2 * count).reshape(count, 2)
+    radius = np.sqrt(-2.0 * np.log(u[:, 0]))
+    angle = 2.0 * np.pi * u[:, 1]
+    return radius * np.cos(angle) + 1j * (radius * np.sin(angle))
+
+
+def complex_normal_matrix(seed: int, rows: int, cols: int) -> np.ndarray:
+    return complex_normals(seed, rows * cols).reshape((cols, rows)).T
