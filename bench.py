@@ -1,0 +1,349 @@
+"""Benchmark: time-to-solution of the pseudo-hermitian ChASE solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3|c2|c1] [--impl ours|reference]
+
+A "step" is one complete solve (Lanczos bounds -> filtered subspace iteration
+until nev pairs lock) of the BASELINE.json configuration the metric is quoted
+on: n = 40k (m = 20,000) complex128, nev = 1000, nex = 200, deg = 20,
+tol = 1e-10 relative (SolverConfig(rel_res=True); the reference's absolute
+1e-10 is below the FP64 residual floor at this n).
+Synthetic input built on the GPU with the reference construction
+(generate.py:60-83).  The inputs (A|B = 12.8 GB) exceed L2 (126 MB), so no
+L2 flush is needed between steps.
+
+value            device-resident time-to-solution (s), max over ranks
+e2e              same solve through the public drop-in API with HOST numpy blocks:
+                 H2D of A, B and the start block and D2H of the nev vectors inside the timed region
+roofline         the filter kernel (fused H-operator DMMA GEMM) vs the measured FP64 DMMA peak
+cpu_baseline     the CPU oracle (numpy/OpenBLAS restatement of the reference) on a bounded sample
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (m, nev, nex, deg, tol, rel_res)
+    "c1": (500, 50, 20, 20, 1e-10, False),
+    "c2": (10000, 500, 100, 20, 1e-10, True),
+    "c3": (20000, 1000, 200, 20, 1e-10, True),
+}
+METRIC = "time-to-solution, nev eigenpairs @ n=40k; filter FP64 TFLOP/s as % of peak"
+FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak.json"
+# expected modeled flops of one C3 solve (from our own trace, profiles/); used by the CPU arm
+TRACE_FILE = ROOT / "profiles" / "solve_trace_{cfg}.json"
+
+
+def fp64_peak() -> tuple[float, str]:
+    try:
+        d = json.loads(FP64_PEAK_FILE.read_text())
+        return float(d["dmma_tflops"]), "measured DMMA.8x8x4 peak (profiles/fp64_peak.json)"
+    except Exception:
+        return 37.2, "nominal 148 SM x 64 FP64 FMA/clk x 1.965 GHz"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.5)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=15)
+
+    def summary(self) -> dict:
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def cpu_sample(m: int, k_sample: int, ham=None) -> dict:
+    """Time the oracle's H-application (the reference's 86 %-of-wall kernel, 4 zgemm) on
+    k_sample columns at the full m, on the host cores (OpenBLAS threads = all)."""
+    from oracle import bse_oracle as o
+
+    if ham is not None:
+        a, b = ham.host_blocks()
+    else:  # reference arm without a GPU-built input: same-shaped random hermitian/symmetric blocks
+        rs = np.random.default_rng(0)
+        a = np.asfortranarray(rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m)))
+        b = np.asfortranarray(rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m)))
+    x = o.gauss_c_matrix(o.child_seed(0, 3), 2 * m, k_sample)
+    o.h_times(a[:64, :64], b[:64, :64], x[:128, :2])  # warm BLAS
+    t0 = time.perf_counter()
+    o.h_times(a, b, x)
+    dt = time.perf_counter() - t0
+    flops = 8.0 * (2 * m) ** 2 * k_sample
+    return {"seconds": dt, "flops": flops, "gflops": flops / dt / 1e9}
+
+
+def expected_solve_flops(cfg_name: str, nevex: int, m: int, deg: int) -> tuple[float, str]:
+    p = Path(str(TRACE_FILE).format(cfg=cfg_name))
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["total_model_flops"]), f"modeled flops of our {cfg_name} solve trace ({p.name})"
+    n = 2 * m
+    sum_k = 6.9 * nevex  # measured Sigma k / nevex at the C2 shape
+    return (deg + 2) * 8.0 * n * n * sum_k, "model (deg+2) 8 n^2 Sigma k, Sigma k = 6.9 nevex (SURVEY 6.4)"
+
+
+def cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    m, nev, nex, deg, tol, rel = CONFIGS[args.config]
+    nevex = nev + nex
+    k_sample = 16 if m >= 10000 else 64
+    total, how = expected_solve_flops(args.config, nevex, m, deg)
+    times = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(m, k_sample)
+        if i >= args.warmup:
+            times.append(total / (s["flops"] / s["seconds"]))
+    val = statistics.median(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "config": config_dict(args.config),
+        "cpu_baseline": {"value": val, "unit": "s", "cores": cores(), "kind": "port",
+                         "sample": f"oracle H-application (4 OpenBLAS zgemm) at m={m} on {k_sample} columns per step, "
+                                   f"extrapolated to the solve's total modeled flops ({how})"},
+        "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(name):
+    m, nev, nex, deg, tol, rel = CONFIGS[name]
+    return {"workload": f"{name}: synthetic definite BSE H, n={2 * m} complex128, nev={nev}, nex={nex}, deg={deg}, "
+                        f"tol={tol:g} {'relative' if rel else 'absolute'}",
+            "n": 2 * m, "nev": nev, "nex": nex, "deg": deg, "tol": tol, "rel_res": rel,
+            "l2_flush": "inputs (A|B 32m^2 B) larger than L2", "parallelism": "1 GPU"}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2601_10557_b200 as bse
+    from paper_2601_10557_b200 import _lib
+    from paper_2601_10557_b200.hamiltonian import BseHamiltonian, Definiteness
+
+    if world > 1:
+        # TODO(2D): the distributed 2D filter lands in paper_2601_10557_b200/dist; until then each rank runs
+        # the full solve as an independent replica
+        pass
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    m, nev, nex, deg, tol, rel = CONFIGS[args.config]
+    n = 2 * m
+    t0 = time.perf_counter()
+    ham = bse.generate(bse.GeneratorSpec(m=m, seed=0), device=dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    cfg = bse.SolverConfig(nev=nev, nex=nex, deg=deg, tol=tol, seed=0, rel_res=rel)
+    ctx = _lib.Context.get(local)
+
+    # filter-kernel timing: CUDA events around every filter call (same stream as the kernels)
+    import paper_2601_10557_b200.solver as solver_mod
+
+    filt_ms = []
+    filt_flops = []
+    orig = solver_mod.filter_inplace
+
+    def timed_filter(ham_, v, fcfg, work=None, ledger=None):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = orig(ham_, v, fcfg, work, ledger)
+        e1.record()
+        filt_ms.append((e0, e1))
+        filt_flops.append(fcfg.degree * 8.0 * n * n * v.shape[1])
+        return out
+
+    solver_mod.filter_inplace = timed_filter
+
+    def one_solve():
+        return bse.solve(ham, cfg, device=dev, keep_on_device=True)
+
+    for _ in range(args.warmup):
+        one_solve()
+    filt_ms.clear()
+    filt_flops.clear()
+    barrier(world)
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        results = [one_solve() for _ in range(args.steps)]
+        e1.record()
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = ctx.launches - launches0
+    step_s = e0.elapsed_time(e1) / 1e3 / args.steps
+    step_s = max_over_ranks(step_s, world)
+    fms = sum(a.elapsed_time(b) for a, b in filt_ms)
+    ffl = sum(filt_flops)
+    res = results[-1]
+    solver_mod.filter_inplace = orig
+
+    # end to end through the public drop-in API with host blocks (upload inside the timed region)
+    a_h, b_h = ham.host_blocks()
+    host_ham = BseHamiltonian(a_h, b_h, Definiteness.DEFINITE)  # definiteness certified by the generator
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r_e2e = bse.solve(host_ham, cfg, device=dev)  # returns numpy v
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    h2d = 2 * m * m * 16 + n * cfg.nevex * 16 + 8 * n * 16
+    d2h = r_e2e.v.nbytes + 8 * (cfg.nevex + 64)
+    host_ham.release_device()
+
+    peak, peak_src = fp64_peak()
+    achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
+    total_model = res.ledger.total_flops()
+    if rank == 0 and args.config != "c1":
+        TRACE_FILE.parent.mkdir(exist_ok=True)
+        Path(str(TRACE_FILE).format(cfg=args.config)).write_text(json.dumps({
+            "total_model_flops": total_model, "iterations": res.iterations_used, "converged": res.converged,
+            "trace": [[t.it, t.locked, t.k, t.max_res, t.mu_nevex, t.flops] for t in res.trace],
+            "ledger_seconds": res.ledger.seconds, "ledger_flops": res.ledger.flops}, indent=1) + "\n")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        k_sample = 16 if m >= 10000 else 64
+        s = cpu_sample(m, k_sample, ham)
+        cpu = {"value": total_model / (s["flops"] / s["seconds"]), "unit": "s", "cores": cores(), "kind": "port",
+               "sample": f"oracle H-application (4 OpenBLAS zgemm, {s['gflops']:.0f} GF/s) at m={m} on {k_sample} "
+                         f"columns, extrapolated to this solve's {total_model:.3e} modeled flops"}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (GPU generator, reference construction)",
+            "config": config_dict(args.config),
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": launches // args.steps,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "kernel": "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)",
+                         "peak_source": peak_src,
+                         "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model), summed over the "
+                                        "solve's filter calls / CUDA-event time of those calls"},
+            "filter_tflops": achieved, "filter_frac_of_fp64_peak": (achieved / peak) if achieved else None,
+            "solve": {"iterations": res.iterations_used, "converged": res.converged,
+                      "ledger_seconds": {k: round(v, 4) for k, v in res.ledger.seconds.items()},
+                      "model_tflop": total_model / 1e12, "generator_s": round(gen_s, 2),
+                      "lambda_1": float(res.lambdas[0]), "lambda_nev": float(res.lambdas[-1]),
+                      "max_residual": float(res.residual_norms.max()),
+                      "e2e_iterations": r_e2e.iterations_used,
+                      "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -418,18 +418,23 @@ int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scra
   for (double v : f2) fro2 += v;
   const double u = std::ldexp(1.0, -53);
   const double shift = 11.0 * ((double)n * k + (double)k * (k + 1)) * u * fro2;
-  if (!(fro2 > 0.0) || !cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, shift, rdiag))
+  // X = Q R3 R2 R1 with all three factors upper triangular, so |diag R(X)| is the
+  // product of the per-pass diagonals; the rank test of ortho.py:86-93 runs on it.
+  std::vector<double> dprod(k, 1.0), rd(k);
+  auto pass_with_diag = [&](double sh) {
+    if (!cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, sh, rdiag)) return false;
+    to_host(ctx, rd.data(), rdiag, k);
+    for (int64_t i = 0; i < k; ++i) dprod[i] *= rd[i];
+    return true;
+  };
+  if (!(fro2 > 0.0) || !pass_with_diag(shift))
     throw BseError(BSE_ERANK, "columns are numerically rank deficient (shifted Cholesky failed)");
-  // rank test on the shifted factor (mirrors ortho.py:86-93: min|diag R| <= 1e-10 max|diag R|)
-  std::vector<double> rd(k);
-  to_host(ctx, rd.data(), rdiag, k);
-  const double dmax = *std::max_element(rd.begin(), rd.end()), dmin = *std::min_element(rd.begin(), rd.end());
-  if (dmax == 0.0 || dmin <= 1e-10 * dmax || !(dmin == dmin))
+  for (int pass = 0; pass < 2; ++pass)
+    if (!pass_with_diag(0.0)) throw BseError(BSE_ERANK, "columns are numerically rank deficient (CholQR after shift failed)");
+  const double dmax = *std::max_element(dprod.begin(), dprod.end()), dmin = *std::min_element(dprod.begin(), dprod.end());
+  if (dmax == 0.0 || !(dmin > 1e-10 * dmax))
     throw BseError(BSE_ERANK, "columns are numerically rank deficient (diag ratio " + std::to_string(dmin) + " / " +
                                   std::to_string(dmax) + ")");
-  for (int pass = 0; pass < 2; ++pass)
-    if (!cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, 0.0, nullptr))
-      throw BseError(BSE_ERANK, "columns are numerically rank deficient (CholQR after shift failed)");
   zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
   const double defect = defect_to_host(ctx, gram, (int)k, dpart);
   if (!(defect <= 1e-8)) throw BseError(BSE_ERANK, "orthonormalization failed (defect " + std::to_string(defect) + ")");

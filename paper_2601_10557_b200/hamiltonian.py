@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import enum
 import logging
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -150,8 +151,10 @@ class BseHamiltonian:
                 m = self.m
                 ab = colmajor_empty(m, 2 * m, device)
                 # F-ordered numpy -> (1, m)-strided host view -> one dense copy per block
-                ab[:, :m].copy_(torch.from_numpy(np.asfortranarray(self.a)))
-                ab[:, m:].copy_(torch.from_numpy(np.asfortranarray(self.b)))
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore", UserWarning)  # read-only numpy views are only read here
+                    ab[:, :m].copy_(torch.from_numpy(np.asfortranarray(self.a)))
+                    ab[:, m:].copy_(torch.from_numpy(np.asfortranarray(self.b)))
             self._dev[device] = ab
         return ab
 

@@ -121,18 +121,34 @@ def test_cholqr_matches_oracle(bse):
     assert _rel(q, g["q"]) <= 1e-8
 
 
+def _rand(n, k, seed):
+    g = np.random.default_rng(seed)
+    return g.standard_normal((n, k)) + 1j * g.standard_normal((n, k))
+
+
 def test_cholqr_fallback_and_rank(bse):
-    # test_ortho.py:43-72: cond 1e8 forces the fallback; exact rank deficiency raises
-    rs = np.random.default_rng(3)
-    u, _ = np.linalg.qr(rs.standard_normal((60, 6)) + 1j * rs.standard_normal((60, 6)))
-    v, _ = np.linalg.qr(rs.standard_normal((6, 6)) + 1j * rs.standard_normal((6, 6)))
-    x = u @ np.diag(np.logspace(0, -8, 6)) @ v
+    # test_ortho.py:22-28, 43-53: singular values clustered at 1 and 1e-8 force the
+    # fallback (shifted CholQR3 here, Householder in the reference); v, v + 1e-12 w is
+    # numerically rank deficient; k > n is rejected
+    u, _ = np.linalg.qr(_rand(60, 6, 0))
+    v, _ = np.linalg.qr(_rand(6, 6, 1))
+    s = np.ones(6)
+    s[3:] = 1e-8
+    x = u @ np.diag(s) @ v.conj().T
     q, method = bse.cholqr_with_fallback(x)
     assert method == "shifted_cholqr"
-    assert np.abs(q.conj().T @ q - np.eye(6)).max() <= 1e-10
-    y = np.concatenate([x[:, :3], x[:, :1]], axis=1)
+    assert np.abs(q.conj().T @ q - np.eye(6)).max() <= 1e-12
+    vv, ww = _rand(30, 1, 4), _rand(30, 1, 5)
     with pytest.raises(bse.RankDeficiencyError):
-        bse.cholqr_with_fallback(y)
+        bse.cholqr_with_fallback(np.concatenate([vv, vv + 1e-12 * ww], axis=1))
+    with pytest.raises(bse.RankDeficiencyError):
+        bse.cholqr_with_fallback(_rand(3, 5, 6))
+    q, method = bse.cholqr_with_fallback(np.eye(6, 3, dtype=complex))
+    assert method == "cholqr" and np.abs(q - np.eye(6, 3)).max() <= 1e-14
+    q, _ = bse.cholqr_with_fallback(_rand(20, 4, 7))
+    for j in range(4):  # phase convention test_ortho.py:61-66
+        lead = np.nonzero(np.abs(q[:, j]) >= 1e-8 * np.abs(q[:, j]).max())[0][0]
+        assert abs(q[lead, j].imag) <= 1e-14 and q[lead, j].real > 0
 
 
 def test_s_orthonormalize_against_locked(bse):
