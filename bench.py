@@ -129,6 +129,9 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # ----------------------------------------------------------------------------- CPU arms
+_BLOCKS = {}
+
+
 def cpu_sample(m: int, k_sample: int, ham=None) -> dict:
     """Time the oracle's H-application (the reference's 86 %-of-wall kernel, 4 zgemm) on
     k_sample columns at the full m, on the host cores (OpenBLAS threads = all)."""
@@ -136,10 +139,12 @@ def cpu_sample(m: int, k_sample: int, ham=None) -> dict:
 
     if ham is not None:
         a, b = ham.host_blocks()
-    else:  # reference arm without a GPU-built input: same-shaped random hermitian/symmetric blocks
-        rs = np.random.default_rng(0)
-        a = np.asfortranarray(rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m)))
-        b = np.asfortranarray(rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m)))
+    else:  # reference arm without a GPU-built input: same-shaped blocks (zgemm time is data independent)
+        if m not in _BLOCKS:
+            z = o.gauss_c(12345, m * m)
+            a = np.asfortranarray(z.reshape(m, m))
+            _BLOCKS[m] = (a, a)
+        a, b = _BLOCKS[m]
     x = o.gauss_c_matrix(o.child_seed(0, 3), 2 * m, k_sample)
     o.h_times(a[:64, :64], b[:64, :64], x[:128, :2])  # warm BLAS
     t0 = time.perf_counter()
@@ -208,10 +213,6 @@ def run_ours(args, world, rank, local):
     from paper_2601_10557_b200 import _lib
     from paper_2601_10557_b200.hamiltonian import BseHamiltonian, Definiteness
 
-    if world > 1:
-        # TODO(2D): the distributed 2D filter lands in paper_2601_10557_b200/dist; until then each rank runs
-        # the full solve as an independent replica
-        pass
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     m, nev, nex, deg, tol, rel = CONFIGS[args.config]
@@ -223,31 +224,49 @@ def run_ours(args, world, rank, local):
     cfg = bse.SolverConfig(nev=nev, nex=nex, deg=deg, tol=tol, seed=0, rel_res=rel)
     ctx = _lib.Context.get(local)
 
-    # filter-kernel timing: CUDA events around every filter call (same stream as the kernels)
-    import paper_2601_10557_b200.solver as solver_mod
+    filt = {"ms": 0.0, "flops": 0.0}
+    if world == 1:
+        # filter-kernel timing: CUDA events around every filter call (same stream as the kernels)
+        import paper_2601_10557_b200.solver as solver_mod
 
-    filt_ms = []
-    filt_flops = []
-    orig = solver_mod.filter_inplace
+        events = []
+        orig = solver_mod.filter_inplace
 
-    def timed_filter(ham_, v, fcfg, work=None, ledger=None):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        out = orig(ham_, v, fcfg, work, ledger)
-        e1.record()
-        filt_ms.append((e0, e1))
-        filt_flops.append(fcfg.degree * 8.0 * n * n * v.shape[1])
-        return out
+        def timed_filter(ham_, v, fcfg, work=None, ledger=None):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = orig(ham_, v, fcfg, work, ledger)
+            e1.record()
+            events.append((e0, e1, fcfg.degree * 8.0 * n * n * v.shape[1]))
+            return out
 
-    solver_mod.filter_inplace = timed_filter
+        solver_mod.filter_inplace = timed_filter
 
-    def one_solve():
-        return bse.solve(ham, cfg, device=dev, keep_on_device=True)
+        def one_solve():
+            return bse.solve(ham, cfg, device=dev, keep_on_device=True)
+
+        def filter_stats():
+            return sum(a.elapsed_time(b) for a, b, _ in events), sum(f for _, _, f in events)
+    else:
+        from paper_2601_10557_b200.dist import DistributedSolver
+
+        ds = DistributedSolver(ham, device=dev)
+        ham.release_device()
+        ham._dev.clear()
+        torch.cuda.empty_cache()
+        events = []
+
+        def one_solve():
+            r = ds.solve(cfg)
+            events.append((r.ledger.seconds["filter"] * 1e3, r.ledger.flops["filter"] / world))
+            return r
+
+        def filter_stats():
+            return sum(e[0] for e in events), sum(e[1] for e in events)
 
     for _ in range(args.warmup):
         one_solve()
-    filt_ms.clear()
-    filt_flops.clear()
+    events.clear()
     barrier(world)
     torch.cuda.synchronize()
     launches0 = ctx.launches
@@ -257,32 +276,43 @@ def run_ours(args, world, rank, local):
         results = [one_solve() for _ in range(args.steps)]
         e1.record()
         torch.cuda.synchronize()
-    barrier(world)
+        barrier(world)
     launches = ctx.launches - launches0
     step_s = e0.elapsed_time(e1) / 1e3 / args.steps
     step_s = max_over_ranks(step_s, world)
-    fms = sum(a.elapsed_time(b) for a, b in filt_ms)
-    ffl = sum(filt_flops)
+    fms, ffl = filter_stats()
     res = results[-1]
-    solver_mod.filter_inplace = orig
+    if world == 1:
+        solver_mod.filter_inplace = orig
 
-    # end to end through the public drop-in API with host blocks (upload inside the timed region)
-    a_h, b_h = ham.host_blocks()
-    host_ham = BseHamiltonian(a_h, b_h, Definiteness.DEFINITE)  # definiteness certified by the generator
+    # end to end through the public API with HOST buffers: upload inside the timed region
+    if world == 1:
+        a_h, b_h = ham.host_blocks()
+        host_ham = BseHamiltonian(a_h, b_h, Definiteness.DEFINITE)  # definiteness certified by the generator
+        h2d = 2 * m * m * 16 + n * cfg.nevex * 16 + 8 * n * 16
+    else:
+        pieces = ds.tile_pieces_host()
+        h2d = world * sum(x.nbytes for pair in pieces.values() for x in pair) + world * (n // world) * cfg.nevex * 16
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r_e2e = bse.solve(host_ham, cfg, device=dev)  # returns numpy v
+    if world == 1:
+        r_e2e = bse.solve(host_ham, cfg, device=dev)  # returns numpy v
+        v_host = r_e2e.v
+    else:
+        ds.load(pieces)
+        r_e2e = ds.solve(cfg)
+        v_host = r_e2e.v.T.contiguous().cpu().numpy().T if rank == 0 else None
     torch.cuda.synchronize()
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    h2d = 2 * m * m * 16 + n * cfg.nevex * 16 + 8 * n * 16
-    d2h = r_e2e.v.nbytes + 8 * (cfg.nevex + 64)
-    host_ham.release_device()
+    d2h = n * nev * 16 + 8 * (cfg.nevex + 64)
+    if world == 1:
+        host_ham.release_device()
 
     peak, peak_src = fp64_peak()
     achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
     total_model = res.ledger.total_flops()
-    if rank == 0 and args.config != "c1":
+    if rank == 0 and args.config != "c1" and world == 1:
         TRACE_FILE.parent.mkdir(exist_ok=True)
         Path(str(TRACE_FILE).format(cfg=args.config)).write_text(json.dumps({
             "total_model_flops": total_model, "iterations": res.iterations_used, "converged": res.converged,
@@ -297,25 +327,33 @@ def run_ours(args, world, rank, local):
                "sample": f"oracle H-application (4 OpenBLAS zgemm, {s['gflops']:.0f} GF/s) at m={m} on {k_sample} "
                          f"columns, extrapolated to this solve's {total_model:.3e} modeled flops"}
     if rank == 0:
+        cfgd = config_dict(args.config)
+        if world > 1:
+            from paper_2601_10557_b200.dist import grid_shape
+
+            p, q = grid_shape(world)
+            cfgd["parallelism"] = f"2D block grid {p}x{q} (A/B tiles + block transposes per GPU), NCCL row/col allreduce"
         line = {
             "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic (GPU generator, reference construction)",
-            "config": config_dict(args.config),
-            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(d2h)},
+            "config": cfgd,
+            "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches // args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "kernel": "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)",
                          "peak_source": peak_src,
-                         "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model), summed over the "
-                                        "solve's filter calls / CUDA-event time of those calls"},
-            "filter_tflops": achieved, "filter_frac_of_fp64_peak": (achieved / peak) if achieved else None,
+                         "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model) per GPU, summed over "
+                                        "the solve's filter calls / CUDA-event (1 GPU) or synchronised (N GPUs) "
+                                        "time of those calls"},
+            "filter_tflops_per_gpu": achieved, "filter_frac_of_fp64_peak": (achieved / peak) if achieved else None,
             "solve": {"iterations": res.iterations_used, "converged": res.converged,
                       "ledger_seconds": {k: round(v, 4) for k, v in res.ledger.seconds.items()},
                       "model_tflop": total_model / 1e12, "generator_s": round(gen_s, 2),
                       "lambda_1": float(res.lambdas[0]), "lambda_nev": float(res.lambdas[-1]),
                       "max_residual": float(res.residual_norms.max()),
+                      "locked_per_iter": [t.locked for t in res.trace],
                       "e2e_iterations": r_e2e.iterations_used,
                       "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},
             "clocks": clk.summary(),
@@ -334,11 +372,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    world, rank, local = dist_setup()
     if args.impl == "reference":
-        run_reference(args, world, rank)
-    else:
-        run_ours(args, world, rank, local)
+        # CPU arm: rank 0 alone works; the other ranks exit at once (no process group needed)
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
+        return
+    world, rank, local = dist_setup()
+    run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
 

@@ -109,6 +109,48 @@ int bse_lanczos_sweep(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, co
 /* Cholesky of the materialised S H (hamiltonian.py:208-218); *h_definite = 1/0. */
 int bse_is_definite(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int* h_definite);
 
+/* ---- building blocks of the 2D-distributed solve (paper_2601_10557_b200/dist.py) ---- */
+/* One tile product of the fused H operator with an axpby epilogue:
+ *   y_half = low_sign^[half==low] * ( alpha * (P-product_half - shift_r * s_half) - beta * p_half )
+ * with U = pa x1 + pb x2 and L' = conj(pa) x2 + conj(pb) x1 (H x = [U; -L']), pa/pb mr x kc tiles.
+ * shift_r = d_shift_col[col] (per column, if non-null) or `shift`, applied on output rows
+ * [shift_lo, shift_hi) only: the rows a 2D tile's input block shares with its output block
+ * (PAPER.md:723-740 communication-avoiding filter).                                            */
+typedef struct {
+  const void* pa;
+  const void* pb;
+  int64_t lda, mr, kc;
+  const void* x1;
+  const void* x2;
+  int64_t ldx, k;
+  void* y1;
+  void* y2;
+  int64_t ldy;
+  const void* s1;
+  const void* s2;
+  int64_t lds, shift_lo, shift_hi;
+  double shift;
+  const double* d_shift_col;
+  const void* p1;
+  const void* p2;
+  int64_t ldp;
+  double alpha, beta, low_sign;
+} bse_hop_tile_args;
+int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* args);
+/* CholQR factor step (ortho.py:115-119): hermitise the summed Gram d_g (k x k), add shift I,
+ * R = chol upper (in d_g), |diag R| -> d_rdiag (nullable), R^{-1} -> d_rinv; *h_info > 0 on failure. */
+int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv, double* d_rdiag, int* h_info);
+/* Small pencil of the hermitian RR (rayleigh_ritz.py:113-137) from the summed W = Q^H S H Q
+ * and G2 = Q2^H Q2: ascending Ritz values (host) and the sorted back-transform L^{-H} y (device). */
+int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec, double* h_lam_min_m);
+/* squared column norms of a rows x k block (device out); x /= sqrt(norm2) per column           */
+int bse_colnorm2(bse_ctx* ctx, const void* d_x, int64_t rows, int64_t k, int64_t ldx, double* d_out);
+int bse_colscale_rsqrt(bse_ctx* ctx, void* d_x, int64_t rows, int64_t k, int64_t ldx, const double* d_norm2);
+/* max |G - I| of a k x k device matrix (ortho.py:124)                                         */
+int bse_defect(bse_ctx* ctx, const void* d_g, int64_t k, double* h_out);
+/* y = S x for a block of 2*half rows (rows >= half negated)                                   */
+int bse_sflip(bse_ctx* ctx, const void* d_x, int64_t ldx, void* d_y, int64_t ldy, int64_t half, int64_t k);
+
 /* ---- synthetic inputs (generate.py:60-83 on the device) -------------------- */
 /* complex normals start_index .. +count of stream `seed` (rng.py:63-81):
  * bit-exact splitmix64 words, device libm Box-Muller (<= ~1 ulp from host). */

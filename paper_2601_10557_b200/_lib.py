@@ -30,6 +30,20 @@ _dbl = C.c_double
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)
 
+class HopTileArgs(C.Structure):
+    """bse_hop_tile_args (include/bse200.h)."""
+
+    _fields_ = [
+        ("pa", _vp), ("pb", _vp), ("lda", _i64), ("mr", _i64), ("kc", _i64),
+        ("x1", _vp), ("x2", _vp), ("ldx", _i64), ("k", _i64),
+        ("y1", _vp), ("y2", _vp), ("ldy", _i64),
+        ("s1", _vp), ("s2", _vp), ("lds", _i64), ("shift_lo", _i64), ("shift_hi", _i64),
+        ("shift", _dbl), ("d_shift_col", _vp),
+        ("p1", _vp), ("p2", _vp), ("ldp", _i64),
+        ("alpha", _dbl), ("beta", _dbl), ("low_sign", _dbl),
+    ]
+
+
 # name -> (restype, argtypes); mirrors include/bse200.h
 _SIGS = {
     "bse_version": (C.c_char_p, []),
@@ -49,6 +63,13 @@ _SIGS = {
     "bse_rr_backup": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
     "bse_lanczos_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _dp, _dp, _ip]),
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
+    "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
+    "bse_chol_rinv": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _vp, _ip]),
+    "bse_rr_pencil": (C.c_int, [_vp, _vp, _vp, _i64, _dp, _vp, _dp]),
+    "bse_colnorm2": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "bse_colscale_rsqrt": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "bse_defect": (C.c_int, [_vp, _vp, _i64, _dp]),
+    "bse_sflip": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64]),
     "bse_complex_normals": (C.c_int, [_vp, _vp, C.c_uint64, _i64, _i64]),
     "bse_complex_normals_t": (C.c_int, [_vp, _vp, C.c_uint64, _i64, _i64]),
     "bse_symmetrize": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int]),

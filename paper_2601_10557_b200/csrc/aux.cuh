@@ -255,6 +255,11 @@ __global__ void set_identity_kernel(zval* a, int k) {
     a[idx] = zval{(idx % k) == (idx / k) ? 1.0 : 0.0, 0.0};
 }
 
+__global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = sqrt(in[i]);
+}
+
 // a_ii += s
 __global__ void add_diag_kernel(zval* a, int k, double s) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;

@@ -175,6 +175,9 @@ bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zva
   a.beta = 0.0;
   a.shift = 0.0;
   a.low_sign = 1.0;
+  a.shift_lo = 0;
+  a.shift_hi = (int)m;
+  a.shift_col = nullptr;
   return a;
 }
 
@@ -441,6 +444,71 @@ int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scra
   return 1;
 }
 
+size_t pencil_ws_bytes(int64_t k) { return 3 * al((size_t)k * k * sizeof(zval)) + al(k * 8) + al(k * 4) + al(64); }
+
+// Small hermitian pencil of the oblique RR (rayleigh_ritz.py:113-137) on k x k device data:
+// w = Q^H S H Q and g2 = Q2^H Q2 (raw sums, overwritten).  Returns ascending Ritz values on the
+// host and the sorted back-transform wvec = L^{-H} y[:, order] on the device.
+void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* wvec, double* h_lam_min_m,
+               Scratch& sc) {
+  const size_t kk = (size_t)k * k;
+  zval* mm = sc.take<zval>(kk);
+  zval* tmp = sc.take<zval>(kk);
+  zval* g = sc.take<zval>(kk);
+  double* d_w = sc.take<double>(k);
+  int* d_perm = sc.take<int>(k);
+  int* d_info = sc.take<int>(4);
+  bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(w, (int)k);
+  check_launch(ctx);
+  bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g2, mm, (int)k);
+  check_launch(ctx);
+  bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
+  check_launch(ctx);
+  // :116-120  |lambda|_min(M) >= 1e-8
+  CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+  heevd(ctx, tmp, (int)k, d_w, false, d_info);
+  std::vector<double> hw(k);
+  to_host(ctx, hw.data(), d_w, k);
+  double lmm = INFINITY;
+  for (double v : hw) lmm = std::min(lmm, std::fabs(v));
+  if (h_lam_min_m) *h_lam_min_m = lmm;
+  if (!(lmm >= 1e-8)) throw BseError(BSE_EHERMITIAN_RQ, "|lambda_min(Q*SQ)| = " + std::to_string(lmm) + " below 1e-8");
+  // :121-126  L = chol(W)
+  if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0)
+    throw BseError(BSE_EHERMITIAN_RQ, "Cholesky of Q*SHQ failed; S*H is not definite on the subspace");
+  // :127-129  G = L^{-1} M L^{-H}, hermitised
+  const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
+  CUDA_OK(cudaMemcpyAsync(g, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+  BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
+                      (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
+  BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, (int)k,
+                      (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
+  bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k);
+  check_launch(ctx);
+  // :130-133  theta, y = eigh(G); lambda = 1/theta
+  heevd(ctx, g, (int)k, d_w, true, d_info);
+  to_host(ctx, hw.data(), d_w, k);
+  double tmin = INFINITY;
+  for (double v : hw) tmin = std::min(tmin, std::fabs(v));
+  if (tmin < 2.220446049250313e-16) throw BseError(BSE_EHERMITIAN_RQ, "reduced spectrum touches zero; cannot invert");
+  std::vector<double> lam(k);
+  for (int64_t i = 0; i < k; ++i) lam[i] = 1.0 / hw[i];
+  std::vector<int> order(k);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lam[a] < lam[b]; });
+  for (int64_t i = 0; i < k; ++i) h_lam[i] = lam[order[i]];
+  // :134  w = L^{-H} y, columns in ascending-lambda order
+  BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, (int)k,
+                      (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
+  {
+    std::vector<double> packed((k + 1) / 2 + 1);
+    std::memcpy(packed.data(), order.data(), sizeof(int) * k);
+    to_device(ctx, reinterpret_cast<double*>(d_perm), packed.data(), (k + 1) / 2);
+  }
+  bse::gather_cols_kernel<<<dim3(1, (unsigned)k), 256, 0, ctx->stream>>>(g, k, wvec, k, k, d_perm);
+  check_launch(ctx);
+}
+
 }  // namespace
 
 // ============================================================================
@@ -639,76 +707,22 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, con
     const zval* q = static_cast<const zval*>(d_q);
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
-    Scratch sc(ctx, al(n * k * sizeof(zval)) + 5 * al(kk * sizeof(zval)) + 2 * al(k * 8) + al(k * 4) + al(64) +
-                        std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)}) + 4096);
+    const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
+    Scratch sc(ctx, al(n * k * sizeof(zval)) + 3 * al(kk * sizeof(zval)) + al(k * 8) + gwsb + pencil_ws_bytes(k) + 4096);
     zval* t = sc.take<zval>(n * k);
     zval* w = sc.take<zval>(kk);
-    zval* mm = sc.take<zval>(kk);
-    zval* tmp = sc.take<zval>(kk);
-    zval* g = sc.take<zval>(kk);
-    zval* wperm = sc.take<zval>(kk);
-    double* d_w = sc.take<double>(k);
+    zval* g2 = sc.take<zval>(kk);
+    zval* wvec = sc.take<zval>(kk);
     double* d_norm = sc.take<double>(k);
-    int* d_perm = sc.take<int>(k);
-    int* d_info = sc.take<int>(4);
-    zval* gws = sc.take<zval>(std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)}) /
-                                  sizeof(zval) + 1);
-    // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T (hermitised) ; M = I - 2 Q2^H Q2 (hermitised)
+    zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
+    // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T ; Q2^H Q2
     apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
-    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(w, (int)k);
-    check_launch(ctx);
-    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, tmp, k, gws);
-    bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(tmp, mm, (int)k);
-    check_launch(ctx);
-    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
-    check_launch(ctx);
-    // :116-120  |lambda|_min(M) >= 1e-8
-    CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
-    heevd(ctx, tmp, (int)k, d_w, false, d_info);
-    std::vector<double> hw(k);
-    to_host(ctx, hw.data(), d_w, k);
-    double lmm = INFINITY;
-    for (double v : hw) lmm = std::min(lmm, std::fabs(v));
-    if (h_lam_min_m) *h_lam_min_m = lmm;
-    if (!(lmm >= 1e-8))
-      throw BseError(BSE_EHERMITIAN_RQ, "|lambda_min(Q*SQ)| = " + std::to_string(lmm) + " below 1e-8");
-    // :121-126  L = chol(W)
-    if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0)
-      throw BseError(BSE_EHERMITIAN_RQ, "Cholesky of Q*SHQ failed; S*H is not definite on the subspace");
-    // :127-129  G = L^{-1} M L^{-H}, hermitised
-    const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
-    CUDA_OK(cudaMemcpyAsync(g, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
-    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
-                        (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
-    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, (int)k,
-                        (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
-    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k);
-    check_launch(ctx);
-    // :130-133  theta, y = eigh(G); lambda = 1/theta
-    heevd(ctx, g, (int)k, d_w, true, d_info);
-    to_host(ctx, hw.data(), d_w, k);
-    double tmin = INFINITY;
-    for (double v : hw) tmin = std::min(tmin, std::fabs(v));
-    if (tmin < 2.220446049250313e-16) throw BseError(BSE_EHERMITIAN_RQ, "reduced spectrum touches zero; cannot invert");
-    std::vector<double> lam(k);
-    for (int64_t i = 0; i < k; ++i) lam[i] = 1.0 / hw[i];
-    std::vector<int> order(k);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lam[a] < lam[b]; });
-    for (int64_t i = 0; i < k; ++i) h_lam[i] = lam[order[i]];
-    // :134-137  w = L^{-H} y ; V = Q w (sorted) ; unit columns
-    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_C, CUBLAS_DIAG_NON_UNIT, (int)k,
-                        (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
-    {
-      std::vector<double> tmpd((k + 1) / 2 + 1);
-      static_assert(sizeof(int) * 2 == sizeof(double), "packing");
-      std::memcpy(tmpd.data(), order.data(), sizeof(int) * k);
-      to_device(ctx, reinterpret_cast<double*>(d_perm), tmpd.data(), (k + 1) / 2);
-    }
-    bse::gather_cols_kernel<<<dim3(1, (unsigned)k), 256, 0, ctx->stream>>>(g, k, wperm, k, k, d_perm);
-    check_launch(ctx);
-    zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, q, ldq, wperm, k, 0.0, vout, ldvout, gws);
+    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
+    Scratch rest = sc;
+    rr_pencil(ctx, w, g2, k, h_lam, wvec, h_lam_min_m, rest);
+    // :135-136  V = Q w (sorted) ; unit columns
+    zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, q, ldq, wvec, k, 0.0, vout, ldvout, gws);
     bse::colnorm_kernel<<<(int)k, 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
     check_launch(ctx);
     bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
@@ -879,6 +893,123 @@ int bse_is_definite(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int*
     bse::materialize_sh_kernel<<<grid1d(n * n), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ab), lda, m, sh);
     check_launch(ctx);
     *h_definite = potrf(ctx, sh, (int)n, CUBLAS_FILL_MODE_LOWER, d_info) == 0 ? 1 : 0;
+  });
+}
+
+int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* t) {
+  return guarded(ctx, [&] {
+    if (!t) throw BseError(BSE_EVALIDATION, "null args");
+    if (t->k <= 0 || t->mr <= 0) return;
+    bse::HopArgs a{};
+    a.pa = static_cast<const zval*>(t->pa);
+    a.pb = static_cast<const zval*>(t->pb);
+    a.lda = t->lda;
+    a.mr = (int)t->mr;
+    a.kc = (int)t->kc;
+    a.x1 = static_cast<const zval*>(t->x1);
+    a.x2 = static_cast<const zval*>(t->x2);
+    a.ldx = t->ldx;
+    a.k = (int)t->k;
+    a.y1 = static_cast<zval*>(t->y1);
+    a.y2 = static_cast<zval*>(t->y2);
+    a.ldy = t->ldy;
+    a.s1 = static_cast<const zval*>(t->s1);
+    a.s2 = static_cast<const zval*>(t->s2);
+    a.lds = t->lds;
+    a.shift_lo = (int)t->shift_lo;
+    a.shift_hi = (int)t->shift_hi;
+    a.shift = t->shift;
+    a.shift_col = t->d_shift_col;
+    a.p1 = static_cast<const zval*>(t->p1);
+    a.p2 = static_cast<const zval*>(t->p2);
+    a.ldp = t->ldp;
+    a.alpha = t->alpha;
+    a.beta = t->beta;
+    a.low_sign = t->low_sign;
+    if (a.beta != 0.0 && (!a.p1 || !a.p2)) throw BseError(BSE_EVALIDATION, "beta != 0 needs p1/p2");
+    if ((a.shift != 0.0 || a.shift_col) && a.shift_hi > a.shift_lo && (!a.s1 || !a.s2))
+      throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
+    if (a.kc <= 0) throw BseError(BSE_EVALIDATION, "empty contraction");
+    launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+  });
+}
+
+int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv, double* d_rdiag, int* h_info) {
+  return guarded(ctx, [&] {
+    if (k <= 0) return;
+    Scratch sc(ctx, al(64));
+    int* d_info = sc.take<int>(4);
+    zval* g = static_cast<zval*>(d_g);
+    bse::hermitize_kernel<<<grid1d(k * k), 256, 0, ctx->stream>>>(g, (int)k);
+    check_launch(ctx);
+    if (shift != 0.0) {
+      bse::add_diag_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(g, (int)k, shift);
+      check_launch(ctx);
+    }
+    const int info = potrf(ctx, g, (int)k, CUBLAS_FILL_MODE_UPPER, d_info);
+    *h_info = info;
+    if (info != 0) return;
+    if (d_rdiag) {
+      bse::absdiag_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(g, (int)k, d_rdiag);
+      check_launch(ctx);
+    }
+    zval* rinv = static_cast<zval*>(d_rinv);
+    bse::set_identity_kernel<<<grid1d(k * k), 256, 0, ctx->stream>>>(rinv, (int)k);
+    check_launch(ctx);
+    const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
+    BLAS_OK(cublasZtrsm(ctx->blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
+                        (int)k, &z1, cz(g), (int)k, cz(rinv), (int)k));
+  });
+}
+
+int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec, double* h_lam_min_m) {
+  return guarded(ctx, [&] {
+    if (k <= 0) return;
+    Scratch sc(ctx, pencil_ws_bytes(k) + 4096);
+    rr_pencil(ctx, static_cast<zval*>(d_w), static_cast<zval*>(d_g2), k, h_lam, static_cast<zval*>(d_wvec),
+              h_lam_min_m, sc);
+  });
+}
+
+int bse_colnorm2(bse_ctx* ctx, const void* d_x, int64_t rows, int64_t k, int64_t ldx, double* d_out) {
+  return guarded(ctx, [&] {
+    if (k <= 0) return;
+    bse::frob2_kernel<<<(int)k, 256, 0, ctx->stream>>>(static_cast<const zval*>(d_x), ldx, rows, d_out);
+    check_launch(ctx);
+  });
+}
+
+int bse_colscale_rsqrt(bse_ctx* ctx, void* d_x, int64_t rows, int64_t k, int64_t ldx, const double* d_norm2) {
+  return guarded(ctx, [&] {
+    if (k <= 0 || rows <= 0) return;
+    Scratch sc(ctx, al(k * 8));
+    double* nrm = sc.take<double>(k);
+    bse::sqrt_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(d_norm2, nrm, (int)k);
+    check_launch(ctx);
+    bse::colscale_inv_kernel<<<dim3(grid1d(rows, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(
+        static_cast<zval*>(d_x), ldx, rows, nrm);
+    check_launch(ctx);
+  });
+}
+
+int bse_defect(bse_ctx* ctx, const void* d_g, int64_t k, double* h_out) {
+  return guarded(ctx, [&] {
+    if (k <= 0) {
+      *h_out = 0.0;
+      return;
+    }
+    Scratch sc(ctx, al(1024 * 8));
+    double* part = sc.take<double>(1024);
+    *h_out = defect_to_host(ctx, static_cast<const zval*>(d_g), (int)k, part);
+  });
+}
+
+int bse_sflip(bse_ctx* ctx, const void* d_x, int64_t ldx, void* d_y, int64_t ldy, int64_t half, int64_t k) {
+  return guarded(ctx, [&] {
+    if (k <= 0 || half <= 0) return;
+    bse::sflip_copy_kernel<<<grid1d(2 * half * k), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_x), ldx,
+                                                                           static_cast<zval*>(d_y), ldy, half, k);
+    check_launch(ctx);
   });
 }
 

@@ -46,6 +46,10 @@ struct HopArgs {
   const zval* p2;
   int64_t ldp;
   double alpha, beta, shift, low_sign;
+  // the shift term applies to output rows [shift_lo, shift_hi) only (the rows this tile's
+  // input block shares with its output block in the 2D layout); per-column shifts when set
+  int shift_lo, shift_hi;
+  const double* shift_col;
   // residual mode
   const double* lam;  // per column
   double* partial;    // [gridDim.y][k]
@@ -186,13 +190,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
           // H x rows: up = U, low = -L'
           double hu_r = ur[i][j][h], hu_i = ui[i][j][h];
           double hl_r = -lr[i][j][h], hl_i = -li[i][j][h];
-          if (a.shift != 0.0) {
+          if ((a.shift != 0.0 || a.shift_col) && row >= a.shift_lo && row < a.shift_hi) {
+            const double sh = a.shift_col ? a.shift_col[col] : a.shift;
             const zval s1 = a.s1[(int64_t)col * a.lds + row];
             const zval s2 = a.s2[(int64_t)col * a.lds + row];
-            hu_r = hu_r - a.shift * s1.re;
-            hu_i = hu_i - a.shift * s1.im;
-            hl_r = hl_r - a.shift * s2.re;
-            hl_i = hl_i - a.shift * s2.im;
+            hu_r = hu_r - sh * s1.re;
+            hu_i = hu_i - sh * s1.im;
+            hl_r = hl_r - sh * s2.re;
+            hl_i = hl_i - sh * s2.im;
           }
           zval o1{a.alpha * hu_r, a.alpha * hu_i}, o2{a.alpha * hl_r, a.alpha * hl_i};
           if (a.beta != 0.0) {

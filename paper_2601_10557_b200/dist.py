@@ -1,0 +1,655 @@
+"""2D block-distributed pseudo-hermitian ChASE over a p x q grid of GPUs.
+
+The scheme of PAPER.md:723-740 (not shipped by the reference):
+
+* GPU (I, J) of a p x q grid (8 -> 2 x 4, 4 -> 2 x 2, 2 -> 1 x 2) owns the
+  tiles A[R_I, C_J], B[R_I, C_J] and their block transposes A[C_J, R_I] =
+  A[R_I, C_J]^H, B[C_J, R_I] = B[R_I, C_J]^T (A hermitian, B symmetric), i.e.
+  only blocks of A and B — 4 m^2 / (p q) x 16 bytes per GPU.
+* Vectors live in one of two layouts: "col" (rows C_J of both halves,
+  replicated down the column communicator) and "row" (rows R_I, replicated
+  along the row communicator).  A forward tile product maps col -> row and is
+  summed over the row communicator; the transposed-tile product maps row ->
+  col and is summed over the column communicator (the block form of
+  H V = W <=> H^* S V = S W).  The filter alternates the two, so an even
+  degree returns V to its starting layout without ever moving A or B.
+* The Chebyshev shift term -c Y is folded into the partial product on the
+  rows where a tile's input and output blocks intersect, the -beta Y_prev
+  term is added by one designated member, so the summed partials ARE
+  Y_{j+1}: the whole recurrence is one fused DMMA GEMM + one allreduce per
+  step, with two buffers (one per layout) and no copies.
+* CholQR Grams, the projection against the locked vectors, W = Q^H S H Q,
+  Q2^H Q2 and the residual norms are local partial products plus ONE
+  allreduce each; the k x k pencil is solved redundantly on every GPU
+  (PAPER.md:725).  Q is allgathered once per iteration for the RR.
+
+Everything device-side goes through an ``ops`` object: ``CudaOps`` (the bse200
+C ABI) in production; the CPU gloo tests substitute a torch reference.
+Vectors are held as "storage" tensors of shape (k, rows) (column-major
+matrices rows x k, leading dimension = rows), so column slices are contiguous
+for the collectives.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, rng
+from .chebyshev import FilterConfig
+from .errors import HermitianRqError, LanczosBreakdownError, NumericalError, RankDeficiencyError, ValidationError
+from .lanczos import MAX_RESTARTS, SAFETY_INFLATION, SpectralBounds, _cutoff, update_cutoff
+from .metrics import PhaseLedger
+from .rayleigh_ritz import lock_converged, RitzSet
+from .solver import SolveResult, SolverConfig, TraceRecord, TAG_LANCZOS, TAG_SUBSPACE
+
+ZB = 16  # bytes per complex128
+
+
+def grid_shape(world: int) -> tuple[int, int]:
+    """Grid as square as possible with p <= q."""
+    p = int(math.isqrt(world))
+    while world % p:
+        p -= 1
+    return p, world // p
+
+
+def split(m: int, parts: int) -> list[int]:
+    base, extra = divmod(m, parts)
+    edges = [0]
+    for i in range(parts):
+        edges.append(edges[-1] + base + (1 if i < extra else 0))
+    return edges
+
+
+class Grid:
+    """Block ownership of the m x m index space on a p x q grid."""
+
+    def __init__(self, m: int, world: int, rank: int, p: int | None = None, q: int | None = None):
+        if p is None or q is None:
+            p, q = grid_shape(world)
+        if p * q != world:
+            raise ValidationError(f"grid {p}x{q} does not match world size {world}")
+        self.m, self.p, self.q, self.world, self.rank = m, p, q, world, rank
+        self.I, self.J = divmod(rank, q)
+        self.re, self.ce = split(m, p), split(m, q)
+        self.r0, self.r1 = self.re[self.I], self.re[self.I + 1]
+        self.c0, self.c1 = self.ce[self.J], self.ce[self.J + 1]
+        self.nr, self.nc = self.r1 - self.r0, self.c1 - self.c0
+        # rows shared by the output and input blocks of a forward (col -> row) product,
+        # in output-row coordinates; the transposed product uses the same global interval
+        lo, hi = max(self.r0, self.c0), min(self.r1, self.c1)
+        self.diag = (lo, hi) if hi > lo else (0, 0)
+
+    def row_members(self) -> list[int]:
+        return [self.I * self.q + j for j in range(self.q)]
+
+    def col_members(self) -> list[int]:
+        return [i * self.q + self.J for i in range(self.p)]
+
+
+class Comm:
+    """Row / column communicators of the grid (torch.distributed groups; NCCL on GPUs, gloo in tests)."""
+
+    def __init__(self, grid: Grid):
+        self.g = grid
+        self.row = self.col = None
+        if grid.world > 1:
+            import torch.distributed as dist
+
+            self.dist = dist
+            rows = [dist.new_group([i * grid.q + j for j in range(grid.q)]) for i in range(grid.p)]
+            cols = [dist.new_group([i * grid.q + j for i in range(grid.p)]) for j in range(grid.q)]
+            self.row, self.col = rows[grid.I], cols[grid.J]
+
+    @staticmethod
+    def _real(t):
+        import torch
+
+        return torch.view_as_real(t) if t.is_complex() else t
+
+    def sum_row(self, t) -> None:
+        if self.g.q > 1:
+            self.dist.all_reduce(self._real(t), group=self.row)
+
+    def sum_col(self, t) -> None:
+        if self.g.p > 1:
+            self.dist.all_reduce(self._real(t), group=self.col)
+
+    def max_all(self, t) -> None:
+        if self.g.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+
+    def gather(self, t, group: str) -> list:
+        """allgather of equally shaped contiguous tensors within the row / col group."""
+        import torch
+
+        size = self.g.q if group == "row" else self.g.p
+        if size == 1:
+            return [t]
+        outs = [torch.empty_like(t) for _ in range(size)]
+        self.dist.all_gather([self._real(o) for o in outs], self._real(t), group=self.row if group == "row" else self.col)
+        return outs
+
+
+# ----------------------------------------------------------------------------- device ops (C ABI)
+class CudaOps:
+    """Thin wrappers over the bse200 C ABI for the distributed algorithm."""
+
+    def __init__(self, device):
+        import torch
+
+        self.torch = torch
+        self.device = device
+        self.ctx = _lib.Context.get(device.index)
+
+    def empty(self, k: int, rows: int):
+        return self.torch.empty((k, rows), dtype=self.torch.complex128, device=self.device)
+
+    def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
+            p=None, low_sign=1.0):
+        """y (storage k x 2 mr) = low_sign^{low} (alpha (tile-product of x - shift s) - beta p)."""
+        k = x.shape[0]
+        mr, kc = tile.mr, tile.kc
+        xa, ya = x.data_ptr(), y.data_ptr()
+        args = _lib.HopTileArgs()
+        args.pa, args.pb, args.lda, args.mr, args.kc = tile.pa, tile.pb, tile.lda, mr, kc
+        args.x1, args.x2, args.ldx, args.k = xa, xa + kc * ZB, x.stride(0), k
+        args.y1, args.y2, args.ldy = ya, ya + mr * ZB, y.stride(0)
+        lo, hi = shift_rows
+        if (shift != 0.0 or shift_col is not None) and hi > lo:
+            args.s1, args.s2, args.lds = xa + s_off * ZB, xa + (kc + s_off) * ZB, x.stride(0)
+            args.shift_lo, args.shift_hi = lo, hi
+            args.shift = shift
+            args.d_shift_col = shift_col.data_ptr() if shift_col is not None else None
+        if beta != 0.0:
+            pa_ = p.data_ptr()
+            args.p1, args.p2, args.ldp = pa_, pa_ + mr * ZB, p.stride(0)
+        args.alpha, args.beta, args.low_sign = alpha, beta, low_sign
+        self.ctx.call("bse_hop_tile", ctypes.byref(args))
+
+    def gram(self, a, b):
+        """a^H b for storage blocks with equal rows -> (k2, k1) storage of the k1 x k2 result."""
+        k1, rows = a.shape
+        k2 = b.shape[0]
+        out = self.empty(k2, k1)
+        self.ctx.call("bse_zgemm_cn", k1, k2, rows, 1.0, _lib.dptr(a), a.stride(0), _lib.dptr(b), b.stride(0), 0.0,
+                      _lib.dptr(out), k1)
+        return out
+
+    def nn(self, a, w, out=None, alpha=1.0, beta=0.0):
+        """out = alpha a @ W + beta out ; a storage (k1, rows), w storage (k2, k1) of a k1 x k2 matrix."""
+        k1, rows = a.shape
+        k2 = w.shape[0]
+        if out is None:
+            out = self.empty(k2, rows)
+        self.ctx.call("bse_zgemm_nn", rows, k2, k1, alpha, _lib.dptr(a), a.stride(0), _lib.dptr(w), w.stride(0),
+                      beta, _lib.dptr(out), out.stride(0))
+        return out
+
+    def chol_rinv(self, g, shift=0.0, rdiag=None):
+        k = g.shape[0]
+        rinv = self.empty(k, k)
+        info = ctypes.c_int(0)
+        self.ctx.call("bse_chol_rinv", _lib.dptr(g), k, shift, _lib.dptr(rinv),
+                      _lib.dptr(rdiag) if rdiag is not None else None, ctypes.byref(info))
+        return rinv, info.value
+
+    def rr_pencil(self, w, g2):
+        k = w.shape[0]
+        lam = np.zeros(k)
+        wvec = self.empty(k, k)
+        lmm = ctypes.c_double(0.0)
+        self.ctx.call("bse_rr_pencil", _lib.dptr(w), _lib.dptr(g2), k, _lib.hptr(lam), _lib.dptr(wvec),
+                      ctypes.byref(lmm))
+        return lam, wvec, lmm.value
+
+    def colnorm2(self, x):
+        out = self.torch.empty(x.shape[0], dtype=self.torch.float64, device=self.device)
+        self.ctx.call("bse_colnorm2", _lib.dptr(x), x.shape[1], x.shape[0], x.stride(0), _lib.dptr(out))
+        return out
+
+    def colscale_rsqrt(self, x, n2):
+        self.ctx.call("bse_colscale_rsqrt", _lib.dptr(x), x.shape[1], x.shape[0], x.stride(0), _lib.dptr(n2))
+
+    def defect(self, g) -> float:
+        out = ctypes.c_double(0.0)
+        self.ctx.call("bse_defect", _lib.dptr(g), g.shape[0], ctypes.byref(out))
+        return out.value
+
+    def sflip(self, x):
+        y = self.empty(x.shape[0], x.shape[1])
+        self.ctx.call("bse_sflip", _lib.dptr(x), x.stride(0), _lib.dptr(y), y.stride(0), x.shape[1] // 2, x.shape[0])
+        return y
+
+
+@dataclass
+class Tile:
+    """[P_A | P_B] of one tile product: pa, pb device addresses, mr x kc each, leading dim lda."""
+
+    buf: object
+    pa: int
+    pb: int
+    lda: int
+    mr: int
+    kc: int
+
+
+def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
+    """Forward tile (A, B)[R_I, C_J] and transposed tile (A, B)[C_J, R_I] from full (host or device)
+    blocks; each stored as one column-major [A_t | B_t] buffer."""
+    torch = ops.torch
+
+    def one(rows, cols):
+        r0, r1 = rows
+        c0, c1 = cols
+        mr, kc = r1 - r0, c1 - c0
+        buf = torch.empty((2 * kc, mr), dtype=torch.complex128, device=ops.device)  # storage of mr x 2kc
+        for h, blk in enumerate((a_blocks, b_blocks)):
+            src = blk[r0:r1, c0:c1]
+            if isinstance(src, np.ndarray):
+                src = torch.from_numpy(np.ascontiguousarray(src.T)).T
+            buf[h * kc:(h + 1) * kc].copy_(src.T)
+        addr = buf.data_ptr()
+        return Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc)
+
+    fwd = one((grid.r0, grid.r1), (grid.c0, grid.c1))
+    trn = one((grid.c0, grid.c1), (grid.r0, grid.r1))
+    return fwd, trn
+
+
+# ----------------------------------------------------------------------------- distributed solver
+class DistSolver:
+    """SPMD solve on one rank of the grid; every rank calls it with the same config."""
+
+    def __init__(self, grid: Grid, comm: Comm, ops, fwd: Tile, trn: Tile):
+        self.g, self.c, self.ops, self.fwd, self.trn = grid, comm, ops, fwd, trn
+        self.torch = ops.torch
+
+    # ---- layout helpers -----------------------------------------------------------------
+    def col_rows(self, full_storage):
+        """col layout [X1[C_J]; X2[C_J]] of a full (k, n) storage block."""
+        g, m = self.g, self.g.m
+        return self.torch.cat([full_storage[:, g.c0:g.c1], full_storage[:, m + g.c0:m + g.c1]], dim=1).contiguous()
+
+    def assemble_from_col(self, local):
+        """allgather the col-layout blocks along the row communicator -> full (k, n) storage."""
+        g, torch = self.g, self.torch
+        k = local.shape[0]
+        mx = max(g.ce[j + 1] - g.ce[j] for j in range(g.q))
+        pad = torch.zeros((k, 2 * mx), dtype=local.dtype, device=local.device)
+        pad[:, :g.nc] = local[:, :g.nc]
+        pad[:, mx:mx + g.nc] = local[:, g.nc:]
+        parts = self.c.gather(pad, "row")
+        full = torch.empty((k, 2 * g.m), dtype=local.dtype, device=local.device)
+        for j, part in enumerate(parts):
+            a, b = g.ce[j], g.ce[j + 1]
+            full[:, a:b] = part[:, :b - a]
+            full[:, g.m + a:g.m + b] = part[:, mx:mx + b - a]
+        return full
+
+    def assemble_from_row(self, local):
+        """allgather the row-layout blocks along the column communicator -> full (k, n) storage."""
+        g, torch = self.g, self.torch
+        k = local.shape[0]
+        mx = max(g.re[i + 1] - g.re[i] for i in range(g.p))
+        pad = torch.zeros((k, 2 * mx), dtype=local.dtype, device=local.device)
+        pad[:, :g.nr] = local[:, :g.nr]
+        pad[:, mx:mx + g.nr] = local[:, g.nr:]
+        parts = self.c.gather(pad, "col")
+        full = torch.empty((k, 2 * g.m), dtype=local.dtype, device=local.device)
+        for i, part in enumerate(parts):
+            a, b = g.re[i], g.re[i + 1]
+            full[:, a:b] = part[:, :b - a]
+            full[:, g.m + a:g.m + b] = part[:, mx:mx + b - a]
+        return full
+
+    def row_rows(self, full_storage):
+        g, m = self.g, self.g.m
+        return self.torch.cat([full_storage[:, g.r0:g.r1], full_storage[:, m + g.r0:m + g.r1]], dim=1).contiguous()
+
+    # ---- H products -----------------------------------------------------------------------
+    def forward(self, x_col, y_row, **kw):
+        """col -> row partial product, summed over the row communicator into y_row."""
+        g = self.g
+        lo, hi = g.diag
+        self.ops.hop(self.fwd, x_col, y_row, shift_rows=(lo - g.r0, hi - g.r0), s_off=g.r0 - g.c0, **kw)
+        self.c.sum_row(y_row)
+
+    def transposed(self, x_row, y_col, **kw):
+        """row -> col partial product (block-transposed tiles), summed over the column communicator."""
+        g = self.g
+        lo, hi = g.diag
+        self.ops.hop(self.trn, x_row, y_col, shift_rows=(lo - g.c0, hi - g.c0), s_off=g.c0 - g.r0, **kw)
+        self.c.sum_col(y_col)
+
+    def chebyshev(self, v_col, cfg: FilterConfig, row_buf):
+        """p(H) v in place (col layout); row_buf: (k, 2 nr) scratch.  chebyshev.py:58-74."""
+        c, e = cfg.center, cfg.half_width
+        s1 = e / (cfg.scale_ref - c)
+        s = s1
+        k = v_col.shape[0]
+        yr = row_buf[:k]
+        # step 1: col -> row, Y1 = (s1/e)(H Y0 - c Y0)
+        self.forward(v_col, yr, alpha=s1 / e, shift=c)
+        src, dst = yr, v_col
+        for step in range(2, cfg.degree + 1):
+            sn = 1.0 / (2.0 / s1 - s)
+            # Y_{j+1} = (2 sn / e)(H Y_j - c Y_j) - (s sn) Y_{j-1}; Y_{j-1} lives in dst (in place)
+            owner = self._beta_owner(step)
+            kw = dict(alpha=2.0 * sn / e, shift=c, beta=(s * sn) if owner else 0.0, p=dst if owner else None)
+            if step % 2 == 0:
+                self.transposed(src, dst, **kw)
+            else:
+                self.forward(src, dst, **kw)
+            src, dst = dst, src
+            s = sn
+        return v_col  # even degree: the result is back in the col buffer
+
+    def _beta_owner(self, step: int) -> bool:
+        # the -beta Y_prev term is added once per reduction group
+        return (self.g.I == 0) if step % 2 == 0 else (self.g.J == 0)
+
+    # ---- orthonormalisation -----------------------------------------------------------------
+    def _gram_row(self, a, b=None):
+        gm = self.ops.gram(a, a if b is None else b)
+        self.c.sum_row(gm)
+        return gm
+
+    def cholqr(self, q_col):
+        """Distributed CholQR2 (+ shifted CholQR3 fallback) of a col-layout block; returns (q, method)."""
+        x0 = q_col.clone()
+        q = q_col
+        ok = True
+        for _ in range(2):
+            rinv, info = self.ops.chol_rinv(self._gram_row(q))
+            if info != 0:
+                ok = False
+                break
+            q = self.ops.nn(q, rinv)
+        if ok and self.ops.defect(self._gram_row(q)) <= 1e-8:
+            return q, "cholqr"
+        # shifted CholQR3 on the original block
+        n2 = self.ops.colnorm2(x0)
+        self.c.sum_row(n2)
+        k = x0.shape[0]
+        n = 2 * self.g.m
+        shift = 11.0 * (n * k + k * (k + 1)) * 2.0**-53 * float(n2.sum().item())
+        rd = self.torch.empty(k, dtype=self.torch.float64, device=x0.device)
+        prod = np.ones(k)
+        q = x0
+        for sh in (shift, 0.0, 0.0):
+            rinv, info = self.ops.chol_rinv(self._gram_row(q), shift=sh, rdiag=rd)
+            if info != 0 or not shift > 0:
+                raise RankDeficiencyError("columns are numerically rank deficient (shifted Cholesky failed)")
+            prod *= rd.cpu().numpy()
+            q = self.ops.nn(q, rinv)
+        if not prod.min() > 1e-10 * prod.max():
+            raise RankDeficiencyError(f"columns are numerically rank deficient (diag ratio {prod.min():.3e})")
+        if not self.ops.defect(self._gram_row(q)) <= 1e-8:
+            raise RankDeficiencyError("orthonormalization failed")
+        return q, "shifted_cholqr"
+
+    def s_orthonormalize(self, v_col, locked_col):
+        """ortho.py:132-158 distributed: project out span(S Y), then CholQR2 (col layout)."""
+        if locked_col is not None and locked_col.shape[0]:
+            basis, _ = self.cholqr(self.ops.sflip(locked_col))
+            proj = self._gram_row(basis, v_col)  # l x k
+            self.ops.nn(basis, proj, out=v_col, alpha=-1.0, beta=1.0)
+        return self.cholqr(v_col)
+
+    # ---- Rayleigh-Ritz + residuals ------------------------------------------------------------
+    def rayleigh_ritz(self, q_col, row_buf):
+        """rayleigh_ritz.py:98-143 distributed; returns (lam, v_col, lambda_min_m)."""
+        k = q_col.shape[0]
+        t_row = row_buf[:k]
+        self.forward(q_col, t_row, low_sign=-1.0)  # T = S H Q (rows R_I)
+        q_full = self.assemble_from_col(q_col)
+        w = self.ops.gram(self.row_rows(q_full), t_row)
+        self.c.sum_col(w)
+        g2 = self.ops.gram(q_col[:, self.g.nc:], q_col[:, self.g.nc:])
+        self.c.sum_row(g2)
+        lam, wvec, lmm = self.ops.rr_pencil(w, g2)
+        v = self.ops.nn(q_col, wvec)
+        n2 = self.ops.colnorm2(v)
+        self.c.sum_row(n2)
+        self.ops.colscale_rsqrt(v, n2)
+        return lam, v, lmm
+
+    def residuals(self, v_col, lam, row_buf) -> np.ndarray:
+        k = v_col.shape[0]
+        r_row = row_buf[:k]
+        lam_d = self.torch.as_tensor(np.ascontiguousarray(lam), dtype=self.torch.float64, device=v_col.device)
+        self.forward(v_col, r_row, shift_col=lam_d)  # R = H V - V Lambda (rows R_I)
+        n2 = self.ops.colnorm2(r_row)
+        self.c.sum_col(n2)
+        return np.sqrt(n2.cpu().numpy())
+
+    # ---- Lanczos (lanczos.py:53-142) ------------------------------------------------------------
+    def matvec_full(self, x_full):
+        """H x for a full (1, n) storage vector; returns the full product on every rank."""
+        y_row = self.ops.empty(1, 2 * self.g.nr)
+        self.forward(self.col_rows(x_full), y_row)
+        return self.assemble_from_row(y_row)
+
+    def lanczos(self, nevex: int, steps: int, seed: int, ledger: PhaseLedger) -> SpectralBounds:
+        torch = self.torch
+        n, m = 2 * self.g.m, self.g.m
+        sgn = torch.ones(n, dtype=torch.float64, device=self.ops.device)
+        sgn[m:] = -1.0
+
+        def sdot(x, y):  # Re vdot(S x, y)
+            return float(torch.sum(sgn * (x.real * y.real + x.imag * y.imag)).item())
+
+        def sweep(start):
+            hr = self.matvec_full(start)
+            ledger.add_flops("lanczos", 8.0 * n * n)
+            nrm2 = sdot(hr[0], start[0])
+            if not nrm2 > 0:
+                from .errors import IndefiniteError
+
+                raise IndefiniteError("start vector has non-positive S*H norm; matrix is not definite")
+            sc = math.sqrt(nrm2)
+            q, z = start / sc, hr / sc
+            q_old = torch.zeros_like(q)
+            beta_prev, al, be = 0.0, [], []
+            for j in range(steps):
+                al.append(sdot(z[0], z[0]))
+                if j == steps - 1:
+                    break
+                w = z - al[-1] * q - beta_prev * q_old
+                gv = self.matvec_full(w)
+                ledger.add_flops("lanczos", 8.0 * n * n)
+                b2 = sdot(gv[0], w[0])
+                if b2 <= (1e-14 * max(1.0, max(abs(a) for a in al), beta_prev)) ** 2:
+                    break
+                beta = math.sqrt(b2)
+                be.append(beta)
+                q_old, q = q, w / beta
+                z = gv / beta
+                beta_prev = beta
+            return np.array(al), np.array(be), len(al) < steps
+
+        al = be = np.empty(0)
+        for attempt in range(MAX_RESTARTS + 1):
+            st = torch.from_numpy(rng.complex_normals(rng.substream(seed, attempt), n)).to(self.ops.device)[None, :]
+            al, be, early = sweep(st)
+            if not early or len(al) >= min(4, steps):
+                break
+        if len(al) < min(4, steps):
+            raise LanczosBreakdownError(f"Lanczos broke down before {min(4, steps)} steps")
+        if len(al) % 2:
+            al = al[:-1]
+            be = be[: len(al) - 1]
+        import scipy.linalg as sla
+
+        theta, y = sla.eigh_tridiagonal(al, be)
+        wts = y[0, :] ** 2
+        mu_1 = float(theta[0]) - SAFETY_INFLATION * abs(float(theta[0]))
+        cut = float(min(max(_cutoff(theta, wts, nevex, n), mu_1), -mu_1))
+        return SpectralBounds(mu_1=mu_1, mu_nevex=cut, mu_n=-mu_1, steps=len(al), ritz_values=theta,
+                              ritz_weights=wts)
+
+    # ---- outer loop (solver.py:125-250) -----------------------------------------------------------
+    def solve(self, cfg: SolverConfig) -> SolveResult:
+        torch = self.torch
+        g = self.g
+        n, nevex, nev, tol = 2 * g.m, cfg.nevex, cfg.nev, cfg.tol
+        cfg.validate(n)
+        if cfg.rr_variant == "backup":
+            raise NumericalError("the backup projection is not distributed yet (rr_variant='backup')")
+        ledger = PhaseLedger()
+        with ledger.timing("lanczos"):
+            bounds = self.lanczos(nevex, cfg.lanczos_steps, rng.substream(cfg.seed, TAG_LANCZOS), ledger)
+        normalizer = abs(bounds.mu_1) if cfg.rel_res else 1.0
+        v = start_block_col(rng.substream(cfg.seed, TAG_SUBSPACE), n, nevex, g, self.ops)
+        row_buf = self.ops.empty(nevex, 2 * g.nr)
+        locked = self.ops.empty(nev, 2 * g.nc)
+        nlock, lvals, lres, trace = 0, [], [], []
+        converged, it_used, current = False, 0, bounds
+        lam = res = act = None
+        for it in range(1, cfg.maxiter + 1):
+            it_used = it
+            before = ledger.total_flops()
+            k = nevex - nlock
+            fcfg = FilterConfig.from_bounds(current, cfg.deg, cfg.plain_kernel_only)
+            with ledger.timing("filter"):
+                self.chebyshev(v, fcfg, row_buf)
+            ledger.add_flops("filter", cfg.deg * 8.0 * n * n * k)
+            with ledger.timing("ortho"):
+                v, _ = self.s_orthonormalize(v, locked[:nlock] if nlock else None)
+            if nlock:
+                ledger.add_flops("ortho", 16.0 * n * nlock * k)
+            ledger.add_flops("ortho", 2 * (8.0 * n * k * k + 4.0 * n * k * k))
+            with ledger.timing("rr"):
+                try:
+                    lam, vecs, lmm = self.rayleigh_ritz(v, row_buf)
+                except HermitianRqError as exc:
+                    raise NumericalError(f"hermitian projection failed at iteration {it} (distributed backup "
+                                         f"projection not available): {exc}") from exc
+            ledger.add_flops("rr", 8.0 * n * n * k + 8.0 * n * n * k + 12.0 * n * k * k + 16.0 * k**3)
+            with ledger.timing("residuals"):
+                res = self.residuals(vecs, lam, row_buf)
+            ledger.add_flops("residuals", 8.0 * n * n * k)
+            ritz = RitzSet(values=lam, vectors=None, residual_norms=res)
+            new, act = lock_converged(ritz, tol, nev - nlock, normalizer)
+            cnt = new.size
+            if cnt:
+                locked[nlock:nlock + cnt].copy_(vecs[:cnt])
+                nlock += cnt
+                lvals.extend(lam[:cnt].tolist())
+                lres.extend(res[:cnt].tolist())
+            unl = res[act]
+            trace.append(TraceRecord(it=it, locked=nlock, k=k, max_res=float(res.max()),
+                                     min_res_unlocked=float(unl.min()) if unl.size else 0.0,
+                                     mu_nevex=current.mu_nevex, variant="hermitian", lambda_min_m=lmm,
+                                     flops=ledger.total_flops() - before))
+            if nlock >= nev:
+                converged = True
+                break
+            v = vecs[cnt:]
+            act_vals = lam[act]
+            still = act_vals[~ritz.converged[act]]
+            cand = still if still.size else act_vals
+            cand = np.minimum(cand[cand >= current.mu_1], 0.0)
+            if cand.size:
+                current = update_cutoff(current, cand)
+        if converged:
+            vals, blocks, resid = np.array(lvals), locked[:nlock], np.array(lres)
+        else:
+            miss = nev - nlock
+            vals = np.concatenate([lvals, lam[act][:miss]])
+            blocks = torch.cat([locked[:nlock], vecs[torch.as_tensor(act[:miss], device=vecs.device)]], dim=0)
+            resid = np.concatenate([lres, res[act][:miss]])
+        order = np.argsort(vals, kind="stable")[:nev]
+        full = self.assemble_from_col(blocks[torch.as_tensor(order, device=blocks.device)].contiguous())
+        return SolveResult(lambdas=vals[order], v=full, residual_norms=resid[order], iterations_used=it_used,
+                           converged=converged, trace=trace, bounds=bounds, ledger=ledger, backup_events=0)
+
+
+def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):
+    """Rows C_J of both halves of the reference start block complex_normal_matrix(seed, n, cols)
+    (solver.py:139-141), drawn bit-exactly on the host for just this rank's rows."""
+    torch = ops.torch
+    m = grid.m
+    out = np.empty((cols, 2 * grid.nc), dtype=np.complex128)
+    for j in range(cols):
+        out[j, :grid.nc] = rng.complex_normals(seed, grid.nc, start_index=j * n + grid.c0, threads=1)
+        out[j, grid.nc:] = rng.complex_normals(seed, grid.nc, start_index=j * n + m + grid.c0, threads=1)
+    return torch.from_numpy(out).to(ops.device)
+
+
+class DistributedSolver:
+    """Holds the grid, the communicators and this rank's tiles across solves (SPMD; every rank of an
+    initialised torch.distributed world constructs it with the same Hamiltonian).  ``source`` is a
+    BseHamiltonian (host or device-born) or an (A, B) pair of host/device blocks, or a dict
+    {"fwd": (A_t, B_t), "trn": (A_t', B_t')} of this rank's own tile blocks."""
+
+    def __init__(self, source, *, m: int | None = None, device=None, grid: Grid | None = None, ops=None):
+        import torch
+
+        world = torch.distributed.get_world_size() if torch.distributed.is_initialized() else 1
+        rank = torch.distributed.get_rank() if torch.distributed.is_initialized() else 0
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+        self.ops = ops or CudaOps(device)
+        if isinstance(source, dict):
+            if m is None:
+                raise ValidationError("m is required with pre-sliced tiles")
+        elif hasattr(source, "device_blocks"):
+            m = source.m
+            if source.a is not None:
+                source = (source.a, source.b)
+            else:
+                ab = source.device_blocks(device)
+                source = (ab[:, :m], ab[:, m:])
+        else:
+            m = source[0].shape[0]
+        self.grid = grid or Grid(m, world, rank)
+        self.comm = Comm(self.grid)
+        self.load(source)
+
+    def load(self, source) -> None:
+        """(Re)upload this rank's tiles (host -> device when the blocks are numpy)."""
+        if isinstance(source, dict):
+            self.fwd, self.trn = make_tiles_from_pieces(self.ops, source)
+        else:
+            self.fwd, self.trn = make_tiles(self.ops, self.grid, *source)
+        self.inner = DistSolver(self.grid, self.comm, self.ops, self.fwd, self.trn)
+
+    def tile_pieces_host(self) -> dict:
+        """This rank's tile blocks as host numpy arrays (for end-to-end timing from host buffers)."""
+        out = {}
+        for name, t in (("fwd", self.fwd), ("trn", self.trn)):
+            mat = t.buf.cpu().numpy().T  # (mr, 2kc) F-order view
+            out[name] = (np.asfortranarray(mat[:, :t.kc]), np.asfortranarray(mat[:, t.kc:]))
+        return out
+
+    def solve(self, cfg: SolverConfig) -> SolveResult:
+        res = self.inner.solve(cfg)
+        res.v = res.v.T  # (n, nev) column-major view
+        return res
+
+
+def make_tiles_from_pieces(ops, pieces: dict):
+    torch = ops.torch
+    tiles = []
+    for name in ("fwd", "trn"):
+        a_t, b_t = pieces[name]
+        mr, kc = a_t.shape
+        buf = torch.empty((2 * kc, mr), dtype=torch.complex128, device=ops.device)
+        for h, blk in enumerate((a_t, b_t)):
+            src = torch.from_numpy(np.ascontiguousarray(blk.T)) if isinstance(blk, np.ndarray) else blk.T
+            buf[h * kc:(h + 1) * kc].copy_(src)
+        addr = buf.data_ptr()
+        tiles.append(Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc))
+    return tuple(tiles)
+
+
+def solve_distributed(source, cfg: SolverConfig, *, device=None, grid: Grid | None = None, ops=None) -> SolveResult:
+    """One-shot SPMD solve (see DistributedSolver); world size 1 runs the same code path."""
+    return DistributedSolver(source, device=device, grid=grid, ops=ops).solve(cfg)

@@ -42,11 +42,37 @@ def uniforms(seed: int, start: int, count: int) -> np.ndarray:
     return ((_words(seed, start, count) >> _U64(11)).astype(np.float64) + 1.0) * 2.0**-53
 
 
-def complex_normals(seed: int, count: int, start_index: int = 0) -> np.ndarray:
+def _normals_serial(seed: int, count: int, start_index: int) -> np.ndarray:
     u = uniforms(seed, 2 * start_index, 2 * count).reshape(count, 2)
     radius = np.sqrt(-2.0 * np.log(u[:, 0]))
     angle = 2.0 * np.pi * u[:, 1]
     return radius * np.cos(angle) + 1j * (radius * np.sin(angle))
+
+
+_PARALLEL_MIN = 1 << 20
+
+
+def complex_normals(seed: int, count: int, start_index: int = 0, threads: int | None = None) -> np.ndarray:
+    """Normals start_index .. start_index+count-1.  Large draws are split into
+    counter ranges computed on all host cores (numpy ufuncs release the GIL);
+    the stream is counter based, so the bits do not depend on the split
+    (tests/test_lib_cpu.py checks this)."""
+    if count < _PARALLEL_MIN:
+        return _normals_serial(seed, count, start_index)
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    nt = threads or min(32, os.cpu_count() or 1)
+    out = np.empty(count, dtype=np.complex128)
+    edges = np.linspace(0, count, nt + 1).astype(np.int64)
+
+    def work(i):
+        a, b = int(edges[i]), int(edges[i + 1])
+        out[a:b] = _normals_serial(seed, b - a, start_index + a)
+
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(work, range(nt)))
+    return out
 
 
 def complex_normal_matrix(seed: int, rows: int, cols: int) -> np.ndarray:

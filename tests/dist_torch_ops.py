@@ -1,0 +1,97 @@
+"""Torch (CPU) reference implementation of the device ops of
+paper_2601_10557_b200/dist.py, so the 2D-distributed algorithm (layouts,
+diagonal shift folding, reductions, gathers) can be checked under gloo with
+world_size 2 / 4 on a machine without GPUs.  TEST INFRASTRUCTURE."""
+import numpy as np
+import torch
+
+
+class TorchOps:
+    def __init__(self):
+        self.torch = torch
+        self.device = torch.device("cpu")
+
+    def empty(self, k, rows):
+        return torch.empty((k, rows), dtype=torch.complex128)
+
+    @staticmethod
+    def _mat(tile):
+        kc = tile.kc
+        return tile.buf[:kc].T, tile.buf[kc:2 * kc].T  # (mr x kc) A_t, B_t
+
+    def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
+            p=None, low_sign=1.0):
+        mr, kc = tile.mr, tile.kc
+        at, bt = self._mat(tile)
+        x1, x2 = x[:, :kc].T, x[:, kc:2 * kc].T
+        up = at @ x1 + bt @ x2
+        low = -(at.conj() @ x2 + bt.conj() @ x1)
+        lo, hi = shift_rows
+        if (shift != 0.0 or shift_col is not None) and hi > lo:
+            sh = shift_col[None, :] if shift_col is not None else shift
+            up[lo:hi] = up[lo:hi] - sh * x1[lo + s_off:hi + s_off]
+            low[lo:hi] = low[lo:hi] - sh * x2[lo + s_off:hi + s_off]
+        up, low = alpha * up, alpha * low
+        if beta != 0.0:
+            up = up - beta * p[:, :mr].T
+            low = low - beta * p[:, mr:2 * mr].T
+        low = low * low_sign
+        y[:, :mr] = up.T
+        y[:, mr:2 * mr] = low.T
+
+    def gram(self, a, b):
+        return (a.conj() @ b.T).T.contiguous()  # storage (k2, k1) of a^H b
+
+    def nn(self, a, w, out=None, alpha=1.0, beta=0.0):
+        r = alpha * (a.T @ w.T)
+        if out is None:
+            return r.T.contiguous()
+        out.copy_((r + beta * out.T).T)
+        return out
+
+    def chol_rinv(self, g, shift=0.0, rdiag=None):
+        gm = g.T
+        gm = (gm + gm.conj().T) / 2 + shift * torch.eye(gm.shape[0], dtype=gm.dtype)
+        r, info = torch.linalg.cholesky_ex(gm, upper=True)
+        if int(info) != 0:
+            return None, int(info)
+        if rdiag is not None:
+            rdiag.copy_(torch.diagonal(r).abs())
+        return torch.linalg.inv(r).T.contiguous(), 0
+
+    def rr_pencil(self, w, g2):
+        from paper_2601_10557_b200.errors import HermitianRqError
+
+        wm = w.T
+        wm = (wm + wm.conj().T) / 2
+        k = wm.shape[0]
+        mm = torch.eye(k, dtype=wm.dtype) - 2 * g2.T
+        mm = (mm + mm.conj().T) / 2
+        lmm = float(torch.linalg.eigvalsh(mm).abs().min())
+        if lmm < 1e-8:
+            raise HermitianRqError("M singular")
+        ell, info = torch.linalg.cholesky_ex(wm)
+        if int(info):
+            raise HermitianRqError("W not definite")
+        gg = torch.linalg.solve_triangular(ell, mm, upper=False)
+        gg = torch.linalg.solve_triangular(ell, gg.conj().T, upper=False).conj().T
+        gg = (gg + gg.conj().T) / 2
+        th, y = torch.linalg.eigh(gg)
+        lam = 1.0 / th.numpy()
+        order = np.argsort(lam, kind="stable")
+        wv = torch.linalg.solve_triangular(ell.conj().T, y, upper=True)[:, torch.as_tensor(order)]
+        return lam[order], wv.T.contiguous(), lmm
+
+    def colnorm2(self, x):
+        return (x.real ** 2 + x.imag ** 2).sum(dim=1)
+
+    def colscale_rsqrt(self, x, n2):
+        x /= torch.sqrt(n2)[:, None]
+
+    def defect(self, g):
+        return float((g.T - torch.eye(g.shape[0], dtype=g.dtype)).abs().max())
+
+    def sflip(self, x):
+        y = x.clone()
+        y[:, x.shape[1] // 2:] *= -1
+        return y

@@ -108,3 +108,12 @@ def test_hamiltonian_validation_on_host():
     a = np.array([[2.0, 1.0 + 1e-14], [1.0, 2.0]], dtype=complex)
     h = BseHamiltonian(a, np.zeros((2, 2)))
     assert np.array_equal(h.a, h.a.conj().T) and h.n == 4
+
+
+def test_threaded_rng_is_bit_identical():
+    from paper_2601_10557_b200 import rng
+
+    count = (1 << 20) + 12345
+    ref = rng._normals_serial(99, count, 7)
+    for threads in (1, 3, 8):
+        np.testing.assert_array_equal(rng.complex_normals(99, count, start_index=7, threads=threads), ref)

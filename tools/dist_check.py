@@ -1,0 +1,56 @@
+"""Multi-GPU parity check of the 2D-distributed solve (run under torchrun, NCCL):
+golden reference cases + C1, compared on rank 0 with the reference fixtures."""
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from conftest import GOLDEN, golden, golden_ham, rebuild_c1
+from paper_2601_10557_b200 import SolverConfig
+from paper_2601_10557_b200.dist import solve_distributed
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", local)
+    fails = 0
+    cases = json.loads((GOLDEN / "meta.json").read_text())["cases"]
+    for key in ["m48_s12", "m64_s21", "m24_s100", "m32_s14", "m48_s13"]:
+        m, seed = (int(t[1:]) for t in key.split("_"))
+        a, b = golden_ham(m, seed)
+        res = solve_distributed((a, b), SolverConfig(**cases[key]), device=dev)
+        if rank == 0:
+            g = golden(f"solve_{key}.npz")
+            rel = float(np.max(np.abs(res.lambdas - g["lambdas"]) / np.abs(g["lambdas"])))
+            v = res.v.T.contiguous().cpu().numpy().T
+            ov = float(np.abs(np.abs(np.einsum("ij,ij->j", g["v"].conj(), v)) - 1).max())
+            ok = rel <= 1e-10 and ov <= 1e-8 and abs(res.iterations_used - int(g["iterations_used"])) <= 1
+            fails += not ok
+            print(f"[world {world}] {key}: iters {res.iterations_used}/{int(g['iterations_used'])} "
+                  f"max rel dlambda {rel:.2e} subspace {ov:.2e} {'OK' if ok else 'FAIL'}", flush=True)
+    a, b, g = rebuild_c1()
+    res = solve_distributed((a, b), SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0), device=dev)
+    if rank == 0:
+        rel = float(np.max(np.abs(res.lambdas - g["abs_lambdas"]) / np.abs(g["abs_lambdas"])))
+        ok = rel <= 1e-10 and res.converged and abs(res.iterations_used - int(g["abs_iters"])) <= 1 \
+            and res.residual_norms.max() <= 1e-10
+        fails += not ok
+        print(f"[world {world}] C1 m=500: iters {res.iterations_used}/{int(g['abs_iters'])} max rel dlambda "
+              f"{rel:.2e} max res {res.residual_norms.max():.2e} {'OK' if ok else 'FAIL'}", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
