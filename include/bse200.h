@@ -51,6 +51,10 @@ const char* bse_last_error(const bse_ctx* ctx);
 /* number of bse200 kernels launched through this context (evidence counter) */
 int64_t bse_launch_count(const bse_ctx* ctx);
 const char* bse_version(void);
+/* Complex multiplication used by the Chebyshev-filter products: 4 (4M split, 8 real DMMA per
+ * complex block pair, default) or 3 (3M / Gauss, 6 DMMA: 25% fewer FP64 tensor ops; error bound
+ * grows to ~eps (|Re|+|Im|)^2).  RR and residual products always use 4M.          */
+int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults);
 
 /* ---- Hamiltonian operator ------------------------------------------------ */
 /* y = H x  (low_sign = +1)  or  y = S H x  (low_sign = -1)
@@ -135,6 +139,7 @@ typedef struct {
   const void* p2;
   int64_t ldp;
   double alpha, beta, low_sign;
+  int filter; /* 1: a Chebyshev-filter product (uses the algorithm set by bse_set_filter_algorithm) */
 } bse_hop_tile_args;
 int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* args);
 /* CholQR factor step (ortho.py:115-119): hermitise the summed Gram d_g (k x k), add shift I,

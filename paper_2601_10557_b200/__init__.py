@@ -51,5 +51,6 @@ from .solver import (
     solve,
 )
 from .generate import GeneratorSpec, generate
+from ._lib import filter_algorithm, set_filter_algorithm
 
 __all__ = [n for n in dir() if not n.startswith("_")]

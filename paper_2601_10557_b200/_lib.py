@@ -40,7 +40,7 @@ class HopTileArgs(C.Structure):
         ("s1", _vp), ("s2", _vp), ("lds", _i64), ("shift_lo", _i64), ("shift_hi", _i64),
         ("shift", _dbl), ("d_shift_col", _vp),
         ("p1", _vp), ("p2", _vp), ("ldp", _i64),
-        ("alpha", _dbl), ("beta", _dbl), ("low_sign", _dbl),
+        ("alpha", _dbl), ("beta", _dbl), ("low_sign", _dbl), ("filter", C.c_int),
     ]
 
 
@@ -50,6 +50,7 @@ _SIGS = {
     "bse_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "bse_ctx_destroy": (None, [_vp]),
     "bse_set_stream": (C.c_int, [_vp, _vp]),
+    "bse_set_filter_algorithm": (C.c_int, [_vp, C.c_int]),
     "bse_last_error": (C.c_char_p, [_vp]),
     "bse_launch_count": (_i64, [_vp]),
     "bse_apply_h": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _dbl]),
@@ -92,6 +93,21 @@ _STATUS = {
 
 _lib = None
 _lock = threading.Lock()
+# complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
+_FILTER_CM = {"3m": 3, "4m": 4}[os.environ.get("BSE200_FILTER", "4m").lower()]
+
+
+def set_filter_algorithm(name: str) -> None:
+    """'4m' (default) or '3m' (Gauss: 25% fewer FP64 tensor ops in the filter) for every context."""
+    global _FILTER_CM
+    cm = {"3m": 3, "4m": 4}[name.lower()]
+    _FILTER_CM = cm
+    for ctx in Context._by_device.values():
+        ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, cm))
+
+
+def filter_algorithm() -> str:
+    return f"{_FILTER_CM}m"
 
 
 def load() -> C.CDLL:
@@ -135,6 +151,7 @@ class Context:
             raise RuntimeError(f"bse_ctx_create failed with status {st}")
         self.handle = h
         self._stream = None
+        self.check(self.lib.bse_set_filter_algorithm(h, _FILTER_CM))
 
     @classmethod
     def get(cls, device: int) -> "Context":

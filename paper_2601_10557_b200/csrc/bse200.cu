@@ -37,6 +37,7 @@ struct bse_ctx {
   size_t hws_bytes = 0;
   double* pinned = nullptr;  // pinned host staging (small results)
   size_t pinned_count = 0;
+  int filter_cm = 4;  // complex multiplication of the Chebyshev products: 4 (4M) or 3 (3M / Gauss)
 };
 
 namespace {
@@ -146,17 +147,28 @@ inline int grid1d(int64_t n, int threads = 256, int cap = 148 * 16) {
 // Tile configuration of the fused H-operator GEMM:
 // CTA 64 x 32 complex (up and low halves), 8 warps of 16 x 16, BK = 8, 4 stages.
 using HopMain = bse::HopCfg<64, 32, 8, 2, 2, 4, 2>;
+// 3M (Gauss) variant: 6 accumulators per block pair -> one 8-warp CTA per SM, deeper K stages
+using Hop3M = bse::HopCfg<64, 32, 16, 2, 2, 4, 1>;
 
-template <class C, int EPI>
+template <class C, int EPI, int CM = 4>
 void launch_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   static bool configured = false;
   if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop_kernel<C, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CUDA_OK(cudaFuncSetAttribute(bse::hop_kernel<C, EPI, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::SMEM));
     configured = true;
   }
   dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
-  bse::hop_kernel<C, EPI><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  bse::hop_kernel<C, EPI, CM><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
   check_launch(ctx);
+}
+
+// Chebyshev-step products: 4M (default) or 3M as selected by bse_set_filter_algorithm
+void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
+  if (ctx->filter_cm == 3)
+    launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a);
+  else
+    launch_hop<HopMain, bse::HOP_AXPBY, 4>(ctx, a);
 }
 
 bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, int64_t k) {
@@ -209,7 +221,7 @@ void filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const z
     a.p2 = yprev + m;
     a.ldp = ld;
   }
-  launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+  launch_filter_hop(ctx, a);
 }
 
 // residual norms into d_out (k doubles, device)
@@ -547,6 +559,13 @@ void bse_ctx_destroy(bse_ctx* ctx) {
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
   delete ctx;
+}
+
+int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
+  return guarded(ctx, [&] {
+    if (complex_mults != 3 && complex_mults != 4) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4");
+    ctx->filter_cm = complex_mults;
+  });
 }
 
 int bse_set_stream(bse_ctx* ctx, void* stream) {
@@ -930,7 +949,10 @@ int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* t) {
     if ((a.shift != 0.0 || a.shift_col) && a.shift_hi > a.shift_lo && (!a.s1 || !a.s2))
       throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
     if (a.kc <= 0) throw BseError(BSE_EVALIDATION, "empty contraction");
-    launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+    if (t->filter)
+      launch_filter_hop(ctx, a);
+    else
+      launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
   });
 }
 

@@ -105,7 +105,34 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
   }
 }
 
-template <class C, int EPI>
+// Per (i, j, h) accumulator values -> U = P Xa and L' = conj(P) Xb.
+//  4M: acc = {Ur, Ui, L'r, L'i}.
+//  3M: acc = {T1 = Pr Xar, T2 = Pi Xai, T3 = (Pr+Pi)(Xar+Xai), S1 = Pr Xbr, S2 = Pi Xbi, S3 = (Pr-Pi)(Xbr+Xbi)}
+//      Ur = T1 - T2, Ui = T3 - T1 - T2, L'r = S1 + S2, L'i = S3 - S1 + S2.
+template <int CM>
+struct Acc {
+  static constexpr int N = CM == 3 ? 6 : 4;
+};
+
+template <int CM, int WM, int WN>
+__device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][WN][2], int i, int j, int h, double& ur,
+                                           double& ui, double& lr, double& li) {
+  if constexpr (CM == 3) {
+    const double t1 = acc[0][i][j][h], t2 = acc[1][i][j][h], t3 = acc[2][i][j][h];
+    const double s1 = acc[3][i][j][h], s2 = acc[4][i][j][h], s3 = acc[5][i][j][h];
+    ur = t1 - t2;
+    ui = t3 - t1 - t2;
+    lr = s1 + s2;
+    li = s3 - s1 + s2;
+  } else {
+    ur = acc[0][i][j][h];
+    ui = acc[1][i][j][h];
+    lr = acc[2][i][j][h];
+    li = acc[3][i][j][h];
+  }
+}
+
+template <class C, int EPI, int CM = 4>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   zval* smem = reinterpret_cast<zval*>(smem_raw);
@@ -119,13 +146,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
   const int nkt_part = (a.kc + C::BK - 1) / C::BK;
   const int nkt = 2 * nkt_part;
 
-  double ur[C::WM][C::WN][2], ui[C::WM][C::WN][2], lr[C::WM][C::WN][2], li[C::WM][C::WN][2];
+  double acc[Acc<CM>::N][C::WM][C::WN][2];
 #pragma unroll
-  for (int i = 0; i < C::WM; ++i)
+  for (int q = 0; q < Acc<CM>::N; ++q)
 #pragma unroll
-    for (int j = 0; j < C::WN; ++j)
+    for (int i = 0; i < C::WM; ++i)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) ur[i][j][h] = ui[i][j][h] = lr[i][j][h] = li[i][j][h] = 0.0;
+      for (int j = 0; j < C::WN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
 
   // prologue
 #pragma unroll
@@ -156,19 +183,41 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
         xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
       }
-#pragma unroll
-      for (int i = 0; i < C::WM; ++i) {
-        const double pr = pf[i].re, pi = pf[i].im, npi = -pf[i].im;
+      if constexpr (CM == 3) {
+        double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {
-          dmma(ur[i][j], pr, xa[j].re);
-          dmma(ur[i][j], npi, xa[j].im);
-          dmma(ui[i][j], pr, xa[j].im);
-          dmma(ui[i][j], pi, xa[j].re);
-          dmma(lr[i][j], pr, xb[j].re);
-          dmma(lr[i][j], pi, xb[j].im);
-          dmma(li[i][j], pr, xb[j].im);
-          dmma(li[i][j], npi, xb[j].re);
+          xas[j] = xa[j].re + xa[j].im;
+          xbs[j] = xb[j].re + xb[j].im;
+        }
+#pragma unroll
+        for (int i = 0; i < C::WM; ++i) {
+          const double pr = pf[i].re, pi = pf[i].im, ps = pf[i].re + pf[i].im, pd = pf[i].re - pf[i].im;
+#pragma unroll
+          for (int j = 0; j < C::WN; ++j) {
+            dmma(acc[0][i][j], pr, xa[j].re);
+            dmma(acc[1][i][j], pi, xa[j].im);
+            dmma(acc[2][i][j], ps, xas[j]);
+            dmma(acc[3][i][j], pr, xb[j].re);
+            dmma(acc[4][i][j], pi, xb[j].im);
+            dmma(acc[5][i][j], pd, xbs[j]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < C::WM; ++i) {
+          const double pr = pf[i].re, pi = pf[i].im, npi = -pf[i].im;
+#pragma unroll
+          for (int j = 0; j < C::WN; ++j) {
+            dmma(acc[0][i][j], pr, xa[j].re);
+            dmma(acc[0][i][j], npi, xa[j].im);
+            dmma(acc[1][i][j], pr, xa[j].im);
+            dmma(acc[1][i][j], pi, xa[j].re);
+            dmma(acc[2][i][j], pr, xb[j].re);
+            dmma(acc[2][i][j], pi, xb[j].im);
+            dmma(acc[3][i][j], pr, xb[j].im);
+            dmma(acc[3][i][j], npi, xb[j].re);
+          }
         }
       }
     }
@@ -188,8 +237,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
           const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + h;
           if (col >= a.k) continue;
           // H x rows: up = U, low = -L'
-          double hu_r = ur[i][j][h], hu_i = ui[i][j][h];
-          double hl_r = -lr[i][j][h], hl_i = -li[i][j][h];
+          double hu_r, hu_i, hl_r, hl_i;
+          acc_values<CM, C::WM, C::WN>(acc, i, j, h, hu_r, hu_i, hl_r, hl_i);
+          hl_r = -hl_r;
+          hl_i = -hl_i;
           if ((a.shift != 0.0 || a.shift_col) && row >= a.shift_lo && row < a.shift_hi) {
             const double sh = a.shift_col ? a.shift_col[col] : a.shift;
             const zval s1 = a.s1[(int64_t)col * a.lds + row];
@@ -218,7 +269,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
   } else {
     // residual column norms: sum over this CTA's rows of |Hv - lam v|^2 (both halves)
     __shared__ double red[C::WARPS_M][C::BN];
-    double acc[C::WN][2];
+    double rsum[C::WN][2];
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
 #pragma unroll
@@ -233,8 +284,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
             if (row < a.mr) {
               const zval v1 = a.s1[(int64_t)col * a.lds + row];
               const zval v2 = a.s2[(int64_t)col * a.lds + row];
-              const double r1 = ur[i][j][h] - lam * v1.re, r2 = ui[i][j][h] - lam * v1.im;
-              const double r3 = -lr[i][j][h] - lam * v2.re, r4 = -li[i][j][h] - lam * v2.im;
+              double vur, vui, vlr, vli;
+              acc_values<CM, C::WM, C::WN>(acc, i, j, h, vur, vui, vlr, vli);
+              const double r1 = vur - lam * v1.re, r2 = vui - lam * v1.im;
+              const double r3 = -vlr - lam * v2.re, r4 = -vli - lam * v2.im;
               s += r1 * r1 + r2 * r2 + r3 * r3 + r4 * r4;
             }
           }
@@ -243,14 +296,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         s += __shfl_xor_sync(0xffffffffu, s, 4);
         s += __shfl_xor_sync(0xffffffffu, s, 8);
         s += __shfl_xor_sync(0xffffffffu, s, 16);
-        acc[j][h] = s;
+        rsum[j][h] = s;
       }
     }
     if (g == 0) {
 #pragma unroll
       for (int j = 0; j < C::WN; ++j)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) red[wm][wn * (8 * C::WN) + j * 8 + 2 * t + h] = acc[j][h];
+        for (int h = 0; h < 2; ++h) red[wm][wn * (8 * C::WN) + j * 8 + 2 * t + h] = rsum[j][h];
     }
     __syncthreads();
     for (int cc = threadIdx.x; cc < C::BN; cc += C::THREADS) {

@@ -150,7 +150,7 @@ class CudaOps:
         return self.torch.empty((k, rows), dtype=self.torch.complex128, device=self.device)
 
     def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
-            p=None, low_sign=1.0):
+            p=None, low_sign=1.0, filter=False):
         """y (storage k x 2 mr) = low_sign^{low} (alpha (tile-product of x - shift s) - beta p)."""
         k = x.shape[0]
         mr, kc = tile.mr, tile.kc
@@ -169,6 +169,7 @@ class CudaOps:
             pa_ = p.data_ptr()
             args.p1, args.p2, args.ldp = pa_, pa_ + mr * ZB, p.stride(0)
         args.alpha, args.beta, args.low_sign = alpha, beta, low_sign
+        args.filter = 1 if filter else 0
         self.ctx.call("bse_hop_tile", ctypes.byref(args))
 
     def gram(self, a, b):
@@ -334,13 +335,14 @@ class DistSolver:
         k = v_col.shape[0]
         yr = row_buf[:k]
         # step 1: col -> row, Y1 = (s1/e)(H Y0 - c Y0)
-        self.forward(v_col, yr, alpha=s1 / e, shift=c)
+        self.forward(v_col, yr, alpha=s1 / e, shift=c, filter=True)
         src, dst = yr, v_col
         for step in range(2, cfg.degree + 1):
             sn = 1.0 / (2.0 / s1 - s)
             # Y_{j+1} = (2 sn / e)(H Y_j - c Y_j) - (s sn) Y_{j-1}; Y_{j-1} lives in dst (in place)
             owner = self._beta_owner(step)
-            kw = dict(alpha=2.0 * sn / e, shift=c, beta=(s * sn) if owner else 0.0, p=dst if owner else None)
+            kw = dict(alpha=2.0 * sn / e, shift=c, beta=(s * sn) if owner else 0.0, p=dst if owner else None,
+                      filter=True)
             if step % 2 == 0:
                 self.transposed(src, dst, **kw)
             else:

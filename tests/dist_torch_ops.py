@@ -20,7 +20,7 @@ class TorchOps:
         return tile.buf[:kc].T, tile.buf[kc:2 * kc].T  # (mr x kc) A_t, B_t
 
     def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
-            p=None, low_sign=1.0):
+            p=None, low_sign=1.0, filter=False):
         mr, kc = tile.mr, tile.kc
         at, bt = self._mat(tile)
         x1, x2 = x[:, :kc].T, x[:, kc:2 * kc].T

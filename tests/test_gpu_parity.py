@@ -285,3 +285,23 @@ def test_c1_parity(bse, c1_instance):
         assert r.residual_norms.max() <= thr
         ov = np.abs(np.einsum("ij,ij->j", g[f"{tag}_v10"].conj(), r.v[:, :10]))
         assert np.abs(ov - 1).max() <= 1e-8
+
+
+def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance):
+    """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
+    the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
+    a, b = golden_ham(16, 5)
+    g = golden("ops_m16_s5.npz")
+    ham = bse.BseHamiltonian(a, b)
+    cfg = bse.FilterConfig(int(g["deg"]), float(g["center"]), float(g["half_width"]), float(g["scale_ref"]))
+    try:
+        bse.set_filter_algorithm("3m")
+        out3 = bse.chebyshev_filter(ham, g["x"], cfg)
+        a1, b1, gc = c1_instance
+        r = bse.solve(bse.BseHamiltonian(a1, b1), bse.SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0))
+    finally:
+        bse.set_filter_algorithm("4m")
+    assert _rel(out3, g["filtered"]) <= 1e-12
+    assert r.converged and abs(r.iterations_used - int(gc["abs_iters"])) <= 1
+    assert (np.abs(r.lambdas - gc["abs_lambdas"]) / np.abs(gc["abs_lambdas"])).max() <= 1e-10
+    assert r.residual_norms.max() <= 1e-10
