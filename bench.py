@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -56,44 +55,60 @@ def fp64_peak() -> tuple[float, str]:
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled in-process through NVML during the timed region
+    (an nvidia-smi subprocess per sample stalls the solver's synchronous CUDA calls)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
-    def __init__(self, index: int):
-        self.index = index
-        self.rows: list[list[str]] = []
+    def __init__(self, index: int, period: float = 0.5):
+        self.index, self.period = index, period
+        self.sm, self.mx, self.reasons, self.power = [], [], set(), []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self.h = None
+        try:
+            import pynvml as nv
+            import torch
+
+            nv.nvmlInit()
+            self.nv = nv
+            try:
+                props = torch.cuda.get_device_properties(index)
+                bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+                self.h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = nv.nvmlDeviceGetHandleByIndex(index)
+        except Exception:
+            self.h = None
 
     def _run(self):
+        nv = self.nv
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
-                for line in out.stdout.strip().splitlines():
-                    self.rows.append([c.strip() for c in line.split(",")])
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.mx.append(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1e3)
+                bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= {name for bit, name in self.REASONS.items() if bits & bit}
             except Exception:
                 pass
-            self._stop.wait(0.5)
+            self._stop.wait(self.period)
 
     def __enter__(self):
-        self._t.start()
+        if self.h is not None:
+            self._t.start()
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._t.join(timeout=15)
+        if self._t.is_alive():
+            self._t.join(timeout=15)
 
     def summary(self) -> dict:
-        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows if len(r) >= 8 for i in range(4) if r[4 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.mx) if self.mx else None, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "power_w_max": max(self.power) if self.power else None,
+                "source": "NVML (in-process)"}
 
 
 def dist_setup():
@@ -354,6 +369,7 @@ def run_ours(args, world, rank, local):
                       "lambda_1": float(res.lambdas[0]), "lambda_nev": float(res.lambdas[-1]),
                       "max_residual": float(res.residual_norms.max()),
                       "locked_per_iter": [t.locked for t in res.trace],
+                      "phase_events_s": [[ph, round(dt, 4)] for ph, dt in res.ledger.events],
                       "e2e_iterations": r_e2e.iterations_used,
                       "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},
             "clocks": clk.summary(),

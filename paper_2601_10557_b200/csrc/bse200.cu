@@ -163,12 +163,28 @@ void launch_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   check_launch(ctx);
 }
 
+// tuning variants (selected with bse_set_filter_algorithm codes 40+v / 30+v)
+using Hop4M_1 = bse::HopCfg<64, 32, 8, 2, 2, 5, 2>;
+using Hop4M_2 = bse::HopCfg<128, 32, 8, 2, 2, 4, 1>;
+using Hop4M_3 = bse::HopCfg<64, 64, 8, 2, 2, 4, 1>;
+using Hop3M_1 = bse::HopCfg<64, 32, 8, 2, 2, 6, 1>;
+using Hop3M_2 = bse::HopCfg<64, 16, 8, 2, 1, 4, 2>;
+using Hop3M_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1>;
+using Hop3M_4 = bse::HopCfg<96, 32, 16, 2, 2, 4, 1>;
+
 // Chebyshev-step products: 4M (default) or 3M as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
-  if (ctx->filter_cm == 3)
-    launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a);
-  else
-    launch_hop<HopMain, bse::HOP_AXPBY, 4>(ctx, a);
+  switch (ctx->filter_cm) {
+    case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
+    case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
+    case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
+    case 33: launch_hop<Hop3M_3, bse::HOP_AXPBY, 3>(ctx, a); break;
+    case 34: launch_hop<Hop3M_4, bse::HOP_AXPBY, 3>(ctx, a); break;
+    case 41: launch_hop<Hop4M_1, bse::HOP_AXPBY, 4>(ctx, a); break;
+    case 42: launch_hop<Hop4M_2, bse::HOP_AXPBY, 4>(ctx, a); break;
+    case 43: launch_hop<Hop4M_3, bse::HOP_AXPBY, 4>(ctx, a); break;
+    default: launch_hop<HopMain, bse::HOP_AXPBY, 4>(ctx, a); break;
+  }
 }
 
 bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, int64_t k) {
@@ -563,7 +579,9 @@ void bse_ctx_destroy(bse_ctx* ctx) {
 
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
-    if (complex_mults != 3 && complex_mults != 4) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4");
+    const bool ok = complex_mults == 3 || complex_mults == 4 || (complex_mults >= 31 && complex_mults <= 34) ||
+                    (complex_mults >= 41 && complex_mults <= 43);
+    if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
   });
 }

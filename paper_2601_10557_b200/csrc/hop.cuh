@@ -68,7 +68,6 @@ struct HopCfg {
   static constexpr int STAGE_ELEMS = P_ELEMS + 2 * X_ELEMS;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(zval);
   static_assert(BM % 8 == 0 && BK % 8 == 0 && BN % 8 == 0, "tile dims");
-  static_assert((BK * BM) % THREADS == 0 && (2 * BN * BK) % THREADS == 0, "loader mapping");
 };
 
 template <class C>
@@ -83,8 +82,9 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
   zval* Xas = st + C::P_ELEMS;
   zval* Xbs = Xas + C::X_ELEMS;
 #pragma unroll
-  for (int r = 0; r < (C::BK * C::BM) / C::THREADS; ++r) {
+  for (int r = 0; r < (C::BK * C::BM + C::THREADS - 1) / C::THREADS; ++r) {
     const int id = tid + r * C::THREADS;
+    if ((C::BK * C::BM) % C::THREADS != 0 && id >= C::BK * C::BM) break;
     const int ii = id % C::BM, jj = id / C::BM;
     const int gi = i0 + ii, gj = j0 + jj;
     const bool ok = (gi < a.mr) && (gj < a.kc);
@@ -92,8 +92,9 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
     cp_async16(Ps + jj * C::LDP + ii, src, ok);
   }
 #pragma unroll
-  for (int r = 0; r < (2 * C::BN * C::BK) / C::THREADS; ++r) {
+  for (int r = 0; r < (2 * C::BN * C::BK + C::THREADS - 1) / C::THREADS; ++r) {
     const int id = tid + r * C::THREADS;
+    if ((2 * C::BN * C::BK) % C::THREADS != 0 && id >= 2 * C::BN * C::BK) break;
     const int kk = id % C::BK;
     const int cc = (id / C::BK) % C::BN;
     const int which = id / (C::BK * C::BN);

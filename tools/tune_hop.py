@@ -1,0 +1,77 @@
+"""Filter-step kernel variants (bse_set_filter_algorithm codes) and small-k cuSOLVER timings."""
+import ctypes
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+import torch
+
+from paper_2601_10557_b200 import _lib
+from paper_2601_10557_b200.hamiltonian import colmajor_empty, ld_of
+
+ctx = _lib.Context.get(0)
+dev = torch.device("cuda", 0)
+
+
+def timed(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def variants(m, ks, codes):
+    n = 2 * m
+    ab = colmajor_empty(m, 2 * m, dev)
+    ab.real.normal_()
+    ab.imag.normal_()
+    for k in ks:
+        y = colmajor_empty(n, k, dev); y.real.normal_(); y.imag.normal_()
+        yp = colmajor_empty(n, k, dev); yp.real.normal_(); yp.imag.normal_()
+        yn = colmajor_empty(n, k, dev)
+        for code in codes:
+            ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
+            ms = timed(lambda: ctx.call("bse_filter_step", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(y), _lib.dptr(yp),
+                                        _lib.dptr(yn), n, k, 0.1, 1e-3, 0.5), 3 if m >= 20000 else 5)
+            tf = 8.0 * n * n * k / ms / 1e9
+            cm = 3 if code in (3, 31, 32, 33, 34) else 4
+            print(f"m={m} k={k} code={code}: {ms:8.2f} ms  model {tf:6.2f} TF/s  executed {tf * (0.75 if cm == 3 else 1):6.2f}",
+                  flush=True)
+    ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 4))
+
+
+def solver_small():
+    for k in (100, 200, 400, 600, 800, 1000, 1200):
+        g = torch.randn((k, k), dtype=torch.complex128, device=dev)
+        g = g @ g.conj().T / k + torch.eye(k, dtype=torch.complex128, device=dev)
+        w = np.zeros(k)
+        lam = np.zeros(k)
+        wv = torch.empty_like(g)
+        lmm = ctypes.c_double()
+        t0 = time.perf_counter()
+        ctx.call("bse_eigvalsh", _lib.dptr(g), k, k, _lib.hptr(w))
+        t1 = time.perf_counter()
+        g2 = 0.25 * torch.eye(k, dtype=torch.complex128, device=dev) + 0.01 * (g - torch.eye(k, dtype=g.dtype, device=dev))
+        wm = g.clone()
+        t2 = time.perf_counter()
+        ctx.call("bse_rr_pencil", _lib.dptr(wm), _lib.dptr(g2.clone()), k, _lib.hptr(lam), _lib.dptr(wv), ctypes.byref(lmm))
+        t3 = time.perf_counter()
+        wm = g.clone()
+        t4 = time.perf_counter()
+        ctx.call("bse_rr_pencil", _lib.dptr(wm), _lib.dptr(g2.clone()), k, _lib.hptr(lam), _lib.dptr(wv), ctypes.byref(lmm))
+        t5 = time.perf_counter()
+        print(f"k={k}: eigvalsh {1e3 * (t1 - t0):.1f} ms, rr_pencil {1e3 * (t3 - t2):.1f} ms / again {1e3 * (t5 - t4):.1f} ms",
+              flush=True)
+
+
+if __name__ == "__main__":
+    solver_small()
+    variants(20000, [1200, 300], [4, 41, 42, 43, 3, 31, 32, 33, 34])
+    variants(10000, [600, 113], [4, 41, 42, 43, 3, 31, 32, 33, 34])
