@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
+#include <ctime>
 #include <numeric>
 #include <stdexcept>
 #include <string>
@@ -38,6 +40,8 @@ struct bse_ctx {
   double* pinned = nullptr;  // pinned host staging (small results)
   size_t pinned_count = 0;
   int filter_cm = 4;  // complex multiplication of the Chebyshev products: 4 (4M) or 3 (3M / Gauss)
+  void* sws = nullptr;  // persistent cuSOLVER device workspace (grows, never shrinks)
+  size_t sws_bytes = 0;
 };
 
 namespace {
@@ -118,6 +122,35 @@ struct Scratch {
 
 inline size_t al(size_t bytes) { return (bytes + 255) & ~size_t(255); }
 
+// Opt-in step timer (BSE200_TIMING=1): synchronises the stream at each mark and prints the wall
+// time of every step of an entry point to stderr.  Off by default (no syncs added).
+struct StepTimer {
+  bse_ctx* ctx;
+  const char* name;
+  bool on;
+  double t0, tl;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+  }
+  StepTimer(bse_ctx* c, const char* n) : ctx(c), name(n) {
+    const char* e = getenv("BSE200_TIMING");
+    on = e && e[0] == '1';
+    if (on) {
+      cudaStreamSynchronize(ctx->stream);
+      t0 = tl = now();
+    }
+  }
+  void mark(const char* step, int64_t k = -1) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const double t = now();
+    fprintf(stderr, "[bse200 %s k=%lld] %-22s %8.2f ms\n", name, (long long)k, step, 1e3 * (t - tl));
+    tl = t;
+  }
+};
+
 double* pinned(bse_ctx* ctx, size_t count) {
   if (ctx->pinned_count < count) {
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -126,6 +159,25 @@ double* pinned(bse_ctx* ctx, size_t count) {
     ctx->pinned_count = count;
   }
   return ctx->pinned;
+}
+
+// Persistent device workspace for cuSOLVER: allocated once per size high-water mark, so the
+// k x k factorisations never touch an allocator inside the iteration (stream-ordered
+// cudaMallocAsync/cudaFreeAsync pairs caused 0.2-1.7 s host stalls at C3, profiles/r01/).
+void* solver_ws(bse_ctx* ctx, size_t bytes) {
+  bytes = std::max<size_t>(bytes, 256);
+  if (ctx->sws_bytes < bytes) {
+    const size_t want = std::max(bytes, ctx->sws_bytes * 3 / 2);
+    if (ctx->sws) {
+      CUDA_OK(cudaStreamSynchronize(ctx->stream));
+      CUDA_OK(cudaFree(ctx->sws));
+    }
+    ctx->sws = nullptr;
+    ctx->sws_bytes = 0;
+    CUDA_OK(cudaMalloc(&ctx->sws, want));
+    ctx->sws_bytes = want;
+  }
+  return ctx->sws;
 }
 
 void* host_ws(bse_ctx* ctx, size_t bytes) {
@@ -180,6 +232,8 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
     case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 33: launch_hop<Hop3M_3, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 34: launch_hop<Hop3M_4, bse::HOP_AXPBY, 3>(ctx, a); break;
+    case 35: launch_hop<Hop3M, bse::HOP_AXPBY, 5>(ctx, a); break;    // timing experiment (no operand sums)
+    case 36: launch_hop<Hop3M_2, bse::HOP_AXPBY, 5>(ctx, a); break;  // timing experiment
     case 41: launch_hop<Hop4M_1, bse::HOP_AXPBY, 4>(ctx, a); break;
     case 42: launch_hop<Hop4M_2, bse::HOP_AXPBY, 4>(ctx, a); break;
     case 43: launch_hop<Hop4M_3, bse::HOP_AXPBY, 4>(ctx, a); break;
@@ -321,15 +375,13 @@ cuDoubleComplex* cz(zval* p) { return reinterpret_cast<cuDoubleComplex*>(p); }
 int potrf(bse_ctx* ctx, zval* a, int k, cublasFillMode_t uplo, int* d_info) {
   size_t dws = 0, hws = 0;
   SOLVER_OK(cusolverDnXpotrf_bufferSize(ctx->solver, ctx->params, uplo, k, CUDA_C_64F, a, k, CUDA_C_64F, &dws, &hws));
-  void* dbuf = nullptr;
-  CUDA_OK(cudaMallocAsync(&dbuf, std::max<size_t>(dws, 16), ctx->stream));
+  void* dbuf = solver_ws(ctx, dws);
   void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
   SOLVER_OK(cusolverDnXpotrf(ctx->solver, ctx->params, uplo, k, CUDA_C_64F, a, k, CUDA_C_64F, dbuf, dws, hbuf, hws, d_info));
-  int info = 0;
-  CUDA_OK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_OK(cudaFreeAsync(dbuf, ctx->stream));
+  int* info = reinterpret_cast<int*>(pinned(ctx, 1));
+  CUDA_OK(cudaMemcpyAsync(info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_OK(cudaStreamSynchronize(ctx->stream));
-  return info;
+  return *info;
 }
 
 // hermitian eigendecomposition (values ascending in d_w; vectors overwrite a when want_vec)
@@ -338,16 +390,14 @@ void heevd(bse_ctx* ctx, zval* a, int k, double* d_w, bool want_vec, int* d_info
   size_t dws = 0, hws = 0;
   SOLVER_OK(cusolverDnXsyevd_bufferSize(ctx->solver, ctx->params, jobz, CUBLAS_FILL_MODE_LOWER, k, CUDA_C_64F, a, k,
                                         CUDA_R_64F, d_w, CUDA_C_64F, &dws, &hws));
-  void* dbuf = nullptr;
-  CUDA_OK(cudaMallocAsync(&dbuf, std::max<size_t>(dws, 16), ctx->stream));
+  void* dbuf = solver_ws(ctx, dws);
   void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
   SOLVER_OK(cusolverDnXsyevd(ctx->solver, ctx->params, jobz, CUBLAS_FILL_MODE_LOWER, k, CUDA_C_64F, a, k, CUDA_R_64F,
                              d_w, CUDA_C_64F, dbuf, dws, hbuf, hws, d_info));
-  int info = 0;
-  CUDA_OK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  CUDA_OK(cudaFreeAsync(dbuf, ctx->stream));
+  int* info = reinterpret_cast<int*>(pinned(ctx, 1));
+  CUDA_OK(cudaMemcpyAsync(info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_OK(cudaStreamSynchronize(ctx->stream));
-  if (info != 0) throw BseError(BSE_ENUMERICAL, "hermitian eigensolver failed (info " + std::to_string(info) + ")");
+  if (*info != 0) throw BseError(BSE_ENUMERICAL, "hermitian eigensolver failed (info " + std::to_string(*info) + ")");
 }
 
 void to_host(bse_ctx* ctx, double* h, const double* d, size_t count) {
@@ -429,15 +479,21 @@ int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scra
   int* d_info = sc.take<int>(4);
   // keep the input for the fallback (ortho.py:126 restarts from x)
   bool ok = true;
+  StepTimer tm(ctx, "cholqr");
   zval* x0 = sc.take<zval>(n * k);
   CUDA_OK(cudaMemcpy2DAsync(x0, sizeof(zval) * n, q, sizeof(zval) * ldq, sizeof(zval) * n, (size_t)k,
                             cudaMemcpyDeviceToDevice, ctx->stream));
-  for (int pass = 0; pass < 2 && ok; ++pass) ok = cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, 0.0, nullptr);
+  for (int pass = 0; pass < 2 && ok; ++pass) {
+    ok = cholqr_pass(ctx, q, n, k, ldq, gram, tmp, gws, d_info, 0.0, nullptr);
+    tm.mark("cholqr pass", k);
+  }
   if (ok) {
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
     const double defect = defect_to_host(ctx, gram, (int)k, dpart);
+    tm.mark("defect", k);
     if (defect <= 1e-8) return 0;  // ortho.py:124-126 (NaN fails the test)
   }
+  tm.mark("FALLBACK to shifted CholQR3", k);
   // Shifted CholeskyQR3 (Fukaya et al.): shift = 11 (n k + k (k + 1)) u ||X||_F^2, then CholQR2.
   CUDA_OK(cudaMemcpy2DAsync(q, sizeof(zval) * ldq, x0, sizeof(zval) * n, sizeof(zval) * n, (size_t)k,
                             cudaMemcpyDeviceToDevice, ctx->stream));
@@ -480,6 +536,7 @@ size_t pencil_ws_bytes(int64_t k) { return 3 * al((size_t)k * k * sizeof(zval)) 
 void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* wvec, double* h_lam_min_m,
                Scratch& sc) {
   const size_t kk = (size_t)k * k;
+  StepTimer tm(ctx, "rr_pencil");
   zval* mm = sc.take<zval>(kk);
   zval* tmp = sc.take<zval>(kk);
   zval* g = sc.take<zval>(kk);
@@ -497,6 +554,7 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   heevd(ctx, tmp, (int)k, d_w, false, d_info);
   std::vector<double> hw(k);
   to_host(ctx, hw.data(), d_w, k);
+  tm.mark("eigvalsh(M)", k);
   double lmm = INFINITY;
   for (double v : hw) lmm = std::min(lmm, std::fabs(v));
   if (h_lam_min_m) *h_lam_min_m = lmm;
@@ -513,9 +571,11 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
                       (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
   bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k);
   check_launch(ctx);
+  tm.mark("chol(W), G = L^-1 M L^-H", k);
   // :130-133  theta, y = eigh(G); lambda = 1/theta
   heevd(ctx, g, (int)k, d_w, true, d_info);
   to_host(ctx, hw.data(), d_w, k);
+  tm.mark("eigh(G)", k);
   double tmin = INFINITY;
   for (double v : hw) tmin = std::min(tmin, std::fabs(v));
   if (tmin < 2.220446049250313e-16) throw BseError(BSE_EHERMITIAN_RQ, "reduced spectrum touches zero; cannot invert");
@@ -569,6 +629,7 @@ void bse_ctx_destroy(bse_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->sws) cudaFree(ctx->sws);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   free(ctx->hws);
   if (ctx->params) cusolverDnDestroyParams(ctx->params);
@@ -579,7 +640,7 @@ void bse_ctx_destroy(bse_ctx* ctx) {
 
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
-    const bool ok = complex_mults == 3 || complex_mults == 4 || (complex_mults >= 31 && complex_mults <= 34) ||
+    const bool ok = complex_mults == 3 || complex_mults == 4 || (complex_mults >= 31 && complex_mults <= 36) ||
                     (complex_mults >= 41 && complex_mults <= 43);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
@@ -752,18 +813,23 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, con
     zval* wvec = sc.take<zval>(kk);
     double* d_norm = sc.take<double>(k);
     zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
+    StepTimer tm(ctx, "rr_hermitian");
     // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T ; Q2^H Q2
     apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0);
+    tm.mark("T = S H Q", k);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
     zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
+    tm.mark("grams W, Q2^H Q2", k);
     Scratch rest = sc;
     rr_pencil(ctx, w, g2, k, h_lam, wvec, h_lam_min_m, rest);
+    tm.mark("pencil", k);
     // :135-136  V = Q w (sorted) ; unit columns
     zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, q, ldq, wvec, k, 0.0, vout, ldvout, gws);
     bse::colnorm_kernel<<<(int)k, 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
     check_launch(ctx);
     bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
     check_launch(ctx);
+    tm.mark("V = Q w, normalise", k);
   });
 }
 
@@ -823,17 +889,15 @@ int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const 
     SOLVER_OK(cusolverDnXgeev_bufferSize(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR,
                                          CUSOLVER_EIG_MODE_VECTOR, k, CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F,
                                          nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F, &dws, &hws));
-    void* dbuf = nullptr;
-    CUDA_OK(cudaMallocAsync(&dbuf, std::max<size_t>(dws, 16), ctx->stream));
+    void* dbuf = solver_ws(ctx, dws);
     void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
     SOLVER_OK(cusolverDnXgeev(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, k,
                               CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F, nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F,
                               dbuf, dws, hbuf, hws, d_info));
-    int info = 0;
-    CUDA_OK(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_OK(cudaFreeAsync(dbuf, ctx->stream));
+    int* info = reinterpret_cast<int*>(pinned(ctx, 1));
+    CUDA_OK(cudaMemcpyAsync(info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_OK(cudaStreamSynchronize(ctx->stream));
-    if (info != 0) throw BseError(BSE_ENUMERICAL, "general eigensolver failed (info " + std::to_string(info) + ")");
+    if (*info != 0) throw BseError(BSE_ENUMERICAL, "general eigensolver failed (info " + std::to_string(*info) + ")");
     std::vector<double> ev(2 * k);
     to_host(ctx, ev.data(), reinterpret_cast<double*>(d_ev), 2 * k);
     std::vector<int> order(k);

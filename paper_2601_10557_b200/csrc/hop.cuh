@@ -112,13 +112,13 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
 //      Ur = T1 - T2, Ui = T3 - T1 - T2, L'r = S1 + S2, L'i = S3 - S1 + S2.
 template <int CM>
 struct Acc {
-  static constexpr int N = CM == 3 ? 6 : 4;
+  static constexpr int N = (CM == 3 || CM == 5) ? 6 : 4;
 };
 
 template <int CM, int WM, int WN>
 __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][WN][2], int i, int j, int h, double& ur,
                                            double& ui, double& lr, double& li) {
-  if constexpr (CM == 3) {
+  if constexpr (CM == 3 || CM == 5) {
     const double t1 = acc[0][i][j][h], t2 = acc[1][i][j][h], t3 = acc[2][i][j][h];
     const double s1 = acc[3][i][j][h], s2 = acc[4][i][j][h], s3 = acc[5][i][j][h];
     ur = t1 - t2;
@@ -184,16 +184,18 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
         xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
       }
-      if constexpr (CM == 3) {
+      if constexpr (CM == 3 || CM == 5) {
         double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {
-          xas[j] = xa[j].re + xa[j].im;
-          xbs[j] = xb[j].re + xb[j].im;
+          xas[j] = CM == 5 ? xa[j].re : xa[j].re + xa[j].im;
+          xbs[j] = CM == 5 ? xb[j].im : xb[j].re + xb[j].im;
         }
 #pragma unroll
         for (int i = 0; i < C::WM; ++i) {
-          const double pr = pf[i].re, pi = pf[i].im, ps = pf[i].re + pf[i].im, pd = pf[i].re - pf[i].im;
+          const double pr = pf[i].re, pi = pf[i].im;
+          const double ps = CM == 5 ? pf[i].im : pf[i].re + pf[i].im;
+          const double pd = CM == 5 ? pf[i].re : pf[i].re - pf[i].im;
 #pragma unroll
           for (int j = 0; j < C::WN; ++j) {
             dmma(acc[0][i][j], pr, xa[j].re);

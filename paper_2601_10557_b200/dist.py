@@ -47,6 +47,28 @@ from .rayleigh_ritz import lock_converged, RitzSet
 from .solver import SolveResult, SolverConfig, TraceRecord, TAG_LANCZOS, TAG_SUBSPACE
 
 ZB = 16  # bytes per complex128
+_TIMING = __import__("os").environ.get("BSE200_TIMING") == "1"
+
+
+class _Steps:
+    """Opt-in step timer (BSE200_TIMING=1): device-synchronised wall time per step on rank 0."""
+
+    def __init__(self, name, rank):
+        self.name, self.on = name, _TIMING and rank == 0
+        if self.on:
+            import time
+            import torch
+
+            self.torch, self.time = torch, time
+            torch.cuda.synchronize()
+            self.t = time.perf_counter()
+
+    def mark(self, step, k=-1):
+        if self.on:
+            self.torch.cuda.synchronize()
+            t = self.time.perf_counter()
+            print(f"[dist {self.name} k={k}] {step:<24s} {1e3 * (t - self.t):8.2f} ms", flush=True)
+            self.t = t
 
 
 def grid_shape(world: int) -> tuple[int, int]:
@@ -363,17 +385,24 @@ class DistSolver:
 
     def cholqr(self, q_col):
         """Distributed CholQR2 (+ shifted CholQR3 fallback) of a col-layout block; returns (q, method)."""
+        st = _Steps("cholqr", self.g.rank)
         x0 = q_col.clone()
         q = q_col
         ok = True
         for _ in range(2):
-            rinv, info = self.ops.chol_rinv(self._gram_row(q))
+            gm = self._gram_row(q)
+            st.mark("gram + allreduce", q.shape[0])
+            rinv, info = self.ops.chol_rinv(gm)
+            st.mark("chol_rinv", q.shape[0])
             if info != 0:
                 ok = False
                 break
             q = self.ops.nn(q, rinv)
+            st.mark("Q R^-1", q.shape[0])
         if ok and self.ops.defect(self._gram_row(q)) <= 1e-8:
+            st.mark("defect", q.shape[0])
             return q, "cholqr"
+        st.mark("FALLBACK", q.shape[0])
         # shifted CholQR3 on the original block
         n2 = self.ops.colnorm2(x0)
         self.c.sum_row(n2)
@@ -397,28 +426,37 @@ class DistSolver:
 
     def s_orthonormalize(self, v_col, locked_col):
         """ortho.py:132-158 distributed: project out span(S Y), then CholQR2 (col layout)."""
+        st = _Steps("s_ortho", self.g.rank)
         if locked_col is not None and locked_col.shape[0]:
             basis, _ = self.cholqr(self.ops.sflip(locked_col))
+            st.mark("basis of S Y", locked_col.shape[0])
             proj = self._gram_row(basis, v_col)  # l x k
             self.ops.nn(basis, proj, out=v_col, alpha=-1.0, beta=1.0)
+            st.mark("projection", v_col.shape[0])
         return self.cholqr(v_col)
 
     # ---- Rayleigh-Ritz + residuals ------------------------------------------------------------
     def rayleigh_ritz(self, q_col, row_buf):
         """rayleigh_ritz.py:98-143 distributed; returns (lam, v_col, lambda_min_m)."""
         k = q_col.shape[0]
+        st = _Steps("rr", self.g.rank)
         t_row = row_buf[:k]
         self.forward(q_col, t_row, low_sign=-1.0)  # T = S H Q (rows R_I)
+        st.mark("T = S H Q", k)
         q_full = self.assemble_from_col(q_col)
+        st.mark("allgather Q", k)
         w = self.ops.gram(self.row_rows(q_full), t_row)
         self.c.sum_col(w)
         g2 = self.ops.gram(q_col[:, self.g.nc:], q_col[:, self.g.nc:])
         self.c.sum_row(g2)
+        st.mark("W, Q2^H Q2 + allreduce", k)
         lam, wvec, lmm = self.ops.rr_pencil(w, g2)
+        st.mark("pencil", k)
         v = self.ops.nn(q_col, wvec)
         n2 = self.ops.colnorm2(v)
         self.c.sum_row(n2)
         self.ops.colscale_rsqrt(v, n2)
+        st.mark("V = Q w, normalise", k)
         return lam, v, lmm
 
     def residuals(self, v_col, lam, row_buf) -> np.ndarray:
