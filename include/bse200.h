@@ -95,9 +95,11 @@ int bse_fix_phases(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq);
 /* Hermitian-equivalent oblique RR on the active basis Q (n x k):
  * h_lam (k) ascending Ritz values, d_vout (n x k) unit Ritz vectors,
  * *h_lam_min_m = |lambda|_min(Q*SQ).  BSE_EHERMITIAN_RQ when Q*SQ is
- * singular (< 1e-8), Q*SHQ is not positive definite, or theta ~ 0.        */
+ * singular (< 1e-8), Q*SHQ is not positive definite, or theta ~ 0.
+ * h_res (nullable): residual norms ||H v - lam v|| from the RR intermediate,
+ * H V = S (S H Q) w / |Q w| (rayleigh_ritz.py:182-190 without a second H product). */
 int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
-                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m);
+                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m, double* h_res);
 /* Non-hermitian backup projection (Alg. 3, rayleigh_ritz.py:146-179). */
 int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
                   double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m);
@@ -148,6 +150,10 @@ int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv
 /* Small pencil of the hermitian RR (rayleigh_ritz.py:113-137) from the summed W = Q^H S H Q
  * and G2 = Q2^H Q2: ascending Ritz values (host) and the sorted back-transform L^{-H} y (device). */
 int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec, double* h_lam_min_m);
+/* residual partials from the RR intermediate: out[j] = sum_i |sgn_i u_ij uscale_j - lam_j v_ij|^2,
+ * sgn_i = -1 for rows >= half (u = (S H Q) w, v = unit Ritz vectors, uscale = 1/|Q w|)            */
+int bse_resid_partial(bse_ctx* ctx, const void* d_u, int64_t ldu, const void* d_v, int64_t ldv, int64_t rows,
+                      int64_t half, int64_t k, const double* d_uscale, const double* d_lam, double* d_out);
 /* squared column norms of a rows x k block (device out); x /= sqrt(norm2) per column           */
 int bse_colnorm2(bse_ctx* ctx, const void* d_x, int64_t rows, int64_t k, int64_t ldx, double* d_out);
 int bse_colscale_rsqrt(bse_ctx* ctx, void* d_x, int64_t rows, int64_t k, int64_t ldx, const double* d_norm2);

@@ -60,13 +60,14 @@ _SIGS = {
     "bse_s_orthonormalize": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
     "bse_cholqr": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _ip]),
     "bse_fix_phases": (C.c_int, [_vp, _vp, _i64, _i64, _i64]),
-    "bse_rr_hermitian": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
+    "bse_rr_hermitian": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp, _dp]),
     "bse_rr_backup": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
     "bse_lanczos_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _dp, _dp, _ip]),
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
     "bse_chol_rinv": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _vp, _ip]),
     "bse_rr_pencil": (C.c_int, [_vp, _vp, _vp, _i64, _dp, _vp, _dp]),
+    "bse_resid_partial": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "bse_colnorm2": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_colscale_rsqrt": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_defect": (C.c_int, [_vp, _vp, _i64, _dp]),

@@ -387,3 +387,34 @@ __global__ void scale_shift_kernel(zval* a, int64_t ld, int64_t m, double scale,
 }
 
 }  // namespace bse
+
+namespace bse {
+
+// Residual partials from the RR intermediate: with T = S H Q and V = Q w / d,
+// H V = S T w / d, so  out[j] = sum_i | sgn_i u_ij uscale_j - lam_j v_ij |^2  with u = T w,
+// sgn_i = -1 on rows >= half.  One CTA per column, fixed-order block reduction.
+__global__ void resid_from_rr_kernel(const zval* __restrict__ u, int64_t ldu, const zval* __restrict__ v, int64_t ldv,
+                                     int64_t rows, int64_t half, const double* __restrict__ uscale,
+                                     const double* __restrict__ lam, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int64_t j = blockIdx.x;
+  const zval* uc = u + j * ldu;
+  const zval* vc = v + j * ldv;
+  const double sc = uscale[j], l = lam[j];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const zval a = uc[i], b = vc[i];
+    const double g = (i >= half) ? -sc : sc;
+    const double rr = g * a.re - l * b.re, ri = g * a.im - l * b.im;
+    s += rr * rr + ri * ri;
+  }
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) out[j] = s;
+}
+
+__global__ void recip_kernel(const double* __restrict__ in, double* __restrict__ out, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) out[i] = 1.0 / in[i];
+}
+
+}  // namespace bse

@@ -42,6 +42,8 @@ struct bse_ctx {
   int filter_cm = 4;  // complex multiplication of the Chebyshev products: 4 (4M) or 3 (3M / Gauss)
   void* sws = nullptr;  // persistent cuSOLVER device workspace (grows, never shrinks)
   size_t sws_bytes = 0;
+  void* gv = nullptr;  // split-K GEMV partials
+  size_t gv_bytes = 0;
 };
 
 namespace {
@@ -241,6 +243,32 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   }
 }
 
+// k == 1 products (Lanczos): split-K GEMV, partials in the context workspace tail
+void launch_gemv(bse_ctx* ctx, const bse::HopArgs& a) {
+  const int rb = (a.mr + bse::GV_THREADS - 1) / bse::GV_THREADS;
+  int nsplit = std::max(1, std::min(64, (148 * 8 + rb - 1) / rb));
+  nsplit = std::min(nsplit, std::max(1, a.kc / 64));
+  const int kchunk = (a.kc + nsplit - 1) / nsplit;
+  const size_t need = (size_t)nsplit * 2 * a.mr * sizeof(zval);
+  if (ctx->gv_bytes < need) {
+    if (ctx->gv) {
+      CUDA_OK(cudaStreamSynchronize(ctx->stream));
+      CUDA_OK(cudaFree(ctx->gv));
+    }
+    ctx->gv = nullptr;
+    ctx->gv_bytes = 0;
+    CUDA_OK(cudaMalloc(&ctx->gv, need));
+    ctx->gv_bytes = need;
+  }
+  zval* part = static_cast<zval*>(ctx->gv);
+  bse::gemv_partial_kernel<<<dim3(rb, nsplit), bse::GV_THREADS, 0, ctx->stream>>>(a.pa, a.pb, a.lda, a.mr, a.kc, a.x1,
+                                                                                 a.x2, kchunk, part);
+  check_launch(ctx);
+  bse::gemv_reduce_kernel<<<(2 * a.mr + 255) / 256, 256, 0, ctx->stream>>>(part, nsplit, a.mr, a.y1, a.y2, a.alpha,
+                                                                           a.low_sign);
+  check_launch(ctx);
+}
+
 bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, int64_t k) {
   bse::HopArgs a{};
   const zval* ab = static_cast<const zval*>(d_ab);
@@ -271,7 +299,10 @@ void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval*
   a.y2 = y + m;
   a.ldy = ldy;
   a.low_sign = low_sign;
-  launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+  if (k == 1)
+    launch_gemv(ctx, a);
+  else
+    launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
 }
 
 void filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* y, const zval* yprev,
@@ -630,6 +661,7 @@ void bse_ctx_destroy(bse_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->sws) cudaFree(ctx->sws);
+  if (ctx->gv) cudaFree(ctx->gv);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   free(ctx->hws);
   if (ctx->params) cusolverDnDestroyParams(ctx->params);
@@ -798,7 +830,7 @@ int bse_s_orthonormalize(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t 
 }
 
 int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
-                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
+                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m, double* h_res) {
   return guarded(ctx, [&] {
     if (k == 0) return;
     const int64_t n = 2 * m;
@@ -806,8 +838,13 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, con
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
     const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
-    Scratch sc(ctx, al(n * k * sizeof(zval)) + 3 * al(kk * sizeof(zval)) + al(k * 8) + gwsb + pencil_ws_bytes(k) + 4096);
+    Scratch sc(ctx, (h_res ? 2 : 1) * al(n * k * sizeof(zval)) + 3 * al(kk * sizeof(zval)) + 4 * al(k * 8) + gwsb +
+                        pencil_ws_bytes(k) + 4096);
     zval* t = sc.take<zval>(n * k);
+    zval* u = h_res ? sc.take<zval>(n * k) : nullptr;
+    double* d_lam = sc.take<double>(k);
+    double* d_rinv = sc.take<double>(k);
+    double* d_r2 = sc.take<double>(k);
     zval* w = sc.take<zval>(kk);
     zval* g2 = sc.take<zval>(kk);
     zval* wvec = sc.take<zval>(kk);
@@ -830,6 +867,19 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, con
     bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_norm);
     check_launch(ctx);
     tm.mark("V = Q w, normalise", k);
+    if (h_res) {
+      // residuals from the RR intermediate: H V = S T w / |Q w| (saves the H application of
+      // rayleigh_ritz.py:188; 8 n k^2 instead of 8 n^2 k)
+      zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, t, n, wvec, k, 0.0, u, n, gws);
+      to_device(ctx, d_lam, h_lam, k);
+      bse::recip_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(d_norm, d_rinv, (int)k);
+      check_launch(ctx);
+      bse::resid_from_rr_kernel<<<(int)k, 256, 0, ctx->stream>>>(u, n, vout, ldvout, n, m, d_rinv, d_lam, d_r2);
+      check_launch(ctx);
+      to_host(ctx, h_res, d_r2, k);
+      for (int64_t i = 0; i < k; ++i) h_res[i] = std::sqrt(h_res[i]);
+      tm.mark("residuals from S T w", k);
+    }
   });
 }
 
@@ -1031,7 +1081,10 @@ int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* t) {
     if ((a.shift != 0.0 || a.shift_col) && a.shift_hi > a.shift_lo && (!a.s1 || !a.s2))
       throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
     if (a.kc <= 0) throw BseError(BSE_EVALIDATION, "empty contraction");
-    if (t->filter)
+    const bool plain = a.beta == 0.0 && !a.shift_col && (a.shift == 0.0 || a.shift_hi <= a.shift_lo);
+    if (a.k == 1 && plain)
+      launch_gemv(ctx, a);
+    else if (t->filter)
       launch_filter_hop(ctx, a);
     else
       launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
@@ -1072,6 +1125,17 @@ int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam,
     Scratch sc(ctx, pencil_ws_bytes(k) + 4096);
     rr_pencil(ctx, static_cast<zval*>(d_w), static_cast<zval*>(d_g2), k, h_lam, static_cast<zval*>(d_wvec),
               h_lam_min_m, sc);
+  });
+}
+
+int bse_resid_partial(bse_ctx* ctx, const void* d_u, int64_t ldu, const void* d_v, int64_t ldv, int64_t rows,
+                      int64_t half, int64_t k, const double* d_uscale, const double* d_lam, double* d_out) {
+  return guarded(ctx, [&] {
+    if (k <= 0) return;
+    bse::resid_from_rr_kernel<<<(int)k, 256, 0, ctx->stream>>>(static_cast<const zval*>(d_u), ldu,
+                                                               static_cast<const zval*>(d_v), ldv, rows, half,
+                                                               d_uscale, d_lam, d_out);
+    check_launch(ctx);
   });
 }
 

@@ -321,4 +321,48 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// k = 1 (Lanczos matvecs): the same operator as an HBM-bound split-K GEMV.  Thread = output
+// row (coalesced column-major reads of the A and B tiles, x broadcast), per-split partials,
+// fixed-order reduction.  Per launch: 32 mr kc bytes of A|B read once.
+constexpr int GV_THREADS = 256;
+
+__global__ void __launch_bounds__(GV_THREADS) gemv_partial_kernel(const zval* __restrict__ pa, const zval* __restrict__ pb,
+                                                                  int64_t lda, int mr, int kc, const zval* __restrict__ x1,
+                                                                  const zval* __restrict__ x2, int kchunk,
+                                                                  zval* __restrict__ part) {
+  const int i = blockIdx.x * GV_THREADS + threadIdx.x;
+  const int j0 = blockIdx.y * kchunk, j1 = min(kc, j0 + kchunk);
+  if (i >= mr) return;
+  double ur = 0.0, ui = 0.0, lr = 0.0, li = 0.0;
+#pragma unroll 4
+  for (int j = j0; j < j1; ++j) {
+    const zval a = pa[(int64_t)j * lda + i], b = pb[(int64_t)j * lda + i];
+    const zval p = x1[j], q = x2[j];
+    ur += a.re * p.re - a.im * p.im + b.re * q.re - b.im * q.im;  // U  += a p + b q
+    ui += a.re * p.im + a.im * p.re + b.re * q.im + b.im * q.re;
+    lr += a.re * q.re + a.im * q.im + b.re * p.re + b.im * p.im;  // L' += conj(a) q + conj(b) p
+    li += a.re * q.im - a.im * q.re + b.re * p.im - b.im * p.re;
+  }
+  zval* out = part + (int64_t)blockIdx.y * 2 * mr;
+  out[i] = zval{ur, ui};
+  out[mr + i] = zval{lr, li};
+}
+
+__global__ void gemv_reduce_kernel(const zval* __restrict__ part, int nsplit, int mr, zval* __restrict__ y1,
+                                   zval* __restrict__ y2, double alpha, double low_sign) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= 2 * mr) return;
+  double sr = 0.0, si = 0.0;
+  for (int z = 0; z < nsplit; ++z) {
+    const zval v = part[(int64_t)z * 2 * mr + r];
+    sr += v.re;
+    si += v.im;
+  }
+  if (r < mr)
+    y1[r] = zval{alpha * sr, alpha * si};
+  else
+    y2[r - mr] = zval{-low_sign * alpha * sr, -low_sign * alpha * si};  // low half of H x is -L'
+}
+
 }  // namespace bse

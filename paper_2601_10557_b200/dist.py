@@ -238,6 +238,14 @@ class CudaOps:
     def colscale_rsqrt(self, x, n2):
         self.ctx.call("bse_colscale_rsqrt", _lib.dptr(x), x.shape[1], x.shape[0], x.stride(0), _lib.dptr(n2))
 
+    def resid_partial(self, u, v, half, uscale, lam):
+        """out[j] = sum_i |sgn_i u_ij uscale_j - lam_j v_ij|^2 (sgn = -1 on rows >= half)."""
+        k = u.shape[0]
+        out = self.torch.empty(k, dtype=self.torch.float64, device=self.device)
+        self.ctx.call("bse_resid_partial", _lib.dptr(u), u.stride(0), _lib.dptr(v), v.stride(0), u.shape[1], half, k,
+                      _lib.dptr(uscale), _lib.dptr(lam), _lib.dptr(out))
+        return out
+
     def defect(self, g) -> float:
         out = ctypes.c_double(0.0)
         self.ctx.call("bse_defect", _lib.dptr(g), g.shape[0], ctypes.byref(out))
@@ -436,8 +444,9 @@ class DistSolver:
         return self.cholqr(v_col)
 
     # ---- Rayleigh-Ritz + residuals ------------------------------------------------------------
-    def rayleigh_ritz(self, q_col, row_buf):
-        """rayleigh_ritz.py:98-143 distributed; returns (lam, v_col, lambda_min_m)."""
+    def rayleigh_ritz(self, q_col, row_buf, fused_residuals: bool = False):
+        """rayleigh_ritz.py:98-143 distributed; returns (lam, v_col, lambda_min_m, residuals or None).
+        fused_residuals: H V = S T w / |Q w| from T = S H Q (rows R_I), no second H product."""
         k = q_col.shape[0]
         st = _Steps("rr", self.g.rank)
         t_row = row_buf[:k]
@@ -457,7 +466,18 @@ class DistSolver:
         self.c.sum_row(n2)
         self.ops.colscale_rsqrt(v, n2)
         st.mark("V = Q w, normalise", k)
-        return lam, v, lmm
+        res = None
+        if fused_residuals:
+            torch = self.torch
+            u_row = self.ops.nn(t_row, wvec)
+            vq_row = self.ops.nn(self.row_rows(q_full), wvec)
+            ones = torch.ones(k, dtype=torch.float64, device=v.device)
+            lam_d = torch.as_tensor(np.ascontiguousarray(lam), dtype=torch.float64, device=v.device)
+            r2 = self.ops.resid_partial(u_row, vq_row, self.g.nr, ones, lam_d)
+            self.c.sum_col(r2)
+            res = np.sqrt(r2.cpu().numpy() / n2.cpu().numpy())
+            st.mark("residuals from S T w", k)
+        return lam, v, lmm, res
 
     def residuals(self, v_col, lam, row_buf) -> np.ndarray:
         k = v_col.shape[0]
@@ -564,15 +584,17 @@ class DistSolver:
             if nlock:
                 ledger.add_flops("ortho", 16.0 * n * nlock * k)
             ledger.add_flops("ortho", 2 * (8.0 * n * k * k + 4.0 * n * k * k))
+            from .solver import fused_residuals_for
+
             with ledger.timing("rr"):
                 try:
-                    lam, vecs, lmm = self.rayleigh_ritz(v, row_buf)
+                    lam, vecs, lmm, fres = self.rayleigh_ritz(v, row_buf, fused_residuals_for(cfg))
                 except HermitianRqError as exc:
                     raise NumericalError(f"hermitian projection failed at iteration {it} (distributed backup "
                                          f"projection not available): {exc}") from exc
             ledger.add_flops("rr", 8.0 * n * n * k + 8.0 * n * n * k + 12.0 * n * k * k + 16.0 * k**3)
             with ledger.timing("residuals"):
-                res = self.residuals(vecs, lam, row_buf)
+                res = fres if fres is not None else self.residuals(vecs, lam, row_buf)
             ledger.add_flops("residuals", 8.0 * n * n * k)
             ritz = RitzSet(values=lam, vectors=None, residual_norms=res)
             new, act = lock_converged(ritz, tol, nev - nlock, normalizer)

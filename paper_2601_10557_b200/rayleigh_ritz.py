@@ -54,16 +54,18 @@ class RitzSet:
         return self.values.shape[0]
 
 
-def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger):
+def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residuals: bool = False):
     n, k = q.shape
     lam = np.zeros(k)
     vout = colmajor_empty(n, k, q.device)
     lmm = ctypes.c_double(float("nan"))
     ab = ham.device_blocks(q.device)
     ctx = _lib.Context.get(q.device.index)
+    res = np.zeros(k) if fused_residuals else None
+    extra = (_lib.hptr(res) if fused_residuals else None,) if entry == "bse_rr_hermitian" else ()
     try:
         ctx.call(entry, _lib.dptr(ab), ld_of(ab), ham.m, _lib.dptr(q), ld_of(q), k, _lib.hptr(lam), _lib.dptr(vout),
-                 ld_of(vout), ctypes.byref(lmm))
+                 ld_of(vout), ctypes.byref(lmm), *extra)
     finally:
         if ledger is not None:
             # apply_h inside RR charges 8n^2k to "rr" (hamiltonian.py:148-150) before the model of
@@ -72,11 +74,13 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger):
     if ledger is not None:
         extra = (12.0 * n * k * k + 16.0 * k**3) if variant == "hermitian" else (20.0 * n * k * k + 30.0 * k**3)
         ledger.add_flops("rr", 8.0 * n * n * k + extra)
-    return RitzSet(values=lam, vectors=vout), ReducedProblem(variant=variant, lambda_min_m=lmm.value)
+    return RitzSet(values=lam, vectors=vout, residual_norms=res), ReducedProblem(variant=variant, lambda_min_m=lmm.value)
 
 
-def build_hermitian_rq_device(ham, q, ledger=None):
-    return _rr("bse_rr_hermitian", "hermitian", ham, q, ledger)
+def build_hermitian_rq_device(ham, q, ledger=None, fused_residuals: bool = False):
+    """fused_residuals: also return ||H v - lam v|| computed as |S (S H Q) w / |Q w| - lam v|
+    (saves the residual H application; differs from the explicit product at roundoff)."""
+    return _rr("bse_rr_hermitian", "hermitian", ham, q, ledger, fused_residuals)
 
 
 def build_backup_rq_device(ham, q, ledger=None):

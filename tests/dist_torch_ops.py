@@ -82,6 +82,12 @@ class TorchOps:
         wv = torch.linalg.solve_triangular(ell.conj().T, y, upper=True)[:, torch.as_tensor(order)]
         return lam[order], wv.T.contiguous(), lmm
 
+    def resid_partial(self, u, v, half, uscale, lam):
+        sg = torch.ones(u.shape[1], dtype=torch.float64)
+        sg[half:] = -1.0
+        r = sg[None, :] * u * uscale[:, None] - lam[:, None] * v
+        return (r.real ** 2 + r.imag ** 2).sum(dim=1)
+
     def colnorm2(self, x):
         return (x.real ** 2 + x.imag ** 2).sum(dim=1)
 

@@ -26,7 +26,7 @@ def _rel(a, b):
 
 
 # ------------------------------------------------------------------ operators
-@pytest.mark.parametrize("m,k", [(1, 1), (3, 2), (16, 5), (37, 13), (64, 33), (130, 70), (257, 40)])
+@pytest.mark.parametrize("m,k", [(1, 1), (3, 2), (16, 5), (37, 13), (64, 33), (130, 70), (257, 40), (300, 1), (2001, 1)])
 def test_apply_h_matches_oracle(bse, m, k):
     rs = np.random.default_rng(m * 100 + k)
     a0 = rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m))
@@ -305,3 +305,26 @@ def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance):
     assert r.converged and abs(r.iterations_used - int(gc["abs_iters"])) <= 1
     assert (np.abs(r.lambdas - gc["abs_lambdas"]) / np.abs(gc["abs_lambdas"])).max() <= 1e-10
     assert r.residual_norms.max() <= 1e-10
+
+
+def test_fused_residuals_match_explicit(bse, c1_instance):
+    """(H Q) w residuals vs the explicit H (Q w) product of rayleigh_ritz.py:188."""
+    from paper_2601_10557_b200.hamiltonian import to_colmajor
+    from paper_2601_10557_b200.rayleigh_ritz import build_hermitian_rq_device, residuals_device
+
+    a, b, _ = c1_instance
+    ham = bse.BseHamiltonian(a, b)
+    g = golden("ops_m16_s5.npz")
+    rs = np.random.default_rng(0)
+    for h, q in ((bse.BseHamiltonian(*golden_ham(16, 5)), g["q"]),
+                 (ham, np.linalg.qr(rs.standard_normal((1000, 40)) + 1j * rs.standard_normal((1000, 40)))[0])):
+        qd = to_colmajor(q, torch.device("cuda", 0))
+        r, _ = build_hermitian_rq_device(h, qd, fused_residuals=True)
+        explicit = residuals_device(h, r.values, r.vectors)
+        scale = np.abs(r.values).max()
+        assert np.all(np.abs(r.residual_norms - explicit) <= 1e-12 * scale + 1e-10 * explicit)
+    # a full C1 solve under the relative policy with fused residuals keeps parity
+    r = bse.solve(ham, bse.SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0, rel_res=True))
+    gc = c1_instance[2]
+    assert r.converged and abs(r.iterations_used - int(gc["rel_iters"])) <= 1
+    assert (np.abs(r.lambdas - gc["rel_lambdas"]) / np.abs(gc["rel_lambdas"])).max() <= 1e-10
