@@ -55,6 +55,7 @@ const char* bse_version(void);
  * complex block pair, default) or 3 (3M / Gauss, 6 DMMA: 25% fewer FP64 tensor ops; error bound
  * grows to ~eps (|Re|+|Im|)^2).  RR and residual products always use 4M.          */
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults);
+/* (code 6 = 3M using the precomputed sum planes when the caller passes them)                   */
 
 /* ---- Hamiltonian operator ------------------------------------------------ */
 /* y = H x  (low_sign = +1)  or  y = S H x  (low_sign = -1)
@@ -65,15 +66,19 @@ int bse_apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const vo
 
 /* One Chebyshev step y_next = alpha (H y - c y) - beta y_prev, fused in the
  * GEMM epilogue (chebyshev.py:68-74).  y_next may alias y_prev, not y.    */
-int bse_filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_y, const void* d_yprev,
-                    void* d_ynext, int64_t ld, int64_t k, double c, double alpha, double beta);
+int bse_filter_step(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_y,
+                    const void* d_yprev, void* d_ynext, int64_t ld, int64_t k, double c, double alpha, double beta);
 
 /* Whole filter p(H) V (chebyshev.py:51-75): degree `deg` (even) products,
  * sigma-scaled recurrence with c = center, e = half_width, s = scale_ref.
  * d_v (n x k, ld) is overwritten with the result; d_work must hold 2 n x k
  * blocks with the same ld (rotating recurrence buffers).                   */
-int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_v, int64_t ld, int64_t k,
-                         int deg, double c, double e, double s, void* d_work);
+int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, void* d_v,
+                         int64_t ld, int64_t k, int deg, double c, double e, double s, void* d_work);
+/* 3M operand sums: d_sd (same shape / lda as d_ab, m x cols) <- (re + im, re - im) of d_ab.
+ * Passed as d_sd to the filter entry points, it removes the P-side adds from the 3M kernel's
+ * critical path (+32 m^2 bytes).  d_sd may be NULL everywhere (sums formed on the fly).      */
+int bse_make_sum_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int64_t cols, void* d_sd);
 
 /* Residual norms r_j = ||H v_j - lam_j v_j||_2 (rayleigh_ritz.py:182-190),
  * fused residual-norm epilogue; h_lam (k) in, h_res (k) out on host.      */
@@ -125,6 +130,8 @@ int bse_is_definite(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int*
 typedef struct {
   const void* pa;
   const void* pb;
+  const void* sa; /* optional 3M sum planes of pa / pb (bse_make_sum_planes), may be NULL */
+  const void* sb;
   int64_t lda, mr, kc;
   const void* x1;
   const void* x2;

@@ -34,7 +34,7 @@ class HopTileArgs(C.Structure):
     """bse_hop_tile_args (include/bse200.h)."""
 
     _fields_ = [
-        ("pa", _vp), ("pb", _vp), ("lda", _i64), ("mr", _i64), ("kc", _i64),
+        ("pa", _vp), ("pb", _vp), ("sa", _vp), ("sb", _vp), ("lda", _i64), ("mr", _i64), ("kc", _i64),
         ("x1", _vp), ("x2", _vp), ("ldx", _i64), ("k", _i64),
         ("y1", _vp), ("y2", _vp), ("ldy", _i64),
         ("s1", _vp), ("s2", _vp), ("lds", _i64), ("shift_lo", _i64), ("shift_hi", _i64),
@@ -54,8 +54,9 @@ _SIGS = {
     "bse_last_error": (C.c_char_p, [_vp]),
     "bse_launch_count": (_i64, [_vp]),
     "bse_apply_h": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _dbl]),
-    "bse_filter_step": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _dbl]),
-    "bse_chebyshev_filter": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
+    "bse_filter_step": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _dbl]),
+    "bse_chebyshev_filter": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
+    "bse_make_sum_planes": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_residuals": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _dp]),
     "bse_s_orthonormalize": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
     "bse_cholqr": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _ip]),
@@ -95,20 +96,26 @@ _STATUS = {
 _lib = None
 _lock = threading.Lock()
 # complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
-_FILTER_CM = {"3m": 3, "4m": 4}[os.environ.get("BSE200_FILTER", "4m").lower()]
+_ALGOS = {"4m": 4, "3m": 6, "3m-onthefly": 3}
+_FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "4m").lower()]
 
 
 def set_filter_algorithm(name: str) -> None:
-    """'4m' (default) or '3m' (Gauss: 25% fewer FP64 tensor ops in the filter) for every context."""
+    """'4m' (default), '3m' (Gauss: 25% fewer FP64 tensor ops in the filter, with the operand sums of
+    A and B precomputed once, +32 m^2 bytes) or '3m-onthefly' (sums formed in registers)."""
     global _FILTER_CM
-    cm = {"3m": 3, "4m": 4}[name.lower()]
+    cm = _ALGOS[name.lower()] if isinstance(name, str) else int(name)
     _FILTER_CM = cm
     for ctx in Context._by_device.values():
         ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, cm))
 
 
 def filter_algorithm() -> str:
-    return f"{_FILTER_CM}m"
+    return {v: k for k, v in _ALGOS.items()}.get(_FILTER_CM, str(_FILTER_CM))
+
+
+def uses_sum_planes() -> bool:
+    return _FILTER_CM == 6 or 61 <= _FILTER_CM <= 63
 
 
 def load() -> C.CDLL:

@@ -50,8 +50,9 @@ def filter_inplace(ham: BseHamiltonian, v, cfg: FilterConfig, work=None, ledger:
 
         work = torch.empty(2 * ld_of(v) * k, dtype=torch.complex128, device=v.device)
     ab = ham.device_blocks(v.device)
+    sd = _lib.dptr(ham.device_sum_planes(v.device)) if _lib.uses_sum_planes() else None
     ctx = _lib.Context.get(v.device.index)
-    ctx.call("bse_chebyshev_filter", _lib.dptr(ab), ld_of(ab), ham.m, _lib.dptr(v), ld_of(v), k, cfg.degree,
+    ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(v), ld_of(v), k, cfg.degree,
              cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))
     if ledger is not None:
         ledger.add_flops("filter", cfg.degree * 8.0 * n * n * k)

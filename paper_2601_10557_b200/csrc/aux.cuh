@@ -418,3 +418,18 @@ __global__ void recip_kernel(const double* __restrict__ in, double* __restrict__
 }
 
 }  // namespace bse
+
+namespace bse {
+
+// sd[i, j] = (re + im, re - im) of an m x cols column-major block (3M operand sums, built once)
+__global__ void sum_planes_kernel(const zval* __restrict__ a, int64_t lda, int64_t m, int64_t cols,
+                                  zval* __restrict__ sd) {
+  const int64_t total = m * cols;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m, j = idx / m;
+    const zval v = a[j * lda + i];
+    sd[j * lda + i] = zval{v.re + v.im, v.re - v.im};
+  }
+}
+
+}  // namespace bse

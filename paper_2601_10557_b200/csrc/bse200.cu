@@ -225,10 +225,21 @@ using Hop3M_1 = bse::HopCfg<64, 32, 8, 2, 2, 6, 1>;
 using Hop3M_2 = bse::HopCfg<64, 16, 8, 2, 1, 4, 2>;
 using Hop3M_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1>;
 using Hop3M_4 = bse::HopCfg<96, 32, 16, 2, 2, 4, 1>;
+// 3M with precomputed P-side sums (code 6 and tuning variants 61-63)
+using Hop3MS = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1>;
+using Hop3MS_1 = bse::HopCfg<64, 32, 8, 2, 2, 4, 1, 1>;
+using Hop3MS_2 = bse::HopCfg<64, 32, 16, 2, 2, 3, 1, 1>;
+using Hop3MS_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
 
 // Chebyshev-step products: 4M (default) or 3M as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
-  switch (ctx->filter_cm) {
+  int code = ctx->filter_cm;
+  if ((code == 6 || (code >= 61 && code <= 63)) && (!a.sa || !a.sb)) code = 3;  // no sum planes: sums on the fly
+  switch (code) {
+    case 6: launch_hop<Hop3MS, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 61: launch_hop<Hop3MS_1, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 62: launch_hop<Hop3MS_2, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 63: launch_hop<Hop3MS_3, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
@@ -305,9 +316,13 @@ void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval*
     launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
 }
 
-void filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* y, const zval* yprev,
-                 zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
+void filter_step(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const zval* y,
+                 const zval* yprev, zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
   bse::HopArgs a = hop_args_single(d_ab, lda, m, y, ld, k);
+  if (d_sd) {
+    a.sa = static_cast<const zval*>(d_sd);
+    a.sb = a.sa + m * lda;
+  }
   a.y1 = ynext;
   a.y2 = ynext + m;
   a.ldy = ld;
@@ -672,8 +687,9 @@ void bse_ctx_destroy(bse_ctx* ctx) {
 
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
-    const bool ok = complex_mults == 3 || complex_mults == 4 || (complex_mults >= 31 && complex_mults <= 36) ||
-                    (complex_mults >= 41 && complex_mults <= 43);
+    const bool ok = complex_mults == 3 || complex_mults == 4 || complex_mults == 6 ||
+                    (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
+                    (complex_mults >= 61 && complex_mults <= 63);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
   });
@@ -698,18 +714,27 @@ int bse_apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const vo
   });
 }
 
-int bse_filter_step(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_y, const void* d_yprev,
-                    void* d_ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
+int bse_filter_step(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_y,
+                    const void* d_yprev, void* d_ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
   return guarded(ctx, [&] {
     if (m < 0 || k < 0 || lda < m || ld < 2 * m) throw BseError(BSE_EVALIDATION, "bad shapes");
     if (k == 0 || m == 0) return;
-    filter_step(ctx, d_ab, lda, m, static_cast<const zval*>(d_y), static_cast<const zval*>(d_yprev),
+    filter_step(ctx, d_ab, d_sd, lda, m, static_cast<const zval*>(d_y), static_cast<const zval*>(d_yprev),
                 static_cast<zval*>(d_ynext), ld, k, c, alpha, beta);
   });
 }
 
-int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_v, int64_t ld, int64_t k,
-                         int deg, double c, double e, double s, void* d_work) {
+int bse_make_sum_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int64_t cols, void* d_sd) {
+  return guarded(ctx, [&] {
+    if (m <= 0 || cols <= 0) return;
+    bse::sum_planes_kernel<<<grid1d(m * cols, 256, 148 * 32), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ab), lda,
+                                                                                   m, cols, static_cast<zval*>(d_sd));
+    check_launch(ctx);
+  });
+}
+
+int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, void* d_v,
+                         int64_t ld, int64_t k, int deg, double c, double e, double s, void* d_work) {
   return guarded(ctx, [&] {
     if (deg < 2 || deg % 2) throw BseError(BSE_EVALIDATION, "filter degree must be even and >= 2");
     if (!(e > 0)) throw BseError(BSE_EVALIDATION, "filter half width must be positive");
@@ -720,12 +745,12 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m,
     const double sigma1 = e / (s - c);
     double sigma = sigma1;
     int prev = 0, cur = 1;
-    filter_step(ctx, d_ab, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0);
+    filter_step(ctx, d_ab, d_sd, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0);
     for (int step = 2; step <= deg; ++step) {
       const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
       const int nxt = 3 - prev - cur;
       // y_next = (2 s'/e)(H y - c y) - (s s') y_prev ; written over the free buffer
-      filter_step(ctx, d_ab, lda, m, bufs[cur], bufs[prev], bufs[nxt], ld, k, c, 2.0 * sigma_new / e,
+      filter_step(ctx, d_ab, d_sd, lda, m, bufs[cur], bufs[prev], bufs[nxt], ld, k, c, 2.0 * sigma_new / e,
                   sigma * sigma_new);
       prev = cur;
       cur = nxt;
@@ -1054,6 +1079,8 @@ int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* t) {
     bse::HopArgs a{};
     a.pa = static_cast<const zval*>(t->pa);
     a.pb = static_cast<const zval*>(t->pb);
+    a.sa = static_cast<const zval*>(t->sa);
+    a.sb = static_cast<const zval*>(t->sb);
     a.lda = t->lda;
     a.mr = (int)t->mr;
     a.kc = (int)t->kc;

@@ -28,6 +28,9 @@ struct HopArgs {
   const zval* pa;
   const zval* pb;
   int64_t lda;
+  // 3M with precomputed operand sums (CM == 6): (Pr + Pi, Pr - Pi) planes of the same tiles
+  const zval* sa;
+  const zval* sb;
   int mr;  // output rows per half
   int kc;  // contraction length per part
   // X operand rows for the contraction: x1 (rows of the "upper" half), x2 ("lower")
@@ -55,17 +58,18 @@ struct HopArgs {
   double* partial;    // [gridDim.y][k]
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_, int PS_ = 0>
 struct HopCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_, PS = PS_;
   static constexpr int WARPS_M = BM / (8 * WM);
   static constexpr int WARPS_N = BN / (8 * WN);
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int LDP = BM + 2;  // == 2 (mod 8): conflict-free LDS.128 A fragments
   static constexpr int LDX = BK + 4;  // == 4 (mod 8): conflict-free LDS.128 B fragments
   static constexpr int P_ELEMS = BK * LDP;
+  static constexpr int SD_ELEMS = PS ? BK * LDP : 0;  // (Pr+Pi, Pr-Pi) tile, same layout as P
   static constexpr int X_ELEMS = BN * LDX;
-  static constexpr int STAGE_ELEMS = P_ELEMS + 2 * X_ELEMS;
+  static constexpr int STAGE_ELEMS = P_ELEMS + SD_ELEMS + 2 * X_ELEMS;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(zval);
   static_assert(BM % 8 == 0 && BK % 8 == 0 && BN % 8 == 0, "tile dims");
 };
@@ -76,10 +80,12 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
   const int part = kt >= nkt_part;
   const int j0 = (kt - part * nkt_part) * C::BK;
   const zval* P = part ? a.pb : a.pa;
+  const zval* SD = part ? a.sb : a.sa;
   const zval* XA = part ? a.x2 : a.x1;
   const zval* XB = part ? a.x1 : a.x2;
   zval* Ps = st;
-  zval* Xas = st + C::P_ELEMS;
+  zval* SDs = st + C::P_ELEMS;
+  zval* Xas = SDs + C::SD_ELEMS;
   zval* Xbs = Xas + C::X_ELEMS;
 #pragma unroll
   for (int r = 0; r < (C::BK * C::BM + C::THREADS - 1) / C::THREADS; ++r) {
@@ -90,6 +96,7 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
     const bool ok = (gi < a.mr) && (gj < a.kc);
     const zval* src = ok ? P + (int64_t)gj * a.lda + gi : P;
     cp_async16(Ps + jj * C::LDP + ii, src, ok);
+    if constexpr (C::PS) cp_async16(SDs + jj * C::LDP + ii, ok ? SD + (int64_t)gj * a.lda + gi : SD, ok);
   }
 #pragma unroll
   for (int r = 0; r < (2 * C::BN * C::BK + C::THREADS - 1) / C::THREADS; ++r) {
@@ -112,13 +119,13 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
 //      Ur = T1 - T2, Ui = T3 - T1 - T2, L'r = S1 + S2, L'i = S3 - S1 + S2.
 template <int CM>
 struct Acc {
-  static constexpr int N = (CM == 3 || CM == 5) ? 6 : 4;
+  static constexpr int N = (CM == 3 || CM == 5 || CM == 6) ? 6 : 4;
 };
 
 template <int CM, int WM, int WN>
 __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][WN][2], int i, int j, int h, double& ur,
                                            double& ui, double& lr, double& li) {
-  if constexpr (CM == 3 || CM == 5) {
+  if constexpr (CM == 3 || CM == 5 || CM == 6) {
     const double t1 = acc[0][i][j][h], t2 = acc[1][i][j][h], t3 = acc[2][i][j][h];
     const double s1 = acc[3][i][j][h], s2 = acc[4][i][j][h], s3 = acc[5][i][j][h];
     ur = t1 - t2;
@@ -171,7 +178,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
       cp_async_commit();
     }
     const zval* Ps = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
-    const zval* Xas = Ps + C::P_ELEMS;
+    const zval* SDs = Ps + C::P_ELEMS;
+    const zval* Xas = SDs + C::SD_ELEMS;
     const zval* Xbs = Xas + C::X_ELEMS;
 #pragma unroll
     for (int ks = 0; ks < C::BK / 4; ++ks) {
@@ -184,7 +192,31 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
         xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
       }
-      if constexpr (CM == 3 || CM == 5) {
+      if constexpr (CM == 6) {
+        // 3M with the P-side sums read from shared memory: only the X-side sums remain on the
+        // DMMA critical path
+        zval sd[C::WM];
+#pragma unroll
+        for (int i = 0; i < C::WM; ++i) sd[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
+        double xas[C::WN], xbs[C::WN];
+#pragma unroll
+        for (int j = 0; j < C::WN; ++j) {
+          xas[j] = xa[j].re + xa[j].im;
+          xbs[j] = xb[j].re + xb[j].im;
+        }
+#pragma unroll
+        for (int i = 0; i < C::WM; ++i) {
+#pragma unroll
+          for (int j = 0; j < C::WN; ++j) {
+            dmma(acc[0][i][j], pf[i].re, xa[j].re);
+            dmma(acc[1][i][j], pf[i].im, xa[j].im);
+            dmma(acc[2][i][j], sd[i].re, xas[j]);
+            dmma(acc[3][i][j], pf[i].re, xb[j].re);
+            dmma(acc[4][i][j], pf[i].im, xb[j].im);
+            dmma(acc[5][i][j], sd[i].im, xbs[j]);
+          }
+        }
+      } else if constexpr (CM == 3 || CM == 5) {
         double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {

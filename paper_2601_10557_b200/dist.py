@@ -179,6 +179,8 @@ class CudaOps:
         xa, ya = x.data_ptr(), y.data_ptr()
         args = _lib.HopTileArgs()
         args.pa, args.pb, args.lda, args.mr, args.kc = tile.pa, tile.pb, tile.lda, mr, kc
+        if filter and tile.sd is not None:
+            args.sa, args.sb = tile.sa, tile.sb
         args.x1, args.x2, args.ldx, args.k = xa, xa + kc * ZB, x.stride(0), k
         args.y1, args.y2, args.ldy = ya, ya + mr * ZB, y.stride(0)
         lo, hi = shift_rows
@@ -259,7 +261,8 @@ class CudaOps:
 
 @dataclass
 class Tile:
-    """[P_A | P_B] of one tile product: pa, pb device addresses, mr x kc each, leading dim lda."""
+    """[P_A | P_B] of one tile product: pa, pb device addresses, mr x kc each, leading dim lda;
+    sd: optional 3M sum planes of the same tile (sa, sb addresses)."""
 
     buf: object
     pa: int
@@ -267,6 +270,20 @@ class Tile:
     lda: int
     mr: int
     kc: int
+    sd: object = None
+    sa: int = 0
+    sb: int = 0
+
+
+def add_sum_planes(ops, tile: Tile) -> Tile:
+    """Attach the 3M (re+im, re-im) planes of the tile (CUDA ops only)."""
+    if not hasattr(ops, "ctx"):
+        return tile
+    sd = ops.torch.empty_like(tile.buf)
+    ops.ctx.call("bse_make_sum_planes", tile.buf.data_ptr(), tile.lda, tile.mr, 2 * tile.kc, sd.data_ptr())
+    tile.sd, tile.sa = sd, sd.data_ptr()
+    tile.sb = tile.sa + tile.mr * tile.kc * ZB
+    return tile
 
 
 def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
@@ -289,6 +306,8 @@ def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
 
     fwd = one((grid.r0, grid.r1), (grid.c0, grid.c1))
     trn = one((grid.c0, grid.c1), (grid.r0, grid.r1))
+    if _lib.uses_sum_planes():
+        fwd, trn = add_sum_planes(ops, fwd), add_sum_planes(ops, trn)
     return fwd, trn
 
 
@@ -708,7 +727,8 @@ def make_tiles_from_pieces(ops, pieces: dict):
             src = torch.from_numpy(np.ascontiguousarray(blk.T)) if isinstance(blk, np.ndarray) else blk.T
             buf[h * kc:(h + 1) * kc].copy_(src)
         addr = buf.data_ptr()
-        tiles.append(Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc))
+        t = Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc)
+        tiles.append(add_sum_planes(ops, t) if _lib.uses_sum_planes() else t)
     return tuple(tiles)
 
 

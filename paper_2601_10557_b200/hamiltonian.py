@@ -158,7 +158,22 @@ class BseHamiltonian:
             self._dev[device] = ab
         return ab
 
+    def device_sum_planes(self, device):
+        """(re+im, re-im) planes of [A | B] for the 3M filter (bse_make_sum_planes), built once per device."""
+        torch = _torch()
+        device = torch.device(device)
+        sd_cache = self.__dict__.setdefault("_sd", {})
+        sd = sd_cache.get(device)
+        if sd is None:
+            ab = self.device_blocks(device)
+            sd = colmajor_empty(ab.shape[0], ab.shape[1], device)
+            _lib.Context.get(device.index).call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), ab.shape[0],
+                                                ab.shape[1], _lib.dptr(sd))
+            sd_cache[device] = sd
+        return sd
+
     def release_device(self) -> None:
+        self.__dict__.get("_sd", {}).clear()
         if self.a is not None:
             self._dev.clear()
 

@@ -287,7 +287,8 @@ def test_c1_parity(bse, c1_instance):
         assert np.abs(ov - 1).max() <= 1e-8
 
 
-def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance):
+@pytest.mark.parametrize("algo", ["3m", "3m-onthefly"])
+def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
     a, b = golden_ham(16, 5)
@@ -295,7 +296,7 @@ def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance):
     ham = bse.BseHamiltonian(a, b)
     cfg = bse.FilterConfig(int(g["deg"]), float(g["center"]), float(g["half_width"]), float(g["scale_ref"]))
     try:
-        bse.set_filter_algorithm("3m")
+        bse.set_filter_algorithm(algo)
         out3 = bse.chebyshev_filter(ham, g["x"], cfg)
         a1, b1, gc = c1_instance
         r = bse.solve(bse.BseHamiltonian(a1, b1), bse.SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0))

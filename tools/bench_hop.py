@@ -20,7 +20,7 @@ def run(m, k, reps=5):
     y = colmajor_empty(n, k, dev); y.real.normal_(); y.imag.normal_()
     yp = colmajor_empty(n, k, dev); yp.real.normal_(); yp.imag.normal_()
     ctx = _lib.Context.get(0)
-    args = lambda: (_lib.dptr(ab), ld_of(ab), m, _lib.dptr(y), _lib.dptr(yp), _lib.dptr(yp), n, k, 0.1, 1e-3, 0.5)
+    args = lambda: (_lib.dptr(ab), None, ld_of(ab), m, _lib.dptr(y), _lib.dptr(yp), _lib.dptr(yp), n, k, 0.1, 1e-3, 0.5)
     for _ in range(2):
         ctx.call("bse_filter_step", *args())
     torch.cuda.synchronize()

@@ -63,11 +63,12 @@ def main(m, k, l):
     print(f"  grams + rr_pencil:        {wall(pencil):.1f} ms")
     wk = w.clone()
     print(f"  eigvalsh k x k:           {wall(lambda: ctx.call('bse_eigvalsh', _lib.dptr(wk), k, k, _lib.hptr(lam))):.1f} ms")
-    for alg in ("4m", "3m"):
+    for alg in ("4m", "3m", "3m-onthefly"):
         bse.set_filter_algorithm(alg)
+        sdp = _lib.dptr(ham.device_sum_planes(dev)) if alg == "3m" else None
         yp = v0.clone()
         yn = colmajor_empty(n, k, dev)
-        ms = wall(lambda: ctx.call("bse_filter_step", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(v), _lib.dptr(yp),
+        ms = wall(lambda: ctx.call("bse_filter_step", _lib.dptr(ab), sdp, ld_of(ab), m, _lib.dptr(v), _lib.dptr(yp),
                                    _lib.dptr(yn), n, k, 0.1, 1e-3, 0.5), reps=3)
         print(f"  filter step {alg}: {ms:.1f} ms = {8.0 * n * n * k / ms / 1e9:.2f} TFLOP/s (model)")
     bse.set_filter_algorithm("4m")

@@ -32,16 +32,19 @@ def variants(m, ks, codes):
     ab = colmajor_empty(m, 2 * m, dev)
     ab.real.normal_()
     ab.imag.normal_()
+    sd = colmajor_empty(m, 2 * m, dev)
+    ctx.call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), m, 2 * m, _lib.dptr(sd))
     for k in ks:
         y = colmajor_empty(n, k, dev); y.real.normal_(); y.imag.normal_()
         yp = colmajor_empty(n, k, dev); yp.real.normal_(); yp.imag.normal_()
         yn = colmajor_empty(n, k, dev)
         for code in codes:
             ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
-            ms = timed(lambda: ctx.call("bse_filter_step", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(y), _lib.dptr(yp),
+            sdp = _lib.dptr(sd) if code == 6 or 61 <= code <= 63 else None
+            ms = timed(lambda: ctx.call("bse_filter_step", _lib.dptr(ab), sdp, ld_of(ab), m, _lib.dptr(y), _lib.dptr(yp),
                                         _lib.dptr(yn), n, k, 0.1, 1e-3, 0.5), 3 if m >= 20000 else 5)
             tf = 8.0 * n * n * k / ms / 1e9
-            cm = 3 if code in (3, 31, 32, 33, 34) else 4
+            cm = 3 if code in (3, 31, 32, 33, 34, 6, 61, 62, 63) else 4
             print(f"m={m} k={k} code={code}: {ms:8.2f} ms  model {tf:6.2f} TF/s  executed {tf * (0.75 if cm == 3 else 1):6.2f}",
                   flush=True)
     ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 4))
