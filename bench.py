@@ -326,6 +326,8 @@ def run_ours(args, world, rank, local):
 
     peak, peak_src = fp64_peak()
     achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
+    algo = _lib.filter_algorithm()
+    exec_ratio = 0.75 if algo.startswith("3m") else 1.0  # 3M: 6 real DMMA per complex block pair instead of 8
     total_model = res.ledger.total_flops()
     if rank == 0 and args.config != "c1" and world == 1:
         TRACE_FILE.parent.mkdir(exist_ok=True)
@@ -359,10 +361,14 @@ def run_ours(args, world, rank, local):
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "kernel": "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)",
                          "peak_source": peak_src,
-                         "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model) per GPU, summed over "
-                                        "the solve's filter calls / CUDA-event (1 GPU) or synchronised (N GPUs) "
-                                        "time of those calls"},
+                         "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model, BASELINE.md §3.5) "
+                                        "per GPU, summed over the solve's filter calls / CUDA-event (1 GPU) or "
+                                        "synchronised (N GPUs) time of those calls; with the 3M filter the DMMA pipe "
+                                        "executes 6 n^2 k (filter_executed_*)"},
             "filter_tflops_per_gpu": achieved, "filter_frac_of_fp64_peak": (achieved / peak) if achieved else None,
+            "filter_algorithm": algo,
+            "filter_executed_tflops_per_gpu": achieved * exec_ratio if achieved else None,
+            "filter_executed_frac_of_fp64_peak": achieved * exec_ratio / peak if achieved else None,
             "solve": {"iterations": res.iterations_used, "converged": res.converged,
                       "ledger_seconds": {k: round(v, 4) for k, v in res.ledger.seconds.items()},
                       "model_tflop": total_model / 1e12, "generator_s": round(gen_s, 2),

@@ -97,12 +97,14 @@ _lib = None
 _lock = threading.Lock()
 # complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
 _ALGOS = {"4m": 4, "3m": 6, "3m-onthefly": 3}
-_FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "4m").lower()]
+# default 3M (Gauss) with precomputed operand-sum planes: 25% fewer DMMA, parity-checked at C1
+# (tests/test_gpu_parity.py); BSE200_FILTER=4m restores the 4M split
+_FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "3m").lower()]
 
 
 def set_filter_algorithm(name: str) -> None:
-    """'4m' (default), '3m' (Gauss: 25% fewer FP64 tensor ops in the filter, with the operand sums of
-    A and B precomputed once, +32 m^2 bytes) or '3m-onthefly' (sums formed in registers)."""
+    """'3m' (default; Gauss: 25% fewer FP64 tensor ops in the filter, with the operand sums of A and B
+    precomputed once, +32 m^2 bytes), '3m-onthefly' (sums formed in registers) or '4m'."""
     global _FILTER_CM
     cm = _ALGOS[name.lower()] if isinstance(name, str) else int(name)
     _FILTER_CM = cm

@@ -287,7 +287,7 @@ def test_c1_parity(bse, c1_instance):
         assert np.abs(ov - 1).max() <= 1e-8
 
 
-@pytest.mark.parametrize("algo", ["3m", "3m-onthefly"])
+@pytest.mark.parametrize("algo", ["3m", "3m-onthefly", "4m"])
 def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
@@ -295,13 +295,14 @@ def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     g = golden("ops_m16_s5.npz")
     ham = bse.BseHamiltonian(a, b)
     cfg = bse.FilterConfig(int(g["deg"]), float(g["center"]), float(g["half_width"]), float(g["scale_ref"]))
+    default = bse.filter_algorithm()
     try:
         bse.set_filter_algorithm(algo)
         out3 = bse.chebyshev_filter(ham, g["x"], cfg)
         a1, b1, gc = c1_instance
         r = bse.solve(bse.BseHamiltonian(a1, b1), bse.SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0))
     finally:
-        bse.set_filter_algorithm("4m")
+        bse.set_filter_algorithm(default)
     assert _rel(out3, g["filtered"]) <= 1e-12
     assert r.converged and abs(r.iterations_used - int(gc["abs_iters"])) <= 1
     assert (np.abs(r.lambdas - gc["abs_lambdas"]) / np.abs(gc["abs_lambdas"])).max() <= 1e-10
