@@ -43,6 +43,9 @@ enum {
 
 typedef struct bse_ctx bse_ctx;
 
+/* Hamiltonian flags (bse_set_hamiltonian_flags) */
+#define BSE_HAM_B_ZERO 1u /* B == 0 (TDA / hermitian limit): the operator skips the B half (4 n^2 k flops) */
+
 /* ---- context ------------------------------------------------------------ */
 int bse_ctx_create(int device, bse_ctx** out);
 void bse_ctx_destroy(bse_ctx* ctx);
@@ -55,6 +58,9 @@ const char* bse_version(void);
  * complex block pair, default) or 3 (3M / Gauss, 6 DMMA: 25% fewer FP64 tensor ops; error bound
  * grows to ~eps (|Re|+|Im|)^2).  RR and residual products always use 4M.          */
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults);
+/* Properties of the Hamiltonian the following operator calls on this context act on
+ * (BSE_HAM_* flags); the Python layer sets them before every operator call.                     */
+int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags);
 /* (code 6 = 3M using the precomputed sum planes when the caller passes them)                   */
 
 /* ---- Hamiltonian operator ------------------------------------------------ */

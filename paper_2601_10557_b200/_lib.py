@@ -51,6 +51,7 @@ _SIGS = {
     "bse_ctx_destroy": (None, [_vp]),
     "bse_set_stream": (C.c_int, [_vp, _vp]),
     "bse_set_filter_algorithm": (C.c_int, [_vp, C.c_int]),
+    "bse_set_hamiltonian_flags": (C.c_int, [_vp, C.c_uint]),
     "bse_last_error": (C.c_char_p, [_vp]),
     "bse_launch_count": (_i64, [_vp]),
     "bse_apply_h": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _dbl]),
@@ -96,7 +97,7 @@ _STATUS = {
 _lib = None
 _lock = threading.Lock()
 # complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
-_ALGOS = {"4m": 4, "3m": 6, "3m-onthefly": 3}
+_ALGOS = {"4m": 4, "3m": 6, "3m-onthefly": 3, "3m-xsum": 7}
 # default 3M (Gauss) with precomputed operand-sum planes: 25% fewer DMMA, parity-checked at C1
 # (tests/test_gpu_parity.py); BSE200_FILTER=4m restores the 4M split
 _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "3m").lower()]
@@ -117,7 +118,7 @@ def filter_algorithm() -> str:
 
 
 def uses_sum_planes() -> bool:
-    return _FILTER_CM == 6 or 61 <= _FILTER_CM <= 63
+    return _FILTER_CM in (6, 7) or 61 <= _FILTER_CM <= 63
 
 
 def load() -> C.CDLL:
@@ -188,6 +189,11 @@ class Context:
     def call(self, name: str, *args) -> None:
         self.bind_stream()
         self.check(getattr(self.lib, name)(self.handle, *args))
+
+    def set_ham_flags(self, flags: int) -> None:
+        if flags != getattr(self, "_ham_flags", None):
+            self.check(self.lib.bse_set_hamiltonian_flags(self.handle, flags))
+            self._ham_flags = flags
 
     @property
     def launches(self) -> int:

@@ -42,6 +42,7 @@ struct bse_ctx {
   int filter_cm = 4;  // complex multiplication of the Chebyshev products: 4 (4M) or 3 (3M / Gauss)
   void* sws = nullptr;  // persistent cuSOLVER device workspace (grows, never shrinks)
   size_t sws_bytes = 0;
+  unsigned ham_flags = 0;  // BSE_HAM_B_ZERO: operator calls skip the B half of the contraction
   void* gv = nullptr;  // split-K GEMV partials
   size_t gv_bytes = 0;
 };
@@ -205,7 +206,9 @@ using HopMain = bse::HopCfg<64, 32, 8, 2, 2, 4, 2>;
 using Hop3M = bse::HopCfg<64, 32, 16, 2, 2, 4, 1>;
 
 template <class C, int EPI, int CM = 4>
-void launch_hop(bse_ctx* ctx, const bse::HopArgs& a) {
+void launch_hop(bse_ctx* ctx, const bse::HopArgs& a_in) {
+  bse::HopArgs a = a_in;
+  a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
   static bool configured = false;
   if (!configured) {
     CUDA_OK(cudaFuncSetAttribute(bse::hop_kernel<C, EPI, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -230,12 +233,16 @@ using Hop3MS = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1>;
 using Hop3MS_1 = bse::HopCfg<64, 32, 8, 2, 2, 4, 1, 1>;
 using Hop3MS_2 = bse::HopCfg<64, 32, 16, 2, 2, 3, 1, 1>;
 using Hop3MS_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
+// 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
+using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
 
 // Chebyshev-step products: 4M (default) or 3M as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
-  if ((code == 6 || (code >= 61 && code <= 63)) && (!a.sa || !a.sb)) code = 3;  // no sum planes: sums on the fly
+  if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
+  if ((code == 6 || code == 7 || (code >= 61 && code <= 63)) && (!a.sa || !a.sb)) code = 3;  // no P sum planes
   switch (code) {
+    case 7: launch_hop<Hop3MX, bse::HOP_AXPBY, 7>(ctx, a); break;
     case 6: launch_hop<Hop3MS, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 61: launch_hop<Hop3MS_1, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 62: launch_hop<Hop3MS_2, bse::HOP_AXPBY, 6>(ctx, a); break;
@@ -272,8 +279,8 @@ void launch_gemv(bse_ctx* ctx, const bse::HopArgs& a) {
     ctx->gv_bytes = need;
   }
   zval* part = static_cast<zval*>(ctx->gv);
-  bse::gemv_partial_kernel<<<dim3(rb, nsplit), bse::GV_THREADS, 0, ctx->stream>>>(a.pa, a.pb, a.lda, a.mr, a.kc, a.x1,
-                                                                                 a.x2, kchunk, part);
+  bse::gemv_partial_kernel<<<dim3(rb, nsplit), bse::GV_THREADS, 0, ctx->stream>>>(
+      a.pa, a.pb, a.lda, a.mr, a.kc, a.x1, a.x2, kchunk, part, (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0);
   check_launch(ctx);
   bse::gemv_reduce_kernel<<<(2 * a.mr + 255) / 256, 256, 0, ctx->stream>>>(part, nsplit, a.mr, a.y1, a.y2, a.alpha,
                                                                            a.low_sign);
@@ -317,11 +324,20 @@ void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval*
 }
 
 void filter_step(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const zval* y,
-                 const zval* yprev, zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
+                 const zval* yprev, zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta,
+                 const double* xs = nullptr, double* ys = nullptr, int64_t ldxs = 0) {
   bse::HopArgs a = hop_args_single(d_ab, lda, m, y, ld, k);
   if (d_sd) {
     a.sa = static_cast<const zval*>(d_sd);
     a.sb = a.sa + m * lda;
+  }
+  if (xs && ys) {  // X sums of y in, Re + Im of y_next out (code 7)
+    a.xs1 = xs;
+    a.xs2 = xs + m;
+    a.ldxs = ldxs;
+    a.ys1 = ys;
+    a.ys2 = ys + m;
+    a.ldys = ldxs;
   }
   a.y1 = ynext;
   a.y2 = ynext + m;
@@ -685,9 +701,13 @@ void bse_ctx_destroy(bse_ctx* ctx) {
   delete ctx;
 }
 
+int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
+  return guarded(ctx, [&] { ctx->ham_flags = flags; });
+}
+
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
-    const bool ok = complex_mults == 3 || complex_mults == 4 || complex_mults == 6 ||
+    const bool ok = complex_mults == 3 || complex_mults == 4 || complex_mults == 6 || complex_mults == 7 ||
                     (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
                     (complex_mults >= 61 && complex_mults <= 63);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
@@ -742,16 +762,26 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64
     if (k == 0 || m == 0) return;
     // chebyshev.py:58-74 with three rotating buffers {v, w0, w1}
     zval* bufs[3] = {static_cast<zval*>(d_v), static_cast<zval*>(d_work), static_cast<zval*>(d_work) + ld * k};
+    // code 7: the Re + Im planes of the three buffers (each step's epilogue writes the next one's)
+    const bool xsums = ctx->filter_cm == 7 && d_sd;
+    const int64_t n = 2 * m;
+    Scratch sc(ctx, xsums ? 3 * al((size_t)n * k * sizeof(double)) : 0);
+    double* sums[3] = {nullptr, nullptr, nullptr};
+    if (xsums) {
+      for (int i = 0; i < 3; ++i) sums[i] = sc.take<double>((size_t)n * k);
+      bse::re_plus_im_kernel<<<grid1d(n * k, 256, 148 * 16), 256, 0, ctx->stream>>>(bufs[0], ld, n, k, sums[0], n);
+      check_launch(ctx);
+    }
     const double sigma1 = e / (s - c);
     double sigma = sigma1;
     int prev = 0, cur = 1;
-    filter_step(ctx, d_ab, d_sd, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0);
+    filter_step(ctx, d_ab, d_sd, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0, sums[0], sums[1], n);
     for (int step = 2; step <= deg; ++step) {
       const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
       const int nxt = 3 - prev - cur;
       // y_next = (2 s'/e)(H y - c y) - (s s') y_prev ; written over the free buffer
       filter_step(ctx, d_ab, d_sd, lda, m, bufs[cur], bufs[prev], bufs[nxt], ld, k, c, 2.0 * sigma_new / e,
-                  sigma * sigma_new);
+                  sigma * sigma_new, sums[cur], sums[nxt], n);
       prev = cur;
       cur = nxt;
       sigma = sigma_new;

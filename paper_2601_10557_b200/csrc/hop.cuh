@@ -31,8 +31,14 @@ struct HopArgs {
   // 3M with precomputed operand sums (CM == 6): (Pr + Pi, Pr - Pi) planes of the same tiles
   const zval* sa;
   const zval* sb;
+  // 3M with precomputed X sums too (CM == 7): Re + Im planes of x1 / x2 (leading dim ldxs),
+  // produced by the previous step's epilogue (ys1 / ys2 below)
+  const double* xs1;
+  const double* xs2;
+  int64_t ldxs;
   int mr;  // output rows per half
   int kc;  // contraction length per part
+  int skip_b;  // B == 0 (TDA / hermitian limit): contract over the A part only (4 n^2 k flops)
   // X operand rows for the contraction: x1 (rows of the "upper" half), x2 ("lower")
   const zval* x1;
   const zval* x2;
@@ -53,14 +59,19 @@ struct HopArgs {
   // input block shares with its output block in the 2D layout); per-column shifts when set
   int shift_lo, shift_hi;
   const double* shift_col;
+  // optional Re + Im plane of the output (written by the AXPBY epilogue when non-null)
+  double* ys1;
+  double* ys2;
+  int64_t ldys;
   // residual mode
   const double* lam;  // per column
   double* partial;    // [gridDim.y][k]
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_, int PS_ = 0>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_, int PS_ = 0, int XS_ = 0>
 struct HopCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_, PS = PS_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_, PS = PS_,
+                       XS = XS_;
   static constexpr int WARPS_M = BM / (8 * WM);
   static constexpr int WARPS_N = BN / (8 * WN);
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
@@ -69,7 +80,9 @@ struct HopCfg {
   static constexpr int P_ELEMS = BK * LDP;
   static constexpr int SD_ELEMS = PS ? BK * LDP : 0;  // (Pr+Pi, Pr-Pi) tile, same layout as P
   static constexpr int X_ELEMS = BN * LDX;
-  static constexpr int STAGE_ELEMS = P_ELEMS + SD_ELEMS + 2 * X_ELEMS;
+  static constexpr int LDXS = BK + 4;  // doubles; == 12 (mod 16) for BK = 8: conflict-free LDS.64
+  static constexpr int XS_ELEMS = XS ? BN * LDXS : 0;  // in zval units: two planes of BN x LDXS doubles
+  static constexpr int STAGE_ELEMS = P_ELEMS + SD_ELEMS + 2 * X_ELEMS + XS_ELEMS;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(zval);
   static_assert(BM % 8 == 0 && BK % 8 == 0 && BN % 8 == 0, "tile dims");
 };
@@ -110,6 +123,11 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
     const zval* X = which ? XB : XA;
     const zval* src = ok ? X + (int64_t)gc * a.ldx + gj : X;
     cp_async16((which ? Xbs : Xas) + cc * C::LDX + kk, src, ok);
+    if constexpr (C::XS) {
+      const double* XSg = part ? (which ? a.xs1 : a.xs2) : (which ? a.xs2 : a.xs1);
+      double* XSs = reinterpret_cast<double*>(Xbs + C::X_ELEMS) + which * C::BN * C::LDXS;
+      cp_async8(XSs + cc * C::LDXS + kk, ok ? XSg + (int64_t)gc * a.ldxs + gj : XSg, ok);
+    }
   }
 }
 
@@ -119,13 +137,13 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
 //      Ur = T1 - T2, Ui = T3 - T1 - T2, L'r = S1 + S2, L'i = S3 - S1 + S2.
 template <int CM>
 struct Acc {
-  static constexpr int N = (CM == 3 || CM == 5 || CM == 6) ? 6 : 4;
+  static constexpr int N = (CM == 3 || CM == 5 || CM == 6 || CM == 7) ? 6 : 4;
 };
 
 template <int CM, int WM, int WN>
 __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][WN][2], int i, int j, int h, double& ur,
                                            double& ui, double& lr, double& li) {
-  if constexpr (CM == 3 || CM == 5 || CM == 6) {
+  if constexpr (CM == 3 || CM == 5 || CM == 6 || CM == 7) {
     const double t1 = acc[0][i][j][h], t2 = acc[1][i][j][h], t3 = acc[2][i][j][h];
     const double s1 = acc[3][i][j][h], s2 = acc[4][i][j][h], s3 = acc[5][i][j][h];
     ur = t1 - t2;
@@ -152,7 +170,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
   const int i0 = blockIdx.y * C::BM;
 
   const int nkt_part = (a.kc + C::BK - 1) / C::BK;
-  const int nkt = 2 * nkt_part;
+  const int nkt = a.skip_b ? nkt_part : 2 * nkt_part;
 
   double acc[Acc<CM>::N][C::WM][C::WN][2];
 #pragma unroll
@@ -192,17 +210,24 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
         xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
       }
-      if constexpr (CM == 6) {
-        // 3M with the P-side sums read from shared memory: only the X-side sums remain on the
-        // DMMA critical path
+      if constexpr (CM == 6 || CM == 7) {
+        // 3M with the P-side sums read from shared memory; with CM == 7 the X-side sums too, so
+        // no add sits on the DMMA critical path
         zval sd[C::WM];
 #pragma unroll
         for (int i = 0; i < C::WM; ++i) sd[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
         double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {
-          xas[j] = xa[j].re + xa[j].im;
-          xbs[j] = xb[j].re + xb[j].im;
+          if constexpr (CM == 7) {
+            const double* XSa = reinterpret_cast<const double*>(Xbs + C::X_ELEMS);
+            const int col = wn * (8 * C::WN) + j * 8 + g;
+            xas[j] = XSa[col * C::LDXS + ks * 4 + t];
+            xbs[j] = XSa[C::BN * C::LDXS + col * C::LDXS + ks * 4 + t];
+          } else {
+            xas[j] = xa[j].re + xa[j].im;
+            xbs[j] = xb[j].re + xb[j].im;
+          }
         }
 #pragma unroll
         for (int i = 0; i < C::WM; ++i) {
@@ -298,6 +323,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
           o2.im *= a.low_sign;
           a.y1[(int64_t)col * a.ldy + row] = o1;
           a.y2[(int64_t)col * a.ldy + row] = o2;
+          if (a.ys1) {
+            a.ys1[(int64_t)col * a.ldys + row] = o1.re + o1.im;
+            a.ys2[(int64_t)col * a.ldys + row] = o2.re + o2.im;
+          }
         }
       }
     }
@@ -362,14 +391,15 @@ constexpr int GV_THREADS = 256;
 __global__ void __launch_bounds__(GV_THREADS) gemv_partial_kernel(const zval* __restrict__ pa, const zval* __restrict__ pb,
                                                                   int64_t lda, int mr, int kc, const zval* __restrict__ x1,
                                                                   const zval* __restrict__ x2, int kchunk,
-                                                                  zval* __restrict__ part) {
+                                                                  zval* __restrict__ part, int skip_b) {
   const int i = blockIdx.x * GV_THREADS + threadIdx.x;
   const int j0 = blockIdx.y * kchunk, j1 = min(kc, j0 + kchunk);
   if (i >= mr) return;
   double ur = 0.0, ui = 0.0, lr = 0.0, li = 0.0;
 #pragma unroll 4
   for (int j = j0; j < j1; ++j) {
-    const zval a = pa[(int64_t)j * lda + i], b = pb[(int64_t)j * lda + i];
+    const zval a = pa[(int64_t)j * lda + i];
+    const zval b = skip_b ? zval{0.0, 0.0} : pb[(int64_t)j * lda + i];
     const zval p = x1[j], q = x2[j];
     ur += a.re * p.re - a.im * p.im + b.re * q.re - b.im * q.im;  // U  += a p + b q
     ui += a.re * p.im + a.im * p.re + b.re * q.im + b.im * q.re;

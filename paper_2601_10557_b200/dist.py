@@ -678,11 +678,14 @@ class DistributedSolver:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = device
         self.ops = ops or CudaOps(device)
+        self.flags = 0
         if isinstance(source, dict):
             if m is None:
                 raise ValidationError("m is required with pre-sliced tiles")
+            self.flags = int(source.get("flags", 0))
         elif hasattr(source, "device_blocks"):
             m = source.m
+            self.flags = source.flags
             if source.a is not None:
                 source = (source.a, source.b)
             else:
@@ -690,6 +693,8 @@ class DistributedSolver:
                 source = (ab[:, :m], ab[:, m:])
         else:
             m = source[0].shape[0]
+            b = source[1]
+            self.flags = 0 if (bool(b.any()) if hasattr(b, "any") else True) else 1
         self.grid = grid or Grid(m, world, rank)
         self.comm = Comm(self.grid)
         self.load(source)
@@ -708,9 +713,12 @@ class DistributedSolver:
         for name, t in (("fwd", self.fwd), ("trn", self.trn)):
             mat = t.buf.cpu().numpy().T  # (mr, 2kc) F-order view
             out[name] = (np.asfortranarray(mat[:, :t.kc]), np.asfortranarray(mat[:, t.kc:]))
+        out["flags"] = self.flags
         return out
 
     def solve(self, cfg: SolverConfig) -> SolveResult:
+        if hasattr(self.ops, "ctx"):
+            self.ops.ctx.set_ham_flags(self.flags)
         res = self.inner.solve(cfg)
         res.v = res.v.T  # (n, nev) column-major view
         return res
@@ -719,7 +727,7 @@ class DistributedSolver:
 def make_tiles_from_pieces(ops, pieces: dict):
     torch = ops.torch
     tiles = []
-    for name in ("fwd", "trn"):
+    for name in ("fwd", "trn"):  # "flags" entry (if any) is read by DistributedSolver
         a_t, b_t = pieces[name]
         mr, kc = a_t.shape
         buf = torch.empty((2 * kc, mr), dtype=torch.complex128, device=ops.device)

@@ -156,7 +156,27 @@ class BseHamiltonian:
                     ab[:, :m].copy_(torch.from_numpy(np.asfortranarray(self.a)))
                     ab[:, m:].copy_(torch.from_numpy(np.asfortranarray(self.b)))
             self._dev[device] = ab
+        # every operator call fetches the blocks right before its C call: bind this Hamiltonian's flags
+        _lib.Context.get(device.index).set_ham_flags(self.flags)
         return ab
+
+    @property
+    def b_is_zero(self) -> bool:
+        """B == 0 exactly (TDA / hermitian limit): the operator then skips the B half."""
+        z = self.__dict__.get("_bzero")
+        if z is None:
+            if self.b is not None:
+                b = self.b  # cheap early exits before the full scan (typical B is dense)
+                z = not (b.size and (b[0, 0] != 0 or b[-1, -1] != 0 or np.any(b[:, 0]) or np.any(b)))
+            else:
+                ab = next(iter(self._dev.values()))
+                z = not bool((ab[:, self.m:] != 0).any().item())
+            self._bzero = z
+        return z
+
+    @property
+    def flags(self) -> int:
+        return 1 if self.b_is_zero else 0  # BSE_HAM_B_ZERO
 
     def device_sum_planes(self, device):
         """(re+im, re-im) planes of [A | B] for the 3M filter (bse_make_sum_planes), built once per device."""

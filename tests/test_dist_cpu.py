@@ -43,7 +43,7 @@ def _worker(rank, world, port, key, pq, out):
 
 
 @pytest.mark.parametrize("world,pq,key", [(1, None, "m48_s12"), (2, None, "m48_s12"), (4, None, "m64_s21"),
-                                          (2, (2, 1), "m24_s100"), (4, (1, 4), "m32_s14")])
+                                          (2, (2, 1), "m24_s100"), (4, (1, 4), "m32_s14"), (8, None, "m64_s40")])
 def test_distributed_solve_matches_reference(tmp_path, world, pq, key):
     out = str(tmp_path / "r.npz")
     mp.spawn(_worker, args=(world, _port(), key, pq, out), nprocs=world, join=True)

@@ -50,6 +50,27 @@ def variants(m, ks, codes):
     ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 4))
 
 
+def whole_filter(m, ks, codes, deg=4):
+    """bse_chebyshev_filter (deg steps) per filter code — codes 6/7 get the sum planes."""
+    n = 2 * m
+    ab = colmajor_empty(m, 2 * m, dev)
+    ab.real.normal_()
+    ab.imag.normal_()
+    sd = colmajor_empty(m, 2 * m, dev)
+    ctx.call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), m, 2 * m, _lib.dptr(sd))
+    for k in ks:
+        v = colmajor_empty(n, k, dev); v.real.normal_(); v.imag.normal_()
+        work = torch.empty(2 * n * k, dtype=torch.complex128, device=dev)
+        for code in codes:
+            ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
+            sdp = _lib.dptr(sd) if code in (6, 7) else None
+            ms = timed(lambda: ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sdp, ld_of(ab), m, _lib.dptr(v), n, k,
+                                        deg, 0.0, 1.0, -1.5, _lib.dptr(work)), 2)
+            print(f"filter deg={deg} m={m} k={k} code={code}: {ms / deg:8.2f} ms/step  model "
+                  f"{8.0 * n * n * k * deg / ms / 1e9:6.2f} TF/s", flush=True)
+    ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 6))
+
+
 def solver_small():
     for k in (100, 200, 400, 600, 800, 1000, 1200):
         g = torch.randn((k, k), dtype=torch.complex128, device=dev)
