@@ -139,6 +139,19 @@ def main() -> None:
         })
     np.savez(OUT / "c1_m500_s0.npz", **c1)
     meta["cases"] = solves
+
+    # ---- file formats (FORMATS.md): reference writer outputs on small data -------------------
+    ham8 = small["m8_s11"]
+    fileio.write_pchb(OUT / "m8_s11.pchb", ham8)
+    fileio.write_matrix_market(OUT / "m8_s11_A.mtx", ham8.a, comment=" resonant block, seed=11")
+    r = bs.solve(small["m32_s4"], bs.SolverConfig(nev=4, seed=9))
+    fileio.write_eigenvalues_csv(OUT / "m32_s4_eigenvalues.csv", r.lambdas, r.residual_norms, "0123456789abcdef",
+                                 converged=r.converged)
+    fileio.write_trace_csv(OUT / "m32_s4_trace.csv", r, "0123456789abcdef")
+    fileio.write_pchv(OUT / "m32_s4_v.pchv", r.v)
+    np.savez(OUT / "m32_s4_result.npz", lambdas=r.lambdas, res=r.residual_norms, mu_1=r.bounds.mu_1,
+             mu_n=r.bounds.mu_n, converged=r.converged, **_trace_arrays(r.trace))
+    meta["m8_s11_pchb_digest"] = fileio.digest64(OUT / "m8_s11.pchb")
     (OUT / "meta.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print("golden fixtures written to", OUT)
 

@@ -52,5 +52,6 @@ from .solver import (
 )
 from .generate import GeneratorSpec, generate
 from ._lib import filter_algorithm, set_filter_algorithm
+from . import fileio
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -330,3 +330,24 @@ def test_fused_residuals_match_explicit(bse, c1_instance):
     gc = c1_instance[2]
     assert r.converged and abs(r.iterations_used - int(gc["rel_iters"])) <= 1
     assert (np.abs(r.lambdas - gc["rel_lambdas"]) / np.abs(gc["rel_lambdas"])).max() <= 1e-10
+
+
+def test_pchb_device_reader_and_cli_solve(bse, tmp_path):
+    from paper_2601_10557_b200 import fileio
+    from paper_2601_10557_b200.cli import main
+
+    hd = fileio.read_pchb(GOLDEN / "m8_s11.pchb", device=torch.device("cuda", 0))
+    a, b = golden_ham(8, 11)
+    ga, gb = hd.host_blocks()
+    np.testing.assert_array_equal(ga, a)
+    np.testing.assert_array_equal(gb, b)
+    rc = main(["solve", "--pchb", str(GOLDEN / "m8_s11.pchb"), "--nev", "2", "--tol", "1e-10", "--out", str(tmp_path)])
+    assert rc == 0
+    lines = (tmp_path / "eigenvalues.csv").read_text().splitlines()
+    assert lines[0] == "# bsesolve eigenvalues v1" and lines[4] == "index,eigenvalue,residual" and len(lines) == 7
+    lam = np.array([float(l.split(",")[1]) for l in lines[5:]])
+    ref = o.dense_eigs(a, b)[:2]
+    assert np.abs(lam - ref).max() <= 1e-10 * np.abs(ref).max()
+    v = fileio.read_pchv(tmp_path / "eigenvectors.bin")
+    assert v.shape == (16, 2)
+    assert (tmp_path / "trace.csv").exists() and (tmp_path / "manifest.json").exists()
