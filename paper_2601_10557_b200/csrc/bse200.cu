@@ -235,13 +235,27 @@ using Hop3MS_2 = bse::HopCfg<64, 32, 16, 2, 2, 3, 1, 1>;
 using Hop3MS_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
 // 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
 using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
+// 3M with P sums from planes and X sums computed in shared memory one stage ahead (code 8, 81)
+using Hop3MA = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 2>;
+using Hop3MA_1 = bse::HopCfg<64, 16, 8, 2, 1, 5, 2, 1, 2>;
+// 3M with P and X sums both computed in shared memory one stage ahead (code 9, 91, 92): no sum
+// planes in HBM, no add on the DMMA path
+using Hop3MB = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 2, 2>;
+using Hop3MB_1 = bse::HopCfg<64, 32, 8, 2, 2, 4, 1, 2, 2>;
+using Hop3MB_2 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 2, 2>;
 
 // Chebyshev-step products: 4M (default) or 3M as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
   if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
-  if ((code == 6 || code == 7 || (code >= 61 && code <= 63)) && (!a.sa || !a.sb)) code = 3;  // no P sum planes
+  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 63)) && (!a.sa || !a.sb))
+    code = 3;  // no P sum planes
   switch (code) {
+    case 9: launch_hop<Hop3MB, bse::HOP_AXPBY, 9>(ctx, a); break;
+    case 91: launch_hop<Hop3MB_1, bse::HOP_AXPBY, 9>(ctx, a); break;
+    case 92: launch_hop<Hop3MB_2, bse::HOP_AXPBY, 9>(ctx, a); break;
+    case 8: launch_hop<Hop3MA, bse::HOP_AXPBY, 8>(ctx, a); break;
+    case 81: launch_hop<Hop3MA_1, bse::HOP_AXPBY, 8>(ctx, a); break;
     case 7: launch_hop<Hop3MX, bse::HOP_AXPBY, 7>(ctx, a); break;
     case 6: launch_hop<Hop3MS, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 61: launch_hop<Hop3MS_1, bse::HOP_AXPBY, 6>(ctx, a); break;
@@ -708,6 +722,8 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     const bool ok = complex_mults == 3 || complex_mults == 4 || complex_mults == 6 || complex_mults == 7 ||
+                    complex_mults == 8 || complex_mults == 81 || complex_mults == 9 || complex_mults == 91 ||
+                    complex_mults == 92 ||
                     (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
                     (complex_mults >= 61 && complex_mults <= 63);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");

@@ -82,6 +82,8 @@ struct HopCfg {
   static constexpr int X_ELEMS = BN * LDX;
   static constexpr int LDXS = BK + 4;  // doubles; == 12 (mod 16) for BK = 8: conflict-free LDS.64
   static constexpr int XS_ELEMS = XS ? BN * LDXS : 0;  // in zval units: two planes of BN x LDXS doubles
+  // XS == 1: X sums loaded from global planes (code 7); XS == 2: computed in shared memory one
+  // stage ahead of the MMAs (code 8)
   static constexpr int STAGE_ELEMS = P_ELEMS + SD_ELEMS + 2 * X_ELEMS + XS_ELEMS;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(zval);
   static_assert(BM % 8 == 0 && BK % 8 == 0 && BN % 8 == 0, "tile dims");
@@ -109,7 +111,7 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
     const bool ok = (gi < a.mr) && (gj < a.kc);
     const zval* src = ok ? P + (int64_t)gj * a.lda + gi : P;
     cp_async16(Ps + jj * C::LDP + ii, src, ok);
-    if constexpr (C::PS) cp_async16(SDs + jj * C::LDP + ii, ok ? SD + (int64_t)gj * a.lda + gi : SD, ok);
+    if constexpr (C::PS == 1) cp_async16(SDs + jj * C::LDP + ii, ok ? SD + (int64_t)gj * a.lda + gi : SD, ok);
   }
 #pragma unroll
   for (int r = 0; r < (2 * C::BN * C::BK + C::THREADS - 1) / C::THREADS; ++r) {
@@ -123,7 +125,7 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
     const zval* X = which ? XB : XA;
     const zval* src = ok ? X + (int64_t)gc * a.ldx + gj : X;
     cp_async16((which ? Xbs : Xas) + cc * C::LDX + kk, src, ok);
-    if constexpr (C::XS) {
+    if constexpr (C::XS == 1) {
       const double* XSg = part ? (which ? a.xs1 : a.xs2) : (which ? a.xs2 : a.xs1);
       double* XSs = reinterpret_cast<double*>(Xbs + C::X_ELEMS) + which * C::BN * C::LDXS;
       cp_async8(XSs + cc * C::LDXS + kk, ok ? XSg + (int64_t)gc * a.ldxs + gj : XSg, ok);
@@ -137,13 +139,13 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
 //      Ur = T1 - T2, Ui = T3 - T1 - T2, L'r = S1 + S2, L'i = S3 - S1 + S2.
 template <int CM>
 struct Acc {
-  static constexpr int N = (CM == 3 || CM == 5 || CM == 6 || CM == 7) ? 6 : 4;
+  static constexpr int N = (CM == 3 || CM == 5 || CM == 6 || CM == 7 || CM == 8 || CM == 9) ? 6 : 4;
 };
 
 template <int CM, int WM, int WN>
 __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][WN][2], int i, int j, int h, double& ur,
                                            double& ui, double& lr, double& li) {
-  if constexpr (CM == 3 || CM == 5 || CM == 6 || CM == 7) {
+  if constexpr (CM == 3 || CM == 5 || CM == 6 || CM == 7 || CM == 8 || CM == 9) {
     const double t1 = acc[0][i][j][h], t2 = acc[1][i][j][h], t3 = acc[2][i][j][h];
     const double s1 = acc[3][i][j][h], s2 = acc[4][i][j][h], s3 = acc[5][i][j][h];
     ur = t1 - t2;
@@ -155,6 +157,28 @@ __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][W
     ui = acc[1][i][j][h];
     lr = acc[2][i][j][h];
     li = acc[3][i][j][h];
+  }
+}
+
+// CM == 8 / 9: 3M operand sums of one landed stage, written into its XS planes (X side) and, with
+// PS == 2, its SD tile (P side: (re + im, re - im)); computed one stage ahead of the MMAs
+template <class C>
+__device__ __forceinline__ void hop_stage_xsums(zval* st) {
+  if constexpr (C::PS == 2) {
+    const zval* Ps = st;
+    zval* SDs = st + C::P_ELEMS;
+    for (int id = threadIdx.x; id < C::BK * C::BM; id += C::THREADS) {
+      const int ii = id % C::BM, jj = id / C::BM;
+      const zval v = Ps[jj * C::LDP + ii];
+      SDs[jj * C::LDP + ii] = zval{v.re + v.im, v.re - v.im};
+    }
+  }
+  zval* Xas = st + C::P_ELEMS + C::SD_ELEMS;
+  double* XS = reinterpret_cast<double*>(Xas + 2 * C::X_ELEMS);
+  for (int id = threadIdx.x; id < 2 * C::BN * C::BK; id += C::THREADS) {
+    const int kk = id % C::BK, cc = (id / C::BK) % C::BN, which = id / (C::BK * C::BN);
+    const zval v = Xas[which * C::X_ELEMS + cc * C::LDX + kk];
+    XS[which * C::BN * C::LDXS + cc * C::LDXS + kk] = v.re + v.im;
   }
 }
 
@@ -186,14 +210,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
     if (s < nkt) hop_load_stage<C>(smem + s * C::STAGE_ELEMS, a, s, nkt_part, i0, c0);
     cp_async_commit();
   }
+  if constexpr (CM == 8 || CM == 9) {  // sums of stage 0 before the loop
+    cp_async_wait<C::STAGES - 2>();
+    __syncthreads();
+    hop_stage_xsums<C>(smem);
+  }
 
   for (int kt = 0; kt < nkt; ++kt) {
-    cp_async_wait<C::STAGES - 2>();
+    if constexpr (CM == 8 || CM == 9)
+      cp_async_wait<C::STAGES - 3>();  // stages kt and kt + 1 landed
+    else
+      cp_async_wait<C::STAGES - 2>();
     __syncthreads();
     {
       const int nxt = kt + C::STAGES - 1;
       if (nxt < nkt) hop_load_stage<C>(smem + (nxt % C::STAGES) * C::STAGE_ELEMS, a, nxt, nkt_part, i0, c0);
       cp_async_commit();
+    }
+    if constexpr (CM == 8 || CM == 9) {  // sums for the next stage, consumed after the next barrier
+      if (kt + 1 < nkt) hop_stage_xsums<C>(smem + ((kt + 1) % C::STAGES) * C::STAGE_ELEMS);
     }
     const zval* Ps = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
     const zval* SDs = Ps + C::P_ELEMS;
@@ -210,7 +245,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
         xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
       }
-      if constexpr (CM == 6 || CM == 7) {
+      if constexpr (CM == 6 || CM == 7 || CM == 8 || CM == 9) {
         // 3M with the P-side sums read from shared memory; with CM == 7 the X-side sums too, so
         // no add sits on the DMMA critical path
         zval sd[C::WM];
@@ -219,7 +254,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {
-          if constexpr (CM == 7) {
+          if constexpr (CM == 7 || CM == 8 || CM == 9) {
             const double* XSa = reinterpret_cast<const double*>(Xbs + C::X_ELEMS);
             const int col = wn * (8 * C::WN) + j * 8 + g;
             xas[j] = XSa[col * C::LDXS + ks * 4 + t];

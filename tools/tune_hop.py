@@ -40,7 +40,7 @@ def variants(m, ks, codes):
         yn = colmajor_empty(n, k, dev)
         for code in codes:
             ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
-            sdp = _lib.dptr(sd) if code == 6 or 61 <= code <= 63 else None
+            sdp = _lib.dptr(sd) if code in (6, 7, 8, 81) or 61 <= code <= 63 else None
             ms = timed(lambda: ctx.call("bse_filter_step", _lib.dptr(ab), sdp, ld_of(ab), m, _lib.dptr(y), _lib.dptr(yp),
                                         _lib.dptr(yn), n, k, 0.1, 1e-3, 0.5), 3 if m >= 20000 else 5)
             tf = 8.0 * n * n * k / ms / 1e9
@@ -63,7 +63,7 @@ def whole_filter(m, ks, codes, deg=4):
         work = torch.empty(2 * n * k, dtype=torch.complex128, device=dev)
         for code in codes:
             ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
-            sdp = _lib.dptr(sd) if code in (6, 7) else None
+            sdp = _lib.dptr(sd) if code in (6, 7, 8, 81) else None
             ms = timed(lambda: ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sdp, ld_of(ab), m, _lib.dptr(v), n, k,
                                         deg, 0.0, 1.0, -1.5, _lib.dptr(work)), 2)
             print(f"filter deg={deg} m={m} k={k} code={code}: {ms / deg:8.2f} ms/step  model "
