@@ -311,7 +311,7 @@ def run_ours(args, world, rank, local):
         h2d = 2 * m * m * 16 + n * cfg.nevex * 16 + 8 * n * 16
     else:
         pieces = ds.tile_pieces_host()
-        h2d = world * sum(x.nbytes for pair in pieces.values() for x in pair) + world * (n // world) * cfg.nevex * 16
+        h2d = world * sum(x.nbytes for name in ("fwd", "trn") for x in pieces[name]) + world * (n // world) * cfg.nevex * 16
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -315,6 +315,8 @@ def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
 class DistSolver:
     """SPMD solve on one rank of the grid; every rank calls it with the same config."""
 
+    CHUNK_MIN = 256  # filter column chunking (comm/compute overlap) from this block width on
+
     def __init__(self, grid: Grid, comm: Comm, ops, fwd: Tile, trn: Tile):
         self.g, self.c, self.ops, self.fwd, self.trn = grid, comm, ops, fwd, trn
         self.torch = ops.torch
@@ -377,28 +379,70 @@ class DistSolver:
         self.c.sum_col(y_col)
 
     def chebyshev(self, v_col, cfg: FilterConfig, row_buf):
-        """p(H) v in place (col layout); row_buf: (k, 2 nr) scratch.  chebyshev.py:58-74."""
+        """p(H) v in place (col layout); row_buf: (k, 2 nr) scratch.  chebyshev.py:58-74.
+
+        H acts on each column independently, so the block is split into column chunks that run
+        through the recurrence as independent pipelines: while one chunk's partial product is
+        being allreduced (NCCL on a communication stream), the next chunk's tile GEMM runs."""
         c, e = cfg.center, cfg.half_width
         s1 = e / (cfg.scale_ref - c)
-        s = s1
         k = v_col.shape[0]
-        yr = row_buf[:k]
-        # step 1: col -> row, Y1 = (s1/e)(H Y0 - c Y0)
-        self.forward(v_col, yr, alpha=s1 / e, shift=c, filter=True)
-        src, dst = yr, v_col
-        for step in range(2, cfg.degree + 1):
-            sn = 1.0 / (2.0 / s1 - s)
-            # Y_{j+1} = (2 sn / e)(H Y_j - c Y_j) - (s sn) Y_{j-1}; Y_{j-1} lives in dst (in place)
-            owner = self._beta_owner(step)
-            kw = dict(alpha=2.0 * sn / e, shift=c, beta=(s * sn) if owner else 0.0, p=dst if owner else None,
-                      filter=True)
-            if step % 2 == 0:
-                self.transposed(src, dst, **kw)
-            else:
-                self.forward(src, dst, **kw)
-            src, dst = dst, src
-            s = sn
+        nch = 1 if (self.g.world == 1 or k < self.CHUNK_MIN) else 2
+        edges = split(k, nch)
+        torch = self.torch
+        overlap = nch > 1 and hasattr(self.ops, "ctx")  # streams only with the CUDA ops
+        comp = torch.cuda.current_stream() if overlap else None
+        if overlap and not hasattr(self, "_comm_stream"):
+            self._comm_stream = torch.cuda.Stream(device=v_col.device)
+        reduced = [None] * nch
+        for ci in range(nch):
+            a, b = edges[ci], edges[ci + 1]
+            src, dst = v_col[a:b], row_buf[a:b]
+            s = s1
+            for step in range(1, cfg.degree + 1):
+                if step == 1:
+                    kw = dict(alpha=s1 / e, shift=c)
+                else:
+                    sn = 1.0 / (2.0 / s1 - s)
+                    owner = self._beta_owner(step)
+                    # Y_{j+1} = (2 sn / e)(H Y_j - c Y_j) - (s sn) Y_{j-1}; Y_{j-1} lives in dst (in place)
+                    kw = dict(alpha=2.0 * sn / e, shift=c, beta=(s * sn) if owner else 0.0,
+                              p=dst if owner else None)
+                    s = sn
+                fwd = step % 2 == 1
+                if overlap:
+                    reduced[ci] = self._step_async(src, dst, fwd, kw, comp, reduced[ci])
+                else:
+                    (self.forward if fwd else self.transposed)(src, dst, filter=True, **kw)
+                src, dst = dst, src
+        if overlap:
+            for ev in reduced:
+                comp.wait_event(ev)
         return v_col  # even degree: the result is back in the col buffer
+
+    def _step_async(self, src, dst, fwd, kw, comp, prev_event):
+        """One chunk step: tile GEMM on the compute stream (after the chunk's previous reduction),
+        allreduce on the communication stream; returns the event marking the reduced chunk."""
+        torch = self.torch
+        g = self.g
+        if prev_event is not None:
+            comp.wait_event(prev_event)
+        lo, hi = g.diag
+        if fwd:
+            self.ops.hop(self.fwd, src, dst, shift_rows=(lo - g.r0, hi - g.r0), s_off=g.r0 - g.c0, filter=True, **kw)
+        else:
+            self.ops.hop(self.trn, src, dst, shift_rows=(lo - g.c0, hi - g.c0), s_off=g.c0 - g.r0, filter=True, **kw)
+        done = torch.cuda.Event()
+        done.record(comp)
+        cs = self._comm_stream
+        with torch.cuda.stream(cs):
+            cs.wait_event(done)
+            (self.comm.sum_row if fwd else self.comm.sum_col)(dst)
+            red = torch.cuda.Event()
+            red.record(cs)
+        # keep dst alive for the communication stream's use
+        dst.record_stream(cs)
+        return red
 
     def _beta_owner(self, step: int) -> bool:
         # the -beta Y_prev term is added once per reduction group
@@ -656,11 +700,9 @@ def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):
     (solver.py:139-141), drawn bit-exactly on the host for just this rank's rows."""
     torch = ops.torch
     m = grid.m
-    out = np.empty((cols, 2 * grid.nc), dtype=np.complex128)
-    for j in range(cols):
-        out[j, :grid.nc] = rng.complex_normals(seed, grid.nc, start_index=j * n + grid.c0, threads=1)
-        out[j, grid.nc:] = rng.complex_normals(seed, grid.nc, start_index=j * n + m + grid.c0, threads=1)
-    return torch.from_numpy(out).to(ops.device)
+    rows = np.concatenate([np.arange(grid.c0, grid.c1), m + np.arange(grid.c0, grid.c1)])
+    index = np.arange(cols, dtype=np.int64)[:, None] * n + rows[None, :]  # column-major fill (rng.py:78-81)
+    return torch.from_numpy(rng.complex_normals_at(seed, index)).to(ops.device)
 
 
 class DistributedSolver:

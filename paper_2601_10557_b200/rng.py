@@ -75,5 +75,42 @@ def complex_normals(seed: int, count: int, start_index: int = 0, threads: int | 
     return out
 
 
+def _normals_at(seed: int, index: np.ndarray) -> np.ndarray:
+    """Normals with arbitrary (int64) indices: the same counter arithmetic element by element."""
+    ctr = np.empty(2 * index.size, dtype=_U64)
+    ctr[0::2] = 2 * index.astype(_U64) + _U64(1)  # word counter c -> state seed + (c + 1) * step
+    ctr[1::2] = 2 * index.astype(_U64) + _U64(2)
+    with np.errstate(over="ignore"):
+        z = _U64(seed & _WRAP) + ctr * _U64(_STEP)
+        for shift, mul in ((30, _M1), (27, _M2)):
+            z ^= z >> _U64(shift)
+            z *= _U64(mul)
+        z ^= z >> _U64(31)
+    u = (((z >> _U64(11)).astype(np.float64) + 1.0) * 2.0**-53).reshape(index.size, 2)
+    radius = np.sqrt(-2.0 * np.log(u[:, 0]))
+    angle = 2.0 * np.pi * u[:, 1]
+    return radius * np.cos(angle) + 1j * (radius * np.sin(angle))
+
+
+def complex_normals_at(seed: int, index, threads: int | None = None) -> np.ndarray:
+    """Normals #index (any shape), bit-identical to complex_normals at those positions; threaded."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    idx = np.ascontiguousarray(index, dtype=np.int64)
+    flat = idx.reshape(-1)
+    out = np.empty(flat.size, dtype=np.complex128)
+    nt = max(1, min(threads or min(32, os.cpu_count() or 1), flat.size // 65536 + 1))
+    edges = np.linspace(0, flat.size, nt + 1).astype(np.int64)
+
+    def work(i):
+        a, b = int(edges[i]), int(edges[i + 1])
+        out[a:b] = _normals_at(seed, flat[a:b])
+
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(work, range(nt)))
+    return out.reshape(idx.shape)
+
+
 def complex_normal_matrix(seed: int, rows: int, cols: int) -> np.ndarray:
     return complex_normals(seed, rows * cols).reshape((cols, rows)).T

@@ -35,6 +35,9 @@ def _worker(rank, world, port, key, pq, out):
     m, seed = (int(t[1:]) for t in key.split("_"))
     a, b = golden_ham(m, seed)
     grid = Grid(m, world, rank, *pq) if pq else None
+    from paper_2601_10557_b200.dist import DistSolver
+
+    DistSolver.CHUNK_MIN = 4  # exercise the column-chunked filter pipeline on the small cases
     res = solve_distributed((a, b), SolverConfig(**kw), device=torch.device("cpu"), grid=grid, ops=TorchOps())
     if rank == 0:
         np.savez(out, lambdas=res.lambdas, v=res.v.numpy(), res=res.residual_norms, iters=res.iterations_used,

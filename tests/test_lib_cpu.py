@@ -117,3 +117,13 @@ def test_threaded_rng_is_bit_identical():
     ref = rng._normals_serial(99, count, 7)
     for threads in (1, 3, 8):
         np.testing.assert_array_equal(rng.complex_normals(99, count, start_index=7, threads=threads), ref)
+
+
+def test_indexed_rng_matches_stream():
+    from paper_2601_10557_b200 import rng
+
+    full = rng.complex_normal_matrix(rng.substream(0, 3), 40, 7)
+    rows = np.r_[3:9, 23:29]
+    idx = np.arange(7)[:, None] * 40 + rows[None, :]
+    got = rng.complex_normals_at(rng.substream(0, 3), idx, threads=3)
+    np.testing.assert_array_equal(got, full[rows].T)
