@@ -315,7 +315,10 @@ def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
 class DistSolver:
     """SPMD solve on one rank of the grid; every rank calls it with the same config."""
 
-    CHUNK_MIN = 256  # filter column chunking (comm/compute overlap) from this block width on
+    # filter column chunking (allreduce overlapped with the next chunk's GEMM) from this block width
+    # on.  Off by default: at C3 the allreduces are ~1-2% of a step and two half-width GEMMs lose
+    # more (4 GPUs: filter 13.0 s chunked vs 12.5 s, profiles/r01/); BSE200_CHUNK_MIN enables it.
+    CHUNK_MIN = int(__import__("os").environ.get("BSE200_CHUNK_MIN", str(1 << 30)))
 
     def __init__(self, grid: Grid, comm: Comm, ops, fwd: Tile, trn: Tile):
         self.g, self.c, self.ops, self.fwd, self.trn = grid, comm, ops, fwd, trn
@@ -437,7 +440,7 @@ class DistSolver:
         cs = self._comm_stream
         with torch.cuda.stream(cs):
             cs.wait_event(done)
-            (self.comm.sum_row if fwd else self.comm.sum_col)(dst)
+            (self.c.sum_row if fwd else self.c.sum_col)(dst)
             red = torch.cuda.Event()
             red.record(cs)
         # keep dst alive for the communication stream's use

@@ -15,7 +15,9 @@ import torch.distributed as dist
 
 from conftest import GOLDEN, golden, golden_ham, rebuild_c1
 from paper_2601_10557_b200 import SolverConfig
-from paper_2601_10557_b200.dist import solve_distributed
+from paper_2601_10557_b200.dist import DistSolver, solve_distributed
+
+DistSolver.CHUNK_MIN = 8  # exercise the chunked, stream-overlapped filter on the small cases
 
 
 def main():
