@@ -175,6 +175,15 @@ int bse_defect(bse_ctx* ctx, const void* d_g, int64_t k, double* h_out);
 /* y = S x for a block of 2*half rows (rows >= half negated)                                   */
 int bse_sflip(bse_ctx* ctx, const void* d_x, int64_t ldx, void* d_y, int64_t ldy, int64_t half, int64_t k);
 
+/* ---- complex64 filter on the tcgen05 tensor cores (configs[4] c64 variant) ---------------
+ * d_pplanes: 4 fp32 planes (Re hi, Re lo, Im hi, Im lo) of [A | B] in the K-major layout
+ * [m rows][2 mp] (mp = m rounded up to 4), i.e. 32 m mp bytes, built by bse_c64_prepare.
+ * bse_chebyshev_filter_c64: p(H) v with FP32-accurate 3xTF32 tcgen05.mma products, the
+ * recurrence in FP32 (chebyshev.py:51-75); d_v (complex128 n x k) in/out; d_work: 24 mp k floats. */
+int bse_c64_prepare(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_pplanes);
+int bse_chebyshev_filter_c64(bse_ctx* ctx, const void* d_pplanes, int64_t m, void* d_v, int64_t ldv, int64_t k, int deg,
+                             double c, double e, double s, void* d_work);
+
 /* ---- synthetic inputs (generate.py:60-83 on the device) -------------------- */
 /* complex normals start_index .. +count of stream `seed` (rng.py:63-81):
  * bit-exact splitmix64 words, device libm Box-Muller (<= ~1 ulp from host). */

@@ -51,7 +51,7 @@ from .solver import (
     solve,
 )
 from .generate import GeneratorSpec, generate
-from ._lib import filter_algorithm, set_filter_algorithm
+from ._lib import filter_algorithm, filter_precision, set_filter_algorithm, set_filter_precision
 from . import fileio
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -74,6 +74,8 @@ _SIGS = {
     "bse_colscale_rsqrt": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_defect": (C.c_int, [_vp, _vp, _i64, _dp]),
     "bse_sflip": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64]),
+    "bse_c64_prepare": (C.c_int, [_vp, _vp, _i64, _i64, _vp]),
+    "bse_chebyshev_filter_c64": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
     "bse_complex_normals": (C.c_int, [_vp, _vp, C.c_uint64, _i64, _i64]),
     "bse_complex_normals_t": (C.c_int, [_vp, _vp, C.c_uint64, _i64, _i64]),
     "bse_symmetrize": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int]),
@@ -115,6 +117,22 @@ def set_filter_algorithm(name: str) -> None:
 
 def filter_algorithm() -> str:
     return {v: k for k, v in _ALGOS.items()}.get(_FILTER_CM, str(_FILTER_CM))
+
+
+# Chebyshev-filter precision: "c128" (FP64 DMMA, default) or "c64" (FP32-accurate 3xTF32 on the
+# tcgen05 tensor cores; configs[4]); the rest of the solve stays complex128
+_FILTER_PRECISION = os.environ.get("BSE200_PRECISION", "c128").lower()
+
+
+def set_filter_precision(name: str) -> None:
+    global _FILTER_PRECISION
+    if name.lower() not in ("c128", "c64"):
+        raise ValueError("filter precision must be 'c128' or 'c64'")
+    _FILTER_PRECISION = name.lower()
+
+
+def filter_precision() -> str:
+    return _FILTER_PRECISION
 
 
 def uses_sum_planes() -> bool:

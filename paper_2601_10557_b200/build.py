@@ -39,7 +39,7 @@ def stale() -> bool:
 def build_library(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(OUT), str(SRC), "-lcublas", "-lcusolver"]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(OUT), str(SRC), "-lcublas", "-lcusolver"]  # driver API via cudaGetDriverEntryPoint
     proc = subprocess.run(cmd, capture_output=True, text=True)
     log = proc.stdout + proc.stderr
     (PKG / "build.log").write_text(log)

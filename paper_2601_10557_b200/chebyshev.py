@@ -45,6 +45,8 @@ def filter_inplace(ham: BseHamiltonian, v, cfg: FilterConfig, work=None, ledger:
     n, k = v.shape
     if k == 0:
         return v
+    if _lib.filter_precision() == "c64":
+        return _filter_c64(ham, v, cfg, ledger)
     if work is None or work.numel() < 2 * ld_of(v) * k:
         import torch
 
@@ -54,6 +56,23 @@ def filter_inplace(ham: BseHamiltonian, v, cfg: FilterConfig, work=None, ledger:
     ctx = _lib.Context.get(v.device.index)
     ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(v), ld_of(v), k, cfg.degree,
              cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))
+    if ledger is not None:
+        ledger.add_flops("filter", cfg.degree * 8.0 * n * n * k)
+    return v
+
+
+def _filter_c64(ham: BseHamiltonian, v, cfg: FilterConfig, ledger):
+    """complex64 filter on the tcgen05 tensor cores (3xTF32 products, FP32 recurrence)."""
+    import torch
+
+    n, k = v.shape
+    m = ham.m
+    mp = (m + 3) // 4 * 4
+    pl = ham.device_c64_planes(v.device)
+    work = torch.empty(24 * mp * k, dtype=torch.float32, device=v.device)
+    ham.device_blocks(v.device)  # binds the Hamiltonian flags (B = 0)
+    _lib.Context.get(v.device.index).call("bse_chebyshev_filter_c64", _lib.dptr(pl), m, _lib.dptr(v), ld_of(v), k,
+                                          cfg.degree, cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))
     if ledger is not None:
         ledger.add_flops("filter", cfg.degree * 8.0 * n * n * k)
     return v

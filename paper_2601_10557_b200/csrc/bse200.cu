@@ -15,8 +15,11 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/bse200.h"
 #include "aux.cuh"
+#include "c64.cuh"
 #include "hop.cuh"
 #include "zgemm.cuh"
 
@@ -673,6 +676,79 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   check_launch(ctx);
 }
 
+// ---------------------------------------------------------------------------------------------
+// complex64 filter on tcgen05 (c64.cuh): TMA tensor maps and the step driver
+// ---------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw BseError(BSE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D fp32 tensor map with a 64-byte-swizzled box (b0 x b1 x b2), strides in bytes
+CUtensorMap map3d(const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2, uint32_t b0,
+                  uint32_t b1, uint32_t b2) {
+  CUtensorMap map;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {s1, s2};
+  cuuint32_t box[3] = {b0, b1, b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw BseError(BSE_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return map;
+}
+
+inline int64_t pad4(int64_t m) { return (m + 3) & ~int64_t(3); }
+
+// P planes: 4 x [m rows][2 mp] fp32;  view (j < m, row i, part) -> strides (2 mp * 4, mp * 4)
+void c64_p_maps(bse::c64::Maps& mp_, const float* pplanes, int64_t m) {
+  const int64_t mp = pad4(m), plane = m * 2 * mp;
+  for (int q = 0; q < 4; ++q)
+    mp_.p[q] = map3d(pplanes + q * plane, m, m, 2, 2 * mp * 4, mp * 4, bse::c64::BKE, bse::c64::BM, 1);
+}
+
+// X planes of one block: 4 x [k cols][2 mp] fp32;  view (j < m, half, col)
+void c64_x_maps(bse::c64::Maps& mp_, float* const planes[4], int64_t m, int64_t k) {
+  const int64_t mp = pad4(m);
+  for (int q = 0; q < 4; ++q)
+    mp_.x[q] = map3d(planes[q], m, 2, k, mp * 4, 2 * mp * 4, bse::c64::BKE, 1, bse::c64::BN);
+}
+
+void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const float* pplanes, int64_t m, int64_t k, float* const x[4],
+              float* const prev[4], float* const out[4], double alpha, double beta, double shift) {
+  static bool configured = false;
+  if (!configured) {
+    CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bse::c64::SMEM));
+    configured = true;
+  }
+  c64_x_maps(maps, x, m, k);
+  bse::c64::StepArgs a{};
+  a.m = (int)m;
+  a.mp = (int)pad4(m);
+  a.k = (int)k;
+  a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
+  for (int q = 0; q < 4; ++q) {
+    a.x[q] = x[q];
+    a.p[q] = prev ? prev[q] : nullptr;
+    a.out[q] = out[q];
+  }
+  a.alpha = (float)alpha;
+  a.beta = prev ? (float)beta : 0.f;
+  a.shift = (float)shift;
+  dim3 grid((unsigned)((k + bse::c64::BN - 1) / bse::c64::BN), (unsigned)((m + bse::c64::BM - 1) / bse::c64::BM));
+  bse::c64::step_kernel<<<grid, bse::c64::THREADS, bse::c64::SMEM, ctx->stream>>>(maps, a);
+  check_launch(ctx);
+}
+
 }  // namespace
 
 // ============================================================================
@@ -1250,6 +1326,54 @@ int bse_sflip(bse_ctx* ctx, const void* d_x, int64_t ldx, void* d_y, int64_t ldy
     if (k <= 0 || half <= 0) return;
     bse::sflip_copy_kernel<<<grid1d(2 * half * k), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_x), ldx,
                                                                            static_cast<zval*>(d_y), ldy, half, k);
+    check_launch(ctx);
+  });
+}
+
+int bse_c64_prepare(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_pplanes) {
+  return guarded(ctx, [&] {
+    if (m <= 0) return;
+    const int64_t mp = pad4(m), plane = m * 2 * mp;
+    float* pl = static_cast<float*>(d_pplanes);
+    bse::c64::p_planes_kernel<<<grid1d(plane, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        static_cast<const zval*>(d_ab), lda, (int)m, (int)mp, pl, pl + plane, pl + 2 * plane, pl + 3 * plane);
+    check_launch(ctx);
+  });
+}
+
+int bse_chebyshev_filter_c64(bse_ctx* ctx, const void* d_pplanes, int64_t m, void* d_v, int64_t ldv, int64_t k, int deg,
+                             double c, double e, double s, void* d_work) {
+  return guarded(ctx, [&] {
+    if (deg < 2 || deg % 2) throw BseError(BSE_EVALIDATION, "filter degree must be even and >= 2");
+    if (!(e > 0)) throw BseError(BSE_EVALIDATION, "filter half width must be positive");
+    if (k <= 0 || m <= 0) return;
+    const int64_t mp = pad4(m), blk = 2 * mp * k;
+    float* w = static_cast<float*>(d_work);
+    float* bufs[3][4];
+    for (int b = 0; b < 3; ++b)
+      for (int q = 0; q < 4; ++q) bufs[b][q] = w + (int64_t)(4 * b + q) * blk;
+    bse::c64::to_planes_kernel<<<grid1d(blk, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        static_cast<const zval*>(d_v), ldv, (int)m, (int)mp, (int)k, bufs[0][0], bufs[0][1], bufs[0][2], bufs[0][3]);
+    check_launch(ctx);
+    bse::c64::Maps maps;
+    c64_p_maps(maps, static_cast<const float*>(d_pplanes), m);
+    // chebyshev.py:58-74 on three rotating plane blocks
+    const double sigma1 = e / (s - c);
+    double sigma = sigma1;
+    int prev = 0, cur = 1;
+    c64_step(ctx, maps, static_cast<const float*>(d_pplanes), m, k, bufs[0], nullptr, bufs[1], sigma1 / e, 0.0, c);
+    for (int step = 2; step <= deg; ++step) {
+      const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
+      const int nxt = 3 - prev - cur;
+      c64_step(ctx, maps, static_cast<const float*>(d_pplanes), m, k, bufs[cur], bufs[prev], bufs[nxt],
+               2.0 * sigma_new / e, sigma * sigma_new, c);
+      prev = cur;
+      cur = nxt;
+      sigma = sigma_new;
+    }
+    const int64_t n = 2 * m;
+    bse::c64::from_planes_kernel<<<grid1d(n * k, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        bufs[cur][0], bufs[cur][1], bufs[cur][2], bufs[cur][3], (int)m, (int)mp, (int)k, static_cast<zval*>(d_v), ldv);
     check_launch(ctx);
   });
 }

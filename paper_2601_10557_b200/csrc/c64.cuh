@@ -1,0 +1,315 @@
+// complex64 Chebyshev filter on the 5th-generation tensor cores (configs[4] c64 variant).
+//
+// FP32-accurate complex products from tcgen05.mma kind::tf32 with the 3xTF32 split
+// x = hi + lo (hi = tf32(x), lo = x - hi):  a b ~= a_hi b_hi + a_hi b_lo + a_lo b_hi.
+// The operator is the same as the FP64 hop kernel (hop.cuh): with P the K-slab of [A | B],
+//   U = P Xa,  L' = conj(P) Xb,  H x = [U ; -L'],
+// as four real accumulators in TMEM (U_r, U_i, L'_r, L'_i; 128 lanes x 64 fp32 columns each):
+//   U_r = Pr Xar - Pi Xai   U_i = Pr Xai + Pi Xar   L'_r = Pr Xbr + Pi Xbi   L'_i = Pr Xbi - Pi Xbr
+// i.e. 8 real products x 3 = 24 UMMA (128 x 64 x 8) per K step; negation through the
+// instruction descriptor.  Operands live in HBM as fp32 hi/lo planes in K-major layouts
+// (P planes row-major over K, X planes = the column-major vectors) and are fed by 3-D TMA
+// boxes (64-byte swizzle) whose out-of-range rows are zero-filled by the hardware, so the A/B
+// part and upper/lower half boundaries need no special casing.  Warp 0 = TMA producer,
+// warp 1 = MMA issuer, warps 2-9 = accumulation drain + epilogue:
+// y+ = alpha (H y - c y) - beta y-, written back as hi/lo planes for the next step.
+#pragma once
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace bse {
+namespace c64 {
+
+constexpr int BM = 128;               // UMMA M: output rows per CTA (per half)
+constexpr int BN = 64;                // UMMA N: vector columns per CTA
+constexpr int BKE = 16;               // K elements per stage (64-byte swizzle rows)
+constexpr int STAGES = 3;
+constexpr int CHUNK = 2;              // stages per TMEM accumulation chunk (4 UMMA K steps)
+constexpr int PLANE_TILE_P = BM * BKE * 4;  // 8 KB
+constexpr int PLANE_TILE_X = BN * BKE * 4;  // 4 KB
+constexpr int STAGE_BYTES = 4 * PLANE_TILE_P + 8 * PLANE_TILE_X;  // 64 KB
+constexpr int EPI_WARPS = 8;          // 2 per TMEM lane quadrant, 32 columns each
+constexpr int THREADS = 32 * (2 + EPI_WARPS);
+constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+
+// K-major operand in the 64-byte swizzle canonical layout: rows of 64 B (16 fp32), 8-row groups
+// 512 B apart; tile base 512-byte aligned.
+__device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;   // SBO: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;            // version 1
+  d |= (uint64_t)4 << 61;            // SWIZZLE_64B
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
+          tc::smem_addr(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_addr(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+struct Maps {
+  CUtensorMap p[4];  // P planes: Re hi, Re lo, Im hi, Im lo   (3-D: j, row i, part)
+  CUtensorMap x[4];  // X planes of the step input: Re hi, Re lo, Im hi, Im lo (3-D: j, half, column)
+};
+
+struct StepArgs {
+  int m, mp, k;            // rows per half, padded half stride (multiple of 4), columns
+  int skip_b;              // B == 0: contract over the A part only
+  // planes (fp32, column-major n x k with ld = 2 mp, lower half at row mp)
+  const float* x[4];       // step input y (hi/lo, re/im) - shift operand
+  const float* p[4];       // y_prev (may alias out)
+  float* out[4];           // y_next
+  float alpha, beta, shift;
+};
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Accumulation precision: the tensor core adds each MMA into its FP32 TMEM accumulator with
+// truncation, so the error of one long accumulation grows linearly with K (measured ~2^-24 per
+// add: 1.6e-4 relative at K = 8000).  The K loop is therefore cut into chunks of CHUNK stages
+// accumulated in one of two TMEM buffers; the 8 epilogue warps drain each finished chunk into
+// round-to-nearest FP32 register accumulators while the MMA warp fills the other buffer.
+__global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant__ Maps maps, const StepArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int c0 = blockIdx.x * BN, i0 = blockIdx.y * BM;
+  const int nk_part = (a.m + BKE - 1) / BKE;
+  const int nk = a.skip_b ? nk_part : 2 * nk_part;
+  const int nchunks = (nk + CHUNK - 1) / CHUNK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], EPI_WARPS);
+    }
+    tc::fence_barrier_init();
+    for (int q = 0; q < 4; ++q) {
+      tc::prefetch_tmap(&maps.p[q]);
+      tc::prefetch_tmap(&maps.x[q]);
+    }
+  }
+  if (warp == 0) tc::tmem_alloc(tslot, 512);  // 2 buffers x 4 accumulators x 64 fp32 columns
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // -------------------------------------------------------------- TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        const int part = kb >= nk_part;
+        const int j = (kb - part * nk_part) * BKE;
+        tc::mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        unsigned char* st = base + s * STAGE_BYTES;
+        for (int q = 0; q < 4; ++q) tma_load_3d(st + q * PLANE_TILE_P, &maps.p[q], &full[s], j, i0, part);
+        unsigned char* sx = st + 4 * PLANE_TILE_P;
+        // Xa = half `part`, Xb = the other half (part 0: X1, X2; part 1: X2, X1)
+        for (int q = 0; q < 4; ++q) {
+          tma_load_3d(sx + q * PLANE_TILE_X, &maps.x[q], &full[s], j, part, c0);
+          tma_load_3d(sx + (4 + q) * PLANE_TILE_X, &maps.x[q], &full[s], j, 1 - part, c0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // -------------------------------------------------------------- MMA issuer
+      constexpr uint32_t ipos = tc::idesc_tf32(BM, BN, false, false);
+      constexpr uint32_t ineg = tc::idesc_tf32(BM, BN, true, false);
+      for (int ch = 0; ch < nchunks; ++ch) {
+        const int b = ch & 1;
+        if (ch >= 2) tc::mbar_wait(&acc_empty[b], ((ch >> 1) - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t acc_ur = tmem + b * 256, acc_ui = acc_ur + 64, acc_lr = acc_ur + 128, acc_li = acc_ur + 192;
+        const int kb_end = min(nk, (ch + 1) * CHUNK);
+        for (int kb = ch * CHUNK; kb < kb_end; ++kb) {
+          const int s = kb % STAGES;
+          tc::mbar_wait(&full[s], (kb / STAGES) & 1);
+          tc::fence_after_sync();
+          const uint32_t st = tc::smem_addr(base + s * STAGE_BYTES);
+          const uint32_t sx = st + 4 * PLANE_TILE_P;
+#pragma unroll
+          for (int kk = 0; kk < BKE / 8; ++kk) {
+            const uint32_t off = kk * 32;
+            const uint64_t prh = sdesc_k_sw64(st + 0 * PLANE_TILE_P + off),
+                           prl = sdesc_k_sw64(st + 1 * PLANE_TILE_P + off);
+            const uint64_t pih = sdesc_k_sw64(st + 2 * PLANE_TILE_P + off),
+                           pil = sdesc_k_sw64(st + 3 * PLANE_TILE_P + off);
+            uint64_t xa[4], xb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              xa[q] = sdesc_k_sw64(sx + q * PLANE_TILE_X + off);
+              xb[q] = sdesc_k_sw64(sx + (4 + q) * PLANE_TILE_X + off);
+            }
+            const bool first = (kb == ch * CHUNK && kk == 0);
+            // 3xTF32 real product  acc (+/-)= (ph, pl) x (xh, xl)
+            auto prod = [&](uint32_t acc, uint64_t ph, uint64_t pl, uint64_t xh, uint64_t xl, uint32_t id, bool init) {
+              tc::mma_tf32(acc, ph, xh, id, !init);
+              tc::mma_tf32(acc, ph, xl, id, true);
+              tc::mma_tf32(acc, pl, xh, id, true);
+            };
+            prod(acc_ur, prh, prl, xa[0], xa[1], ipos, first);  // + Pr Xar
+            prod(acc_ur, pih, pil, xa[2], xa[3], ineg, false);  // - Pi Xai
+            prod(acc_ui, prh, prl, xa[2], xa[3], ipos, first);  // + Pr Xai
+            prod(acc_ui, pih, pil, xa[0], xa[1], ipos, false);  // + Pi Xar
+            prod(acc_lr, prh, prl, xb[0], xb[1], ipos, first);  // + Pr Xbr
+            prod(acc_lr, pih, pil, xb[2], xb[3], ipos, false);  // + Pi Xbi
+            prod(acc_li, prh, prl, xb[2], xb[3], ipos, first);  // + Pr Xbi
+            prod(acc_li, pih, pil, xb[0], xb[1], ineg, false);  // - Pi Xbr
+          }
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&acc_full[b]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue warps
+    const int ew = warp - 2;
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
+    const int colh = ew >> 2;           // column half: 0 -> [0, 32), 1 -> [32, 64)
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    float acc[4][32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[q][c] = 0.f;
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int b = ch & 1;
+      tc::mbar_wait(&acc_full[b], (ch >> 1) & 1);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float v[16];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          tc::tmem_ld16(tmem + lane_off + b * 256 + q * 64 + colh * 32 + h * 16, v);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) acc[q][h * 16 + c] += v[c];
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty[b]);
+    }
+    // y+ = alpha (H y - c y) - beta y-   with  H y = [U ; -L']
+    const int row = i0 + quad * 32 + lane;
+    const int64_t ld = 2 * (int64_t)a.mp;
+    if (row < a.m) {
+#pragma unroll 4
+      for (int c = 0; c < 32; ++c) {
+        const int col = c0 + colh * 32 + c;
+        if (col >= a.k) break;
+        const int64_t up = (int64_t)col * ld + row, lo = up + a.mp;
+        float hur = acc[0][c], hui = acc[1][c], hlr = -acc[2][c], hli = -acc[3][c];
+        if (a.shift != 0.f) {
+          hur -= a.shift * (a.x[0][up] + a.x[1][up]);
+          hui -= a.shift * (a.x[2][up] + a.x[3][up]);
+          hlr -= a.shift * (a.x[0][lo] + a.x[1][lo]);
+          hli -= a.shift * (a.x[2][lo] + a.x[3][lo]);
+        }
+        float yur = a.alpha * hur, yui = a.alpha * hui, ylr = a.alpha * hlr, yli = a.alpha * hli;
+        if (a.beta != 0.f) {
+          yur -= a.beta * (a.p[0][up] + a.p[1][up]);
+          yui -= a.beta * (a.p[2][up] + a.p[3][up]);
+          ylr -= a.beta * (a.p[0][lo] + a.p[1][lo]);
+          yli -= a.beta * (a.p[2][lo] + a.p[3][lo]);
+        }
+        float h;
+        h = tf32_hi(yur); a.out[0][up] = h; a.out[1][up] = yur - h;
+        h = tf32_hi(yui); a.out[2][up] = h; a.out[3][up] = yui - h;
+        h = tf32_hi(ylr); a.out[0][lo] = h; a.out[1][lo] = ylr - h;
+        h = tf32_hi(yli); a.out[2][lo] = h; a.out[3][lo] = yli - h;
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------- layout conversions
+// P planes from [A | B] (complex128, column-major m x 2m, lda): plane[q][i * (2 mp) + part * mp + j]
+// = hi/lo of Re/Im P[i, part m + j], with P rows of A read as conj(column i) (A hermitian) and
+// rows of B as column i (B symmetric): coalesced reads and writes.
+__global__ void p_planes_kernel(const zval* __restrict__ ab, int64_t lda, int m, int mp, float* __restrict__ pl0,
+                                float* __restrict__ pl1, float* __restrict__ pl2, float* __restrict__ pl3) {
+  const int64_t total = (int64_t)m * 2 * mp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / (2 * mp);
+    const int J = int(idx % (2 * mp));
+    const int part = J >= mp, j = J - part * mp;
+    float re = 0.f, im = 0.f;
+    if (j < m) {
+      const zval v = ab[(int64_t)(part * m + i) * lda + j];  // column i of A (or B), entry j
+      re = (float)v.re;
+      im = part ? (float)v.im : -(float)v.im;  // row i of A = conj(column i)
+    }
+    const float rh = tf32_hi(re), ih = tf32_hi(im);
+    pl0[idx] = rh;
+    pl1[idx] = re - rh;
+    pl2[idx] = ih;
+    pl3[idx] = im - ih;
+  }
+}
+
+// c128 vectors (n x k, ldv) -> hi/lo planes (ld = 2 mp, lower half at mp; pad rows zero)
+__global__ void to_planes_kernel(const zval* __restrict__ v, int64_t ldv, int m, int mp, int k, float* __restrict__ q0,
+                                 float* __restrict__ q1, float* __restrict__ q2, float* __restrict__ q3) {
+  const int64_t ld = 2 * (int64_t)mp, total = ld * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = idx / ld;
+    const int r = int(idx % ld);
+    const int half = r >= mp, rr = r - half * mp;
+    float re = 0.f, im = 0.f;
+    if (rr < m) {
+      const zval z = v[col * ldv + half * m + rr];
+      re = (float)z.re;
+      im = (float)z.im;
+    }
+    const float rh = tf32_hi(re), ih = tf32_hi(im);
+    q0[idx] = rh;
+    q1[idx] = re - rh;
+    q2[idx] = ih;
+    q3[idx] = im - ih;
+  }
+}
+
+__global__ void from_planes_kernel(const float* __restrict__ q0, const float* __restrict__ q1,
+                                   const float* __restrict__ q2, const float* __restrict__ q3, int m, int mp, int k,
+                                   zval* __restrict__ v, int64_t ldv) {
+  const int64_t n = 2 * (int64_t)m, total = n * k, ld = 2 * (int64_t)mp;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = idx / n;
+    const int r = int(idx % n);
+    const int half = r >= m, rr = r - half * m;
+    const int64_t s = col * ld + half * mp + rr;
+    v[col * ldv + r] = zval{(double)q0[s] + (double)q1[s], (double)q2[s] + (double)q3[s]};
+  }
+}
+
+}  // namespace c64
+}  // namespace bse

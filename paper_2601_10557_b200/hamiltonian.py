@@ -192,8 +192,25 @@ class BseHamiltonian:
             sd_cache[device] = sd
         return sd
 
+    def device_c64_planes(self, device):
+        """fp32 hi/lo planes of [A | B] in the K-major layout of the tcgen05 c64 filter
+        (bse_c64_prepare; 32 m mp bytes), built once per device."""
+        torch = _torch()
+        device = torch.device(device)
+        cache = self.__dict__.setdefault("_p64", {})
+        pl = cache.get(device)
+        if pl is None:
+            ab = self.device_blocks(device)
+            m = ab.shape[0]
+            mp = (m + 3) // 4 * 4
+            pl = torch.empty(4 * m * 2 * mp, dtype=torch.float32, device=device)
+            _lib.Context.get(device.index).call("bse_c64_prepare", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(pl))
+            cache[device] = pl
+        return pl
+
     def release_device(self) -> None:
         self.__dict__.get("_sd", {}).clear()
+        self.__dict__.get("_p64", {}).clear()
         if self.a is not None:
             self._dev.clear()
 

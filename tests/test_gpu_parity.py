@@ -351,3 +351,46 @@ def test_pchb_device_reader_and_cli_solve(bse, tmp_path):
     v = fileio.read_pchv(tmp_path / "eigenvectors.bin")
     assert v.shape == (16, 2)
     assert (tmp_path / "trace.csv").exists() and (tmp_path / "manifest.json").exists()
+
+
+def test_c64_tcgen05_filter_accuracy(bse):
+    """complex64 filter on tcgen05 (3xTF32): the filter output within FP32 accuracy of the
+    reference's complex128 filter (golden), and of the oracle on a ragged shape."""
+    a, b = golden_ham(16, 5)
+    g = golden("ops_m16_s5.npz")
+    ham = bse.BseHamiltonian(a, b)
+    cfg = bse.FilterConfig(int(g["deg"]), float(g["center"]), float(g["half_width"]), float(g["scale_ref"]))
+    try:
+        bse.set_filter_precision("c64")
+        out = bse.chebyshev_filter(ham, g["x"], cfg)
+        rs = np.random.default_rng(7)
+        m = 300
+        a2 = rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m))
+        a2 = a2 @ a2.conj().T / m + np.eye(m)
+        b2 = rs.standard_normal((m, m)) + 1j * rs.standard_normal((m, m))
+        b2 = 0.1 * (b2 + b2.T) / 2
+        x2 = rs.standard_normal((2 * m, 130)) + 1j * rs.standard_normal((2 * m, 130))
+        h2 = bse.BseHamiltonian(a2, b2)
+        c2 = bse.FilterConfig(6, 1.0, 3.0, -5.0)
+        out2 = bse.chebyshev_filter(h2, x2, c2)
+    finally:
+        bse.set_filter_precision("c128")
+    assert _rel(out, g["filtered"]) <= 2e-5  # FP32 arithmetic (3xTF32 products, fp32 accumulation)
+    ref2 = o.cheb_filter(a2, b2, x2, 6, 1.0, 3.0, -5.0)
+    assert _rel(out2, ref2) <= 2e-5
+
+
+def test_c64_solve_c1_parity(bse, c1_instance):
+    """C1 with the complex64 filter under the c64 policy (rel_res, tol 1e-5):
+    eigenvalues within 1e-4 relative of the complex128 reference."""
+    a, b, g = c1_instance
+    try:
+        bse.set_filter_precision("c64")
+        r = bse.solve(bse.BseHamiltonian(a, b), bse.SolverConfig(nev=50, nex=20, deg=20, tol=1e-5, seed=0,
+                                                                  rel_res=True))
+    finally:
+        bse.set_filter_precision("c128")
+    assert r.converged
+    rel = np.abs(r.lambdas - g["rel_lambdas"]) / np.abs(g["rel_lambdas"])
+    assert rel.max() <= 1e-4
+    assert r.residual_norms.max() <= 1e-5 * abs(r.bounds.mu_1)
