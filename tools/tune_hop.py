@@ -71,6 +71,24 @@ def whole_filter(m, ks, codes, deg=4):
     ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 6))
 
 
+def c64_filter(m, ks, deg=4):
+    """bse_chebyshev_filter_c64 (tcgen05 3xTF32) per step."""
+    n = 2 * m
+    mp = (m + 3) // 4 * 4
+    ab = colmajor_empty(m, 2 * m, dev)
+    ab.real.normal_()
+    ab.imag.normal_()
+    pl = torch.empty(4 * m * 2 * mp, dtype=torch.float32, device=dev)
+    ctx.call("bse_c64_prepare", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(pl))
+    for k in ks:
+        v = colmajor_empty(n, k, dev); v.real.normal_(); v.imag.normal_()
+        work = torch.empty(24 * mp * k, dtype=torch.float32, device=dev)
+        ms = timed(lambda: ctx.call("bse_chebyshev_filter_c64", _lib.dptr(pl), m, _lib.dptr(v), n, k, deg, 0.0, 1.0,
+                                    -1.5, _lib.dptr(work)), 2)
+        print(f"c64 filter deg={deg} m={m} k={k}: {ms / deg:8.2f} ms/step  model {8.0 * n * n * k * deg / ms / 1e9:7.1f} "
+              f"TF/s  (tf32 executed {3 * 8.0 * n * n * k * deg / ms / 1e9:7.1f})", flush=True)
+
+
 def solver_small():
     for k in (100, 200, 400, 600, 800, 1000, 1200):
         g = torch.randn((k, k), dtype=torch.complex128, device=dev)
