@@ -47,6 +47,17 @@ PRECISION = {"c3c64": "c64"}
 COUPLING = {"c3b0": 0.0}
 METRIC = "time-to-solution, nev eigenpairs @ n=40k; filter FP64 TFLOP/s as % of peak"
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak.json"
+TRAFFIC_FILE = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+
+
+def ncu_traffic(algo: str):
+    """DRAM bytes per launch of the filter kernel at k = 1200 from the committed ncu capture."""
+    try:
+        d = json.loads(TRAFFIC_FILE.read_text())
+        key = "c64" if algo.startswith("c64") else ("3m" if algo.startswith("3m") else "4m")
+        return d[key]["bytes"], f"ncu --set full, {d[key]['kernel']} at k={d[key]['k']} ({TRAFFIC_FILE.name})"
+    except Exception:
+        return None, None
 # expected modeled flops of one C3 solve (from our own trace, profiles/); used by the CPU arm
 TRACE_FILE = ROOT / "profiles" / "solve_trace_{cfg}.json"
 
@@ -370,8 +381,10 @@ def run_ours(args, world, rank, local):
             "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": launches // args.steps,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
-                         "kernel": "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)",
+                         "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(algo)[0],
+                         "traffic_source": ncu_traffic(algo)[1],
+                         "kernel": ("bse::c64::step_kernel (tcgen05 3xTF32 complex64 filter step)" if algo.startswith("c64")
+                                    else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
                          "peak_source": peak_src,
                          "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model, BASELINE.md §3.5) "
                                         "per GPU, summed over the solve's filter calls / CUDA-event (1 GPU) or "
