@@ -42,7 +42,10 @@ CONFIGS = {
     "c3b0": (20000, 1000, 200, 20, 1e-10, True),  # configs[4]: C3 with B = 0 (coupling_ratio 0)
     "c4": (50000, 3000, 500, 20, 1e-10, True),    # configs[3]: n = 100k (8 GPUs in BASELINE.json)
     "c3c64": (20000, 1000, 200, 20, 1e-5, True),  # configs[4]: C3 with the complex64 (tcgen05) filter,
-}                                                 # c64 policy rel tol 1e-5
+                                                  # c64 policy rel tol 1e-5
+    "c3mixed": (20000, 1000, 200, 20, 1e-10, True),  # C3, mixed-precision filter policy (early iterations
+}                                                    # c64 on tcgen05, FP64 from 1e-4 |mu_1| residuals on)
+MIXED = {"c3mixed"}
 PRECISION = {"c3c64": "c64"}
 COUPLING = {"c3b0": 0.0}
 METRIC = "time-to-solution, nev eigenpairs @ n=40k; filter FP64 TFLOP/s as % of peak"
@@ -248,6 +251,7 @@ def run_ours(args, world, rank, local):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     bse.set_filter_precision(PRECISION.get(args.config, "c128"))
+    bse.set_mixed_precision(args.config in MIXED)
     m, nev, nex, deg, tol, rel = CONFIGS[args.config]
     n = 2 * m
     t0 = time.perf_counter()
@@ -400,6 +404,7 @@ def run_ours(args, world, rank, local):
                       "lambda_1": float(res.lambdas[0]), "lambda_nev": float(res.lambdas[-1]),
                       "max_residual": float(res.residual_norms.max()),
                       "locked_per_iter": [t.locked for t in res.trace],
+                      "filter_precision_per_iter": getattr(res, "filter_precisions", None),
                       "phase_events_s": [[ph, round(dt, 4)] for ph, dt in res.ledger.events],
                       "e2e_iterations": r_e2e.iterations_used,
                       "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},

@@ -48,6 +48,7 @@ from .solver import (
     TraceRecord,
     complete_spectrum,
     mirror_largest,
+    set_mixed_precision,
     solve,
 )
 from .generate import GeneratorSpec, generate

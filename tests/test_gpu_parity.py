@@ -394,3 +394,17 @@ def test_c64_solve_c1_parity(bse, c1_instance):
     rel = np.abs(r.lambdas - g["rel_lambdas"]) / np.abs(g["rel_lambdas"])
     assert rel.max() <= 1e-4
     assert r.residual_norms.max() <= 1e-5 * abs(r.bounds.mu_1)
+
+
+def test_mixed_precision_solve_parity(bse, c1_instance, monkeypatch):
+    """Mixed-precision ChASE (early filters complex64 on tcgen05, later FP64): C1 under both
+    tolerance policies keeps the reference's eigenvalues (1e-10 rel), residuals and iterations +-1."""
+    monkeypatch.setenv("BSE200_MIXED", "1")
+    a, b, g = c1_instance
+    ham = bse.BseHamiltonian(a, b)
+    for tag, rel in (("abs", False), ("rel", True)):
+        r = bse.solve(ham, bse.SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0, rel_res=rel))
+        assert r.converged and "c64" in r.filter_precisions and r.filter_precisions[-1] == "c128"
+        assert abs(r.iterations_used - int(g[f"{tag}_iters"])) <= 1
+        assert (np.abs(r.lambdas - g[f"{tag}_lambdas"]) / np.abs(g[f"{tag}_lambdas"])).max() <= 1e-10
+        assert r.residual_norms.max() <= 1e-10 * (abs(r.bounds.mu_1) if rel else 1.0)
