@@ -99,7 +99,7 @@ _STATUS = {
 _lib = None
 _lock = threading.Lock()
 # complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
-_ALGOS = {"4m": 4, "3m": 6, "3m-onthefly": 3, "3m-xsum": 7, "3m-ahead": 8, "3m-smem": 9}
+_ALGOS = {"4m": 4, "3m": 65, "3m-64x16": 6, "3m-onthefly": 3, "3m-xsum": 7, "3m-ahead": 8, "3m-smem": 9}
 # default 3M (Gauss) with precomputed operand-sum planes: 25% fewer DMMA, parity-checked at C1
 # (tests/test_gpu_parity.py); BSE200_FILTER=4m restores the 4M split
 _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "3m").lower()]
@@ -136,7 +136,7 @@ def filter_precision() -> str:
 
 
 def uses_sum_planes() -> bool:
-    return _FILTER_CM in (6, 7, 8, 81) or 61 <= _FILTER_CM <= 63
+    return _FILTER_CM in (6, 7, 8, 81) or 61 <= _FILTER_CM <= 66
 
 
 def load() -> C.CDLL:

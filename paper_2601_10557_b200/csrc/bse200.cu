@@ -236,6 +236,9 @@ using Hop3MS = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1>;
 using Hop3MS_1 = bse::HopCfg<64, 32, 8, 2, 2, 4, 1, 1>;
 using Hop3MS_2 = bse::HopCfg<64, 32, 16, 2, 2, 3, 1, 1>;
 using Hop3MS_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
+using Hop3MS_4 = bse::HopCfg<32, 32, 8, 2, 2, 4, 2, 1>;
+using Hop3MS_5 = bse::HopCfg<32, 32, 8, 2, 2, 4, 3, 1>;
+using Hop3MS_6 = bse::HopCfg<64, 16, 8, 2, 1, 3, 3, 1>;
 // 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
 using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
 // 3M with P sums from planes and X sums computed in shared memory one stage ahead (code 8, 81)
@@ -251,7 +254,7 @@ using Hop3MB_2 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 2, 2>;
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
   if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
-  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 63)) && (!a.sa || !a.sb))
+  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 66)) && (!a.sa || !a.sb))
     code = 3;  // no P sum planes
   switch (code) {
     case 9: launch_hop<Hop3MB, bse::HOP_AXPBY, 9>(ctx, a); break;
@@ -264,6 +267,9 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
     case 61: launch_hop<Hop3MS_1, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 62: launch_hop<Hop3MS_2, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 63: launch_hop<Hop3MS_3, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 64: launch_hop<Hop3MS_4, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 65: launch_hop<Hop3MS_5, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 66: launch_hop<Hop3MS_6, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
@@ -801,7 +807,7 @@ int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
                     complex_mults == 8 || complex_mults == 81 || complex_mults == 9 || complex_mults == 91 ||
                     complex_mults == 92 ||
                     (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
-                    (complex_mults >= 61 && complex_mults <= 63);
+                    (complex_mults >= 61 && complex_mults <= 66);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
   });
