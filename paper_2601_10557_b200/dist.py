@@ -306,9 +306,7 @@ def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
 
     fwd = one((grid.r0, grid.r1), (grid.c0, grid.c1))
     trn = one((grid.c0, grid.c1), (grid.r0, grid.r1))
-    if _lib.uses_sum_planes():
-        fwd, trn = add_sum_planes(ops, fwd), add_sum_planes(ops, trn)
-    return fwd, trn
+    return fwd, trn  # 3M sum planes are attached lazily at the first solve (after the source is freed)
 
 
 # ----------------------------------------------------------------------------- distributed solver
@@ -764,6 +762,10 @@ class DistributedSolver:
     def solve(self, cfg: SolverConfig) -> SolveResult:
         if hasattr(self.ops, "ctx"):
             self.ops.ctx.set_ham_flags(self.flags)
+        if _lib.uses_sum_planes():
+            for t in (self.fwd, self.trn):
+                if t.sd is None:
+                    add_sum_planes(self.ops, t)
         res = self.inner.solve(cfg)
         res.v = res.v.T  # (n, nev) column-major view
         return res
@@ -780,8 +782,7 @@ def make_tiles_from_pieces(ops, pieces: dict):
             src = torch.from_numpy(np.ascontiguousarray(blk.T)) if isinstance(blk, np.ndarray) else blk.T
             buf[h * kc:(h + 1) * kc].copy_(src)
         addr = buf.data_ptr()
-        t = Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc)
-        tiles.append(add_sum_planes(ops, t) if _lib.uses_sum_planes() else t)
+        tiles.append(Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc))
     return tuple(tiles)
 
 
