@@ -326,28 +326,31 @@ def run_ours(args, world, rank, local):
         solver_mod.filter_inplace = orig
 
     # end to end through the public API with HOST buffers: upload inside the timed region
-    if world == 1:
+    if args.no_e2e:
+        r_e2e, e2e_s, h2d, d2h = res, None, 0, 0
+    elif world == 1:
         a_h, b_h = ham.host_blocks()
         host_ham = BseHamiltonian(a_h, b_h, Definiteness.DEFINITE)  # definiteness certified by the generator
         h2d = 2 * m * m * 16 + n * cfg.nevex * 16 + 8 * n * 16
     else:
         pieces = ds.tile_pieces_host()
         h2d = world * sum(x.nbytes for name in ("fwd", "trn") for x in pieces[name]) + world * (n // world) * cfg.nevex * 16
-    barrier(world)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    if world == 1:
-        r_e2e = bse.solve(host_ham, cfg, device=dev)  # returns numpy v
-        v_host = r_e2e.v
-    else:
-        ds.load(pieces)
-        r_e2e = ds.solve(cfg)
-        v_host = r_e2e.v.T.contiguous().cpu().numpy().T if rank == 0 else None
-    torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    d2h = n * nev * 16 + 8 * (cfg.nevex + 64)
-    if world == 1:
-        host_ham.release_device()
+    if not args.no_e2e:
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if world == 1:
+            r_e2e = bse.solve(host_ham, cfg, device=dev)  # returns numpy v
+            v_host = r_e2e.v
+        else:
+            ds.load(pieces)
+            r_e2e = ds.solve(cfg)
+            v_host = r_e2e.v.T.contiguous().cpu().numpy().T if rank == 0 else None
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+        d2h = n * nev * 16 + 8 * (cfg.nevex + 64)
+        if world == 1:
+            host_ham.release_device()
 
     peak, peak_src = fp64_peak()
     achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
@@ -426,6 +429,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer end-to-end solve (long demo runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         # CPU arm: rank 0 alone works; the other ranks exit at once (no process group needed)
