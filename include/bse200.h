@@ -179,7 +179,7 @@ int bse_sflip(bse_ctx* ctx, const void* d_x, int64_t ldx, void* d_y, int64_t ldy
  * d_pplanes: 4 fp32 planes (Re hi, Re lo, Im hi, Im lo) of [A | B] in the K-major layout
  * [m rows][2 mp] (mp = m rounded up to 4), i.e. 32 m mp bytes, built by bse_c64_prepare.
  * bse_chebyshev_filter_c64: p(H) v with FP32-accurate 3xTF32 tcgen05.mma products, the
- * recurrence in FP32 (chebyshev.py:51-75); d_v (complex128 n x k) in/out; d_work: 24 mp k floats. */
+ * recurrence in FP32 (chebyshev.py:51-75); d_v (complex128 n x k) in/out; d_work: 48 mp k floats. */
 int bse_c64_prepare(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_pplanes);
 int bse_chebyshev_filter_c64(bse_ctx* ctx, const void* d_pplanes, int64_t m, void* d_v, int64_t ldv, int64_t k, int deg,
                              double c, double e, double s, void* d_work);

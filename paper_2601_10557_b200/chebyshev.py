@@ -69,7 +69,7 @@ def _filter_c64(ham: BseHamiltonian, v, cfg: FilterConfig, ledger):
     m = ham.m
     mp = (m + 3) // 4 * 4
     pl = ham.device_c64_planes(v.device)
-    work = torch.empty(24 * mp * k, dtype=torch.float32, device=v.device)
+    work = torch.empty(48 * mp * k, dtype=torch.float32, device=v.device)
     ham.device_blocks(v.device)  # binds the Hamiltonian flags (B = 0)
     _lib.Context.get(v.device.index).call("bse_chebyshev_filter_c64", _lib.dptr(pl), m, _lib.dptr(v), ld_of(v), k,
                                           cfg.degree, cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))

@@ -721,15 +721,15 @@ void c64_p_maps(bse::c64::Maps& mp_, const float* pplanes, int64_t m) {
     mp_.p[q] = map3d(pplanes + q * plane, m, m, 2, 2 * mp * 4, mp * 4, bse::c64::BKE, bse::c64::BM, 1);
 }
 
-// X planes of one block: 4 x [k cols][2 mp] fp32;  view (j < m, half, col)
-void c64_x_maps(bse::c64::Maps& mp_, float* const planes[4], int64_t m, int64_t k) {
+// X planes of one block: 8 x [k cols][2 mp] fp32;  view (j < m, half, col)
+void c64_x_maps(bse::c64::Maps& mp_, float* const planes[8], int64_t m, int64_t k) {
   const int64_t mp = pad4(m);
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < 8; ++q)
     mp_.x[q] = map3d(planes[q], m, 2, k, mp * 4, 2 * mp * 4, bse::c64::BKE, 1, bse::c64::BN);
 }
 
-void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const float* pplanes, int64_t m, int64_t k, float* const x[4],
-              float* const prev[4], float* const out[4], double alpha, double beta, double shift) {
+void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const float* pplanes, int64_t m, int64_t k, float* const x[8],
+              float* const prev[8], float* const out[8], double alpha, double beta, double shift) {
   static bool configured = false;
   if (!configured) {
     CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -745,8 +745,8 @@ void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const float* pplanes, int64_t 
   for (int q = 0; q < 4; ++q) {
     a.x[q] = x[q];
     a.p[q] = prev ? prev[q] : nullptr;
-    a.out[q] = out[q];
   }
+  for (int q = 0; q < 8; ++q) a.out[q] = out[q];
   a.alpha = (float)alpha;
   a.beta = prev ? (float)beta : 0.f;
   a.shift = (float)shift;
@@ -1355,11 +1355,13 @@ int bse_chebyshev_filter_c64(bse_ctx* ctx, const void* d_pplanes, int64_t m, voi
     if (k <= 0 || m <= 0) return;
     const int64_t mp = pad4(m), blk = 2 * mp * k;
     float* w = static_cast<float*>(d_work);
-    float* bufs[3][4];
+    float* bufs[3][8];
     for (int b = 0; b < 3; ++b)
-      for (int q = 0; q < 4; ++q) bufs[b][q] = w + (int64_t)(4 * b + q) * blk;
+      for (int q = 0; q < 8; ++q) bufs[b][q] = w + (int64_t)(8 * b + q) * blk;
+    bse::c64::Planes8 p0;
+    for (int q = 0; q < 8; ++q) p0.p[q] = bufs[0][q];
     bse::c64::to_planes_kernel<<<grid1d(blk, 256, 148 * 32), 256, 0, ctx->stream>>>(
-        static_cast<const zval*>(d_v), ldv, (int)m, (int)mp, (int)k, bufs[0][0], bufs[0][1], bufs[0][2], bufs[0][3]);
+        static_cast<const zval*>(d_v), ldv, (int)m, (int)mp, (int)k, p0);
     check_launch(ctx);
     bse::c64::Maps maps;
     c64_p_maps(maps, static_cast<const float*>(d_pplanes), m);

@@ -23,11 +23,15 @@ namespace c64 {
 constexpr int BM = 128;               // UMMA M: output rows per CTA (per half)
 constexpr int BN = 64;                // UMMA N: vector columns per CTA
 constexpr int BKE = 16;               // K elements per stage (64-byte swizzle rows)
-constexpr int STAGES = 3;
+constexpr int STAGES = 2;
 constexpr int CHUNK = 2;              // stages per TMEM accumulation chunk (4 UMMA K steps)
 constexpr int PLANE_TILE_P = BM * BKE * 4;  // 8 KB
 constexpr int PLANE_TILE_X = BN * BKE * 4;  // 4 KB
-constexpr int STAGE_BYTES = 4 * PLANE_TILE_P + 8 * PLANE_TILE_X;  // 64 KB
+// X side per stage: for each half (a, b) and each of hi / lo a stack of three 64-row tiles,
+// a: [-Xi | Xr | Xi], b: [Xr | Xi | -Xr], so that the N = 128 windows [Xr|Xi] / [-Xi|Xr] (a) and
+// [Xr|Xi] / [Xi|-Xr] (b) are contiguous K-major operands
+constexpr int STACK = 3 * PLANE_TILE_X;                                // 12 KB
+constexpr int STAGE_BYTES = 4 * PLANE_TILE_P + 4 * STACK;              // 80 KB
 constexpr int EPI_WARPS = 8;          // 2 per TMEM lane quadrant, 32 columns each
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
 constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
@@ -55,7 +59,7 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
 
 struct Maps {
   CUtensorMap p[4];  // P planes: Re hi, Re lo, Im hi, Im lo   (3-D: j, row i, part)
-  CUtensorMap x[4];  // X planes of the step input: Re hi, Re lo, Im hi, Im lo (3-D: j, half, column)
+  CUtensorMap x[8];  // X planes of the step input: Re hi, Re lo, Im hi, Im lo, -Re hi, -Re lo, -Im hi, -Im lo
 };
 
 struct StepArgs {
@@ -64,7 +68,7 @@ struct StepArgs {
   // planes (fp32, column-major n x k with ld = 2 mp, lower half at row mp)
   const float* x[4];       // step input y (hi/lo, re/im) - shift operand
   const float* p[4];       // y_prev (may alias out)
-  float* out[4];           // y_next
+  float* out[8];           // y_next (hi/lo, re/im, then the negated planes)
   float alpha, beta, shift;
 };
 
@@ -72,6 +76,19 @@ __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// hi/lo planes of (re, im) and of their negations at offset idx
+__device__ __forceinline__ void store_planes(float* const (&q)[8], int64_t idx, float re, float im) {
+  const float rh = tf32_hi(re), ih = tf32_hi(im), rl = re - rh, il = im - ih;
+  q[0][idx] = rh;
+  q[1][idx] = rl;
+  q[2][idx] = ih;
+  q[3][idx] = il;
+  q[4][idx] = -rh;
+  q[5][idx] = -rl;
+  q[6][idx] = -ih;
+  q[7][idx] = -il;
 }
 
 // Accumulation precision: the tensor core adds each MMA into its FP32 TMEM accumulator with
@@ -129,22 +146,28 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
         for (int q = 0; q < 4; ++q) tma_load_3d(st + q * PLANE_TILE_P, &maps.p[q], &full[s], j, i0, part);
         unsigned char* sx = st + 4 * PLANE_TILE_P;
         // Xa = half `part`, Xb = the other half (part 0: X1, X2; part 1: X2, X1)
-        for (int q = 0; q < 4; ++q) {
-          tma_load_3d(sx + q * PLANE_TILE_X, &maps.x[q], &full[s], j, part, c0);
-          tma_load_3d(sx + (4 + q) * PLANE_TILE_X, &maps.x[q], &full[s], j, 1 - part, c0);
+        // plane index: re = 0 + hl, im = 2 + hl, -re = 4 + hl, -im = 6 + hl (hl: 0 hi, 1 lo)
+        for (int hl = 0; hl < 2; ++hl) {
+          unsigned char* sa = sx + hl * STACK;        // a stack: [-Xi | Xr | Xi]
+          unsigned char* sb = sx + (2 + hl) * STACK;  // b stack: [Xr | Xi | -Xr]
+          tma_load_3d(sa, &maps.x[6 + hl], &full[s], j, part, c0);
+          tma_load_3d(sa + PLANE_TILE_X, &maps.x[0 + hl], &full[s], j, part, c0);
+          tma_load_3d(sa + 2 * PLANE_TILE_X, &maps.x[2 + hl], &full[s], j, part, c0);
+          tma_load_3d(sb, &maps.x[0 + hl], &full[s], j, 1 - part, c0);
+          tma_load_3d(sb + PLANE_TILE_X, &maps.x[2 + hl], &full[s], j, 1 - part, c0);
+          tma_load_3d(sb + 2 * PLANE_TILE_X, &maps.x[4 + hl], &full[s], j, 1 - part, c0);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // -------------------------------------------------------------- MMA issuer
-      constexpr uint32_t ipos = tc::idesc_tf32(BM, BN, false, false);
-      constexpr uint32_t ineg = tc::idesc_tf32(BM, BN, true, false);
+      constexpr uint32_t idesc = tc::idesc_tf32(BM, 2 * BN, false, false);  // N = 128 windows
       for (int ch = 0; ch < nchunks; ++ch) {
         const int b = ch & 1;
         if (ch >= 2) tc::mbar_wait(&acc_empty[b], ((ch >> 1) - 1) & 1);
         tc::fence_after_sync();
-        const uint32_t acc_ur = tmem + b * 256, acc_ui = acc_ur + 64, acc_lr = acc_ur + 128, acc_li = acc_ur + 192;
+        const uint32_t acc_u = tmem + b * 256, acc_l = acc_u + 128;  // [U_r | U_i], [L'_r | L'_i]
         const int kb_end = min(nk, (ch + 1) * CHUNK);
         for (int kb = ch * CHUNK; kb < kb_end; ++kb) {
           const int s = kb % STAGES;
@@ -159,27 +182,22 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
                            prl = sdesc_k_sw64(st + 1 * PLANE_TILE_P + off);
             const uint64_t pih = sdesc_k_sw64(st + 2 * PLANE_TILE_P + off),
                            pil = sdesc_k_sw64(st + 3 * PLANE_TILE_P + off);
-            uint64_t xa[4], xb[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              xa[q] = sdesc_k_sw64(sx + q * PLANE_TILE_X + off);
-              xb[q] = sdesc_k_sw64(sx + (4 + q) * PLANE_TILE_X + off);
-            }
+            // windows: w0 = stack rows [0, 128), w1 = rows [64, 192)
+            const uint64_t a_h0 = sdesc_k_sw64(sx + 0 * STACK + off), a_h1 = sdesc_k_sw64(sx + 0 * STACK + PLANE_TILE_X + off);
+            const uint64_t a_l0 = sdesc_k_sw64(sx + 1 * STACK + off), a_l1 = sdesc_k_sw64(sx + 1 * STACK + PLANE_TILE_X + off);
+            const uint64_t b_h0 = sdesc_k_sw64(sx + 2 * STACK + off), b_h1 = sdesc_k_sw64(sx + 2 * STACK + PLANE_TILE_X + off);
+            const uint64_t b_l0 = sdesc_k_sw64(sx + 3 * STACK + off), b_l1 = sdesc_k_sw64(sx + 3 * STACK + PLANE_TILE_X + off);
             const bool first = (kb == ch * CHUNK && kk == 0);
-            // 3xTF32 real product  acc (+/-)= (ph, pl) x (xh, xl)
-            auto prod = [&](uint32_t acc, uint64_t ph, uint64_t pl, uint64_t xh, uint64_t xl, uint32_t id, bool init) {
-              tc::mma_tf32(acc, ph, xh, id, !init);
-              tc::mma_tf32(acc, ph, xl, id, true);
-              tc::mma_tf32(acc, pl, xh, id, true);
+            // 3xTF32 real product  acc += (ph, pl) x (xh, xl)
+            auto prod = [&](uint32_t acc, uint64_t ph, uint64_t pl, uint64_t xh, uint64_t xl, bool init) {
+              tc::mma_tf32(acc, ph, xh, idesc, !init);
+              tc::mma_tf32(acc, ph, xl, idesc, true);
+              tc::mma_tf32(acc, pl, xh, idesc, true);
             };
-            prod(acc_ur, prh, prl, xa[0], xa[1], ipos, first);  // + Pr Xar
-            prod(acc_ur, pih, pil, xa[2], xa[3], ineg, false);  // - Pi Xai
-            prod(acc_ui, prh, prl, xa[2], xa[3], ipos, first);  // + Pr Xai
-            prod(acc_ui, pih, pil, xa[0], xa[1], ipos, false);  // + Pi Xar
-            prod(acc_lr, prh, prl, xb[0], xb[1], ipos, first);  // + Pr Xbr
-            prod(acc_lr, pih, pil, xb[2], xb[3], ipos, false);  // + Pi Xbi
-            prod(acc_li, prh, prl, xb[2], xb[3], ipos, first);  // + Pr Xbi
-            prod(acc_li, pih, pil, xb[0], xb[1], ineg, false);  // - Pi Xbr
+            prod(acc_u, prh, prl, a_h1, a_l1, first);  // Pr [Xar | Xai]
+            prod(acc_u, pih, pil, a_h0, a_l0, false);  // Pi [-Xai | Xar]
+            prod(acc_l, prh, prl, b_h0, b_l0, first);  // Pr [Xbr | Xbi]
+            prod(acc_l, pih, pil, b_h1, b_l1, false);  // Pi [Xbi | -Xbr]
           }
           tc::mma_commit(&empty[s]);
         }
@@ -238,11 +256,8 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
           ylr -= a.beta * (a.p[0][lo] + a.p[1][lo]);
           yli -= a.beta * (a.p[2][lo] + a.p[3][lo]);
         }
-        float h;
-        h = tf32_hi(yur); a.out[0][up] = h; a.out[1][up] = yur - h;
-        h = tf32_hi(yui); a.out[2][up] = h; a.out[3][up] = yui - h;
-        h = tf32_hi(ylr); a.out[0][lo] = h; a.out[1][lo] = ylr - h;
-        h = tf32_hi(yli); a.out[2][lo] = h; a.out[3][lo] = yli - h;
+        store_planes(a.out, up, yur, yui);
+        store_planes(a.out, lo, ylr, yli);
       }
     }
   }
@@ -276,9 +291,12 @@ __global__ void p_planes_kernel(const zval* __restrict__ ab, int64_t lda, int m,
   }
 }
 
+struct Planes8 {
+  float* p[8];
+};
+
 // c128 vectors (n x k, ldv) -> hi/lo planes (ld = 2 mp, lower half at mp; pad rows zero)
-__global__ void to_planes_kernel(const zval* __restrict__ v, int64_t ldv, int m, int mp, int k, float* __restrict__ q0,
-                                 float* __restrict__ q1, float* __restrict__ q2, float* __restrict__ q3) {
+__global__ void to_planes_kernel(const zval* __restrict__ v, int64_t ldv, int m, int mp, int k, Planes8 q) {
   const int64_t ld = 2 * (int64_t)mp, total = ld * k;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t col = idx / ld;
@@ -290,11 +308,7 @@ __global__ void to_planes_kernel(const zval* __restrict__ v, int64_t ldv, int m,
       re = (float)z.re;
       im = (float)z.im;
     }
-    const float rh = tf32_hi(re), ih = tf32_hi(im);
-    q0[idx] = rh;
-    q1[idx] = re - rh;
-    q2[idx] = ih;
-    q3[idx] = im - ih;
+    store_planes(q.p, idx, re, im);
   }
 }
 

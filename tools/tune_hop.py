@@ -82,7 +82,7 @@ def c64_filter(m, ks, deg=4):
     ctx.call("bse_c64_prepare", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(pl))
     for k in ks:
         v = colmajor_empty(n, k, dev); v.real.normal_(); v.imag.normal_()
-        work = torch.empty(24 * mp * k, dtype=torch.float32, device=dev)
+        work = torch.empty(48 * mp * k, dtype=torch.float32, device=dev)
         ms = timed(lambda: ctx.call("bse_chebyshev_filter_c64", _lib.dptr(pl), m, _lib.dptr(v), n, k, deg, 0.0, 1.0,
                                     -1.5, _lib.dptr(work)), 2)
         print(f"c64 filter deg={deg} m={m} k={k}: {ms / deg:8.2f} ms/step  model {8.0 * n * n * k * deg / ms / 1e9:7.1f} "
