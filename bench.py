@@ -57,7 +57,9 @@ def ncu_traffic(algo: str):
     """DRAM bytes per launch of the filter kernel at k = 1200 from the committed ncu capture."""
     try:
         d = json.loads(TRAFFIC_FILE.read_text())
-        key = "c64" if algo.startswith("c64") else ("3m" if algo.startswith("3m") else "4m")
+        key = "c64" if algo.startswith("c64") else algo
+        if key not in d:
+            return None, None
         return d[key]["bytes"], f"ncu --set full, {d[key]['kernel']} at k={d[key]['k']} ({TRAFFIC_FILE.name})"
     except Exception:
         return None, None
@@ -394,7 +396,8 @@ def run_ours(args, world, rank, local):
                          "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(algo)[0],
                          "traffic_source": ncu_traffic(algo)[1],
                          "kernel": ("bse::c64::step_kernel (tcgen05 3xTF32 complex64 filter step)" if algo.startswith("c64")
-                                    else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
+                                    else "bse::hop3m_mb_kernel (fused H-operator 3M DMMA GEMM, mbarrier pipeline, Chebyshev epilogue)"
+                                    if algo == "3m" else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
                          "peak_source": peak_src,
                          "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model, BASELINE.md §3.5) "
                                         "per GPU, summed over the solve's filter calls / CUDA-event (1 GPU) or "

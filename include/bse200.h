@@ -163,6 +163,11 @@ int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv
 /* Small pencil of the hermitian RR (rayleigh_ritz.py:113-137) from the summed W = Q^H S H Q
  * and G2 = Q2^H Q2: ascending Ritz values (host) and the sorted back-transform L^{-H} y (device). */
 int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec, double* h_lam_min_m);
+/* Small problem of the backup RR (rayleigh_ritz.py:160-175) from summed partials G0 = Q^H S H Q
+ * (overwritten), W = Q^H H Q and G2 = Q2^H Q2 (overwritten), all k x k: ascending real parts of the
+ * eigenvalues (host) and the matching eigenvectors y (device, k x k); V = Q y / |Q y| is the caller's. */
+int bse_rr_backup_pencil(bse_ctx* ctx, void* d_g0, const void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_y,
+                         double* h_lam_min_m);
 /* residual partials from the RR intermediate: out[j] = sum_i |sgn_i u_ij uscale_j - lam_j v_ij|^2,
  * sgn_i = -1 for rows >= half (u = (S H Q) w, v = unit Ritz vectors, uscale = 1/|Q w|)            */
 int bse_resid_partial(bse_ctx* ctx, const void* d_u, int64_t ldu, const void* d_v, int64_t ldv, int64_t rows,

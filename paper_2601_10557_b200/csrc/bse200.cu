@@ -21,6 +21,7 @@
 #include "aux.cuh"
 #include "c64.cuh"
 #include "hop.cuh"
+#include "hop_mb.cuh"
 #include "zgemm.cuh"
 
 using bse::zval;
@@ -223,6 +224,20 @@ void launch_hop(bse_ctx* ctx, const bse::HopArgs& a_in) {
   check_launch(ctx);
 }
 
+template <class C>
+void launch_hop_mb(bse_ctx* ctx, const bse::HopArgs& a_in) {
+  bse::HopArgs a = a_in;
+  a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_mb_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    configured = true;
+  }
+  dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
+  bse::hop3m_mb_kernel<C><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  check_launch(ctx);
+}
+
 // tuning variants (selected with bse_set_filter_algorithm codes 40+v / 30+v)
 using Hop4M_1 = bse::HopCfg<64, 32, 8, 2, 2, 5, 2>;
 using Hop4M_2 = bse::HopCfg<128, 32, 8, 2, 2, 4, 1>;
@@ -239,6 +254,16 @@ using Hop3MS_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
 using Hop3MS_4 = bse::HopCfg<32, 32, 8, 2, 2, 4, 2, 1>;
 using Hop3MS_5 = bse::HopCfg<32, 32, 8, 2, 2, 4, 3, 1>;
 using Hop3MS_6 = bse::HopCfg<64, 16, 8, 2, 1, 3, 3, 1>;
+// mbarrier-pipelined 3M (hop_mb.cuh), codes 67-69
+using Hop3MM_7 = bse::HopCfg<32, 32, 8, 2, 2, 4, 2, 1>;
+using Hop3MM_8 = bse::HopCfg<32, 32, 8, 2, 2, 3, 3, 1>;
+using Hop3MM_9 = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1>;
+using Hop3MM_10 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
+using Hop3MM_11 = bse::HopCfg<64, 16, 8, 4, 1, 3, 3, 1>;
+using Hop3MM_12 = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 1>;
+using Hop3MM_13 = bse::HopCfg<96, 16, 8, 6, 1, 3, 2, 1>;
+using Hop3MM_14 = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
+using Hop3MM_15 = bse::HopCfg<128, 16, 8, 4, 1, 4, 1, 1>;
 // 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
 using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
 // 3M with P sums from planes and X sums computed in shared memory one stage ahead (code 8, 81)
@@ -254,7 +279,7 @@ using Hop3MB_2 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 2, 2>;
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
   if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
-  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 66)) && (!a.sa || !a.sb))
+  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 75)) && (!a.sa || !a.sb))
     code = 3;  // no P sum planes
   switch (code) {
     case 9: launch_hop<Hop3MB, bse::HOP_AXPBY, 9>(ctx, a); break;
@@ -270,6 +295,15 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
     case 64: launch_hop<Hop3MS_4, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 65: launch_hop<Hop3MS_5, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 66: launch_hop<Hop3MS_6, bse::HOP_AXPBY, 6>(ctx, a); break;
+    case 67: launch_hop_mb<Hop3MM_7>(ctx, a); break;
+    case 68: launch_hop_mb<Hop3MM_8>(ctx, a); break;
+    case 69: launch_hop_mb<Hop3MM_9>(ctx, a); break;
+    case 70: launch_hop_mb<Hop3MM_10>(ctx, a); break;
+    case 71: launch_hop_mb<Hop3MM_11>(ctx, a); break;
+    case 72: launch_hop_mb<Hop3MM_12>(ctx, a); break;
+    case 73: launch_hop_mb<Hop3MM_13>(ctx, a); break;
+    case 74: launch_hop_mb<Hop3MM_14>(ctx, a); break;
+    case 75: launch_hop_mb<Hop3MM_15>(ctx, a); break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
@@ -807,7 +841,7 @@ int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
                     complex_mults == 8 || complex_mults == 81 || complex_mults == 9 || complex_mults == 91 ||
                     complex_mults == 92 ||
                     (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
-                    (complex_mults >= 61 && complex_mults <= 66);
+                    (complex_mults >= 61 && complex_mults <= 75);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
   });
@@ -1036,6 +1070,78 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, con
   });
 }
 
+size_t backup_ws_bytes(int64_t k) {
+  const size_t kk = (size_t)k * k;
+  return 5 * al(kk * sizeof(zval)) + 2 * al(k * 16) + 2 * al(k * 8) + al(k * 4) + al(64) + gemm_ws_bytes(k, k, k) +
+         4096;
+}
+
+// k x k tail of the backup projection (rayleigh_ritz.py:160-175) from summed partials:
+// g = Q^H S H Q (overwritten), w = Q^H H Q, g2 = Q2^H Q2 (overwritten).  Ascending real parts of
+// eig(g') with g' = diag(d)^{-1} (g - offdiag(M) w), M = I - 2 g2; y = the sorted eigenvectors.
+void backup_pencil(bse_ctx* ctx, zval* g, const zval* w, zval* g2, int64_t k, double* h_lam, zval* yperm,
+                   double* h_lam_min_m, Scratch& sc) {
+  const size_t kk = (size_t)k * k;
+  zval* mm = sc.take<zval>(kk);
+  zval* tmp = sc.take<zval>(kk);
+  zval* y = sc.take<zval>(kk);
+  zval* d_ev = sc.take<zval>(k);
+  double* d_w = sc.take<double>(k);
+  double* d_d = sc.take<double>(k);
+  int* d_perm = sc.take<int>(k);
+  int* d_info = sc.take<int>(4);
+  zval* gws = sc.take<zval>(gemm_ws_bytes(k, k, k) / sizeof(zval) + 1);
+  bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g2, mm, (int)k);
+  check_launch(ctx);
+  bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
+  check_launch(ctx);
+  CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+  heevd(ctx, tmp, (int)k, d_w, false, d_info);
+  std::vector<double> hw(k);
+  to_host(ctx, hw.data(), d_w, k);
+  double lmm = INFINITY;
+  for (double v : hw) lmm = std::min(lmm, std::fabs(v));
+  if (h_lam_min_m) *h_lam_min_m = lmm;
+  bse::diag_real_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(mm, (int)k, 1e-12, d_d);
+  check_launch(ctx);
+  bse::offdiag_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, tmp, (int)k);
+  check_launch(ctx);
+  // g = (g0 - off W) / d
+  zgemm<bse::OPA_N>(ctx, k, k, k, -1.0, tmp, k, w, k, 1.0, g, k, gws);
+  bse::rowscale_inv_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k, d_d);
+  check_launch(ctx);
+  // direct.py:102-116: general eigensolver, ascending real parts (stable)
+  size_t dws = 0, hws = 0;
+  SOLVER_OK(cusolverDnXgeev_bufferSize(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,
+                                       k, CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F, nullptr, 1, CUDA_C_64F, y, k,
+                                       CUDA_C_64F, &dws, &hws));
+  void* dbuf = solver_ws(ctx, dws);
+  void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
+  SOLVER_OK(cusolverDnXgeev(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, k,
+                            CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F, nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F,
+                            dbuf, dws, hbuf, hws, d_info));
+  int* info = reinterpret_cast<int*>(pinned(ctx, 1));
+  CUDA_OK(cudaMemcpyAsync(info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  if (*info != 0) throw BseError(BSE_ENUMERICAL, "general eigensolver failed (info " + std::to_string(*info) + ")");
+  std::vector<double> ev(2 * k);
+  to_host(ctx, ev.data(), reinterpret_cast<double*>(d_ev), 2 * k);
+  std::vector<int> order(k);
+  std::iota(order.begin(), order.end(), 0);
+  for (int64_t i = 0; i < k; ++i)
+    if (!std::isfinite(ev[2 * i]) || !std::isfinite(ev[2 * i + 1]))
+      throw BseError(BSE_ENUMERICAL, "general eigensolver returned non-finite eigenvalues");
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ev[2 * a] < ev[2 * b]; });
+  for (int64_t i = 0; i < k; ++i) h_lam[i] = ev[2 * order[i]];
+  {
+    std::vector<double> tmpd((k + 1) / 2 + 1);
+    std::memcpy(tmpd.data(), order.data(), sizeof(int) * k);
+    to_device(ctx, reinterpret_cast<double*>(d_perm), tmpd.data(), (k + 1) / 2);
+  }
+  bse::gather_cols_kernel<<<dim3(1, (unsigned)k), 256, 0, ctx->stream>>>(y, k, yperm, k, k, d_perm);
+  check_launch(ctx);
+}
+
 int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
                   double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
   return guarded(ctx, [&] {
@@ -1044,84 +1150,38 @@ int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const 
     const zval* q = static_cast<const zval*>(d_q);
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
-    const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k),
-                                  gemm_ws_bytes(k, k, k)});
-    Scratch sc(ctx, al(n * k * sizeof(zval)) + 6 * al(kk * sizeof(zval)) + 3 * al(k * 16) + al(k * 4) + al(64) + gwsb +
-                        4096);
+    const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
+    Scratch sc(ctx, al(n * k * sizeof(zval)) + 4 * al(kk * sizeof(zval)) + al(k * 8) + gwsb + backup_ws_bytes(k));
     zval* t = sc.take<zval>(n * k);
     zval* w = sc.take<zval>(kk);
-    zval* mm = sc.take<zval>(kk);
-    zval* tmp = sc.take<zval>(kk);
+    zval* g2 = sc.take<zval>(kk);
     zval* g = sc.take<zval>(kk);
-    zval* y = sc.take<zval>(kk);
     zval* yperm = sc.take<zval>(kk);
-    zval* d_ev = sc.take<zval>(k);
-    double* d_w = sc.take<double>(k);
-    double* d_d = sc.take<double>(k);
-    int* d_perm = sc.take<int>(k);
-    int* d_info = sc.take<int>(4);
+    double* d_nrm = sc.take<double>(k);
     zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
     // rayleigh_ritz.py:160-168
     apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, 1.0);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
-    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, tmp, k, gws);
-    bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(tmp, mm, (int)k);
-    check_launch(ctx);
-    bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
-    check_launch(ctx);
-    CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
-    heevd(ctx, tmp, (int)k, d_w, false, d_info);
-    std::vector<double> hw(k);
-    to_host(ctx, hw.data(), d_w, k);
-    double lmm = INFINITY;
-    for (double v : hw) lmm = std::min(lmm, std::fabs(v));
-    if (h_lam_min_m) *h_lam_min_m = lmm;
-    bse::diag_real_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(mm, (int)k, 1e-12, d_d);
-    check_launch(ctx);
-    bse::offdiag_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, tmp, (int)k);
-    check_launch(ctx);
+    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
     // g0 = Q^H (S T) = Q1^H T1 - Q2^H T2
     zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q, ldq, t, n, 0.0, g, k, gws);
     zgemm<bse::OPA_C>(ctx, k, k, m, -1.0, q + m, ldq, t + m, n, 1.0, g, k, gws);
-    // g = (g0 - off W) / d
-    zgemm<bse::OPA_N>(ctx, k, k, k, -1.0, tmp, k, w, k, 1.0, g, k, gws);
-    bse::rowscale_inv_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k, d_d);
-    check_launch(ctx);
-    // direct.py:102-116: general eigensolver, ascending real parts (stable)
-    size_t dws = 0, hws = 0;
-    SOLVER_OK(cusolverDnXgeev_bufferSize(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR,
-                                         CUSOLVER_EIG_MODE_VECTOR, k, CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F,
-                                         nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F, &dws, &hws));
-    void* dbuf = solver_ws(ctx, dws);
-    void* hbuf = host_ws(ctx, std::max<size_t>(hws, 16));
-    SOLVER_OK(cusolverDnXgeev(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR, k,
-                              CUDA_C_64F, g, k, CUDA_C_64F, d_ev, CUDA_C_64F, nullptr, 1, CUDA_C_64F, y, k, CUDA_C_64F,
-                              dbuf, dws, hbuf, hws, d_info));
-    int* info = reinterpret_cast<int*>(pinned(ctx, 1));
-    CUDA_OK(cudaMemcpyAsync(info, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_OK(cudaStreamSynchronize(ctx->stream));
-    if (*info != 0) throw BseError(BSE_ENUMERICAL, "general eigensolver failed (info " + std::to_string(*info) + ")");
-    std::vector<double> ev(2 * k);
-    to_host(ctx, ev.data(), reinterpret_cast<double*>(d_ev), 2 * k);
-    std::vector<int> order(k);
-    std::iota(order.begin(), order.end(), 0);
-    for (int64_t i = 0; i < k; ++i)
-      if (!std::isfinite(ev[2 * i]) || !std::isfinite(ev[2 * i + 1]))
-        throw BseError(BSE_ENUMERICAL, "general eigensolver returned non-finite eigenvalues");
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return ev[2 * a] < ev[2 * b]; });
-    for (int64_t i = 0; i < k; ++i) h_lam[i] = ev[2 * order[i]];
-    {
-      std::vector<double> tmpd((k + 1) / 2 + 1);
-      std::memcpy(tmpd.data(), order.data(), sizeof(int) * k);
-      to_device(ctx, reinterpret_cast<double*>(d_perm), tmpd.data(), (k + 1) / 2);
-    }
-    bse::gather_cols_kernel<<<dim3(1, (unsigned)k), 256, 0, ctx->stream>>>(y, k, yperm, k, k, d_perm);
-    check_launch(ctx);
+    backup_pencil(ctx, g, w, g2, k, h_lam, yperm, h_lam_min_m, sc);
     zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, q, ldq, yperm, k, 0.0, vout, ldvout, gws);
-    bse::colnorm_kernel<<<(int)k, 256, 0, ctx->stream>>>(vout, ldvout, n, d_w);
+    bse::colnorm_kernel<<<(int)k, 256, 0, ctx->stream>>>(vout, ldvout, n, d_nrm);
     check_launch(ctx);
-    bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_w);
+    bse::colscale_inv_kernel<<<dim3(grid1d(n, 256, 64), (unsigned)k), 256, 0, ctx->stream>>>(vout, ldvout, n, d_nrm);
     check_launch(ctx);
+  });
+}
+
+int bse_rr_backup_pencil(bse_ctx* ctx, void* d_g0, const void* d_w, void* d_g2, int64_t k, double* h_lam,
+                         void* d_y, double* h_lam_min_m) {
+  return guarded(ctx, [&] {
+    if (k <= 0) return;
+    Scratch sc(ctx, backup_ws_bytes(k));
+    backup_pencil(ctx, static_cast<zval*>(d_g0), static_cast<const zval*>(d_w), static_cast<zval*>(d_g2), k, h_lam,
+                  static_cast<zval*>(d_y), h_lam_min_m, sc);
   });
 }
 

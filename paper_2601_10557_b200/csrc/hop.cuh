@@ -182,6 +182,57 @@ __device__ __forceinline__ void hop_stage_xsums(zval* st) {
   }
 }
 
+// Chebyshev / plain epilogue of one CTA tile: y = alpha (H x - shift x) - beta y_prev, lower half
+// times low_sign, optional Re + Im planes of the output (shared by hop_kernel and hop3m_mb_kernel)
+template <class C, int CM>
+__device__ __forceinline__ void hop_epilogue_axpby(const double (&acc)[Acc<CM>::N][C::WM][C::WN][2], const HopArgs& a,
+                                                   int i0, int c0, int wm, int wn, int g, int t) {
+#pragma unroll
+  for (int i = 0; i < C::WM; ++i) {
+    const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
+    if (row >= a.mr) continue;
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + h;
+        if (col >= a.k) continue;
+        // H x rows: up = U, low = -L'
+        double hu_r, hu_i, hl_r, hl_i;
+        acc_values<CM, C::WM, C::WN>(acc, i, j, h, hu_r, hu_i, hl_r, hl_i);
+        hl_r = -hl_r;
+        hl_i = -hl_i;
+        if ((a.shift != 0.0 || a.shift_col) && row >= a.shift_lo && row < a.shift_hi) {
+          const double sh = a.shift_col ? a.shift_col[col] : a.shift;
+          const zval s1 = a.s1[(int64_t)col * a.lds + row];
+          const zval s2 = a.s2[(int64_t)col * a.lds + row];
+          hu_r = hu_r - sh * s1.re;
+          hu_i = hu_i - sh * s1.im;
+          hl_r = hl_r - sh * s2.re;
+          hl_i = hl_i - sh * s2.im;
+        }
+        zval o1{a.alpha * hu_r, a.alpha * hu_i}, o2{a.alpha * hl_r, a.alpha * hl_i};
+        if (a.beta != 0.0) {
+          const zval q1 = a.p1[(int64_t)col * a.ldp + row];
+          const zval q2 = a.p2[(int64_t)col * a.ldp + row];
+          o1.re = o1.re - a.beta * q1.re;
+          o1.im = o1.im - a.beta * q1.im;
+          o2.re = o2.re - a.beta * q2.re;
+          o2.im = o2.im - a.beta * q2.im;
+        }
+        o2.re *= a.low_sign;
+        o2.im *= a.low_sign;
+        a.y1[(int64_t)col * a.ldy + row] = o1;
+        a.y2[(int64_t)col * a.ldy + row] = o2;
+        if (a.ys1) {
+          a.ys1[(int64_t)col * a.ldys + row] = o1.re + o1.im;
+          a.ys2[(int64_t)col * a.ldys + row] = o2.re + o2.im;
+        }
+      }
+    }
+  }
+}
+
 template <class C, int EPI, int CM = 4>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -321,50 +372,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
 
   // ---------------------------------------------------------------- epilogue
   if constexpr (EPI == HOP_AXPBY) {
-#pragma unroll
-    for (int i = 0; i < C::WM; ++i) {
-      const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
-      if (row >= a.mr) continue;
-#pragma unroll
-      for (int j = 0; j < C::WN; ++j) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + h;
-          if (col >= a.k) continue;
-          // H x rows: up = U, low = -L'
-          double hu_r, hu_i, hl_r, hl_i;
-          acc_values<CM, C::WM, C::WN>(acc, i, j, h, hu_r, hu_i, hl_r, hl_i);
-          hl_r = -hl_r;
-          hl_i = -hl_i;
-          if ((a.shift != 0.0 || a.shift_col) && row >= a.shift_lo && row < a.shift_hi) {
-            const double sh = a.shift_col ? a.shift_col[col] : a.shift;
-            const zval s1 = a.s1[(int64_t)col * a.lds + row];
-            const zval s2 = a.s2[(int64_t)col * a.lds + row];
-            hu_r = hu_r - sh * s1.re;
-            hu_i = hu_i - sh * s1.im;
-            hl_r = hl_r - sh * s2.re;
-            hl_i = hl_i - sh * s2.im;
-          }
-          zval o1{a.alpha * hu_r, a.alpha * hu_i}, o2{a.alpha * hl_r, a.alpha * hl_i};
-          if (a.beta != 0.0) {
-            const zval q1 = a.p1[(int64_t)col * a.ldp + row];
-            const zval q2 = a.p2[(int64_t)col * a.ldp + row];
-            o1.re = o1.re - a.beta * q1.re;
-            o1.im = o1.im - a.beta * q1.im;
-            o2.re = o2.re - a.beta * q2.re;
-            o2.im = o2.im - a.beta * q2.im;
-          }
-          o2.re *= a.low_sign;
-          o2.im *= a.low_sign;
-          a.y1[(int64_t)col * a.ldy + row] = o1;
-          a.y2[(int64_t)col * a.ldy + row] = o2;
-          if (a.ys1) {
-            a.ys1[(int64_t)col * a.ldys + row] = o1.re + o1.im;
-            a.ys2[(int64_t)col * a.ldys + row] = o2.re + o2.im;
-          }
-        }
-      }
-    }
+    hop_epilogue_axpby<C, CM>(acc, a, i0, c0, wm, wn, g, t);
   } else {
     // residual column norms: sum over this CTA's rows of |Hv - lam v|^2 (both halves)
     __shared__ double red[C::WARPS_M][C::BN];

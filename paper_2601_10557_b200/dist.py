@@ -33,6 +33,7 @@ for the collectives.
 from __future__ import annotations
 
 import ctypes
+import logging
 import math
 from dataclasses import dataclass
 
@@ -48,6 +49,9 @@ from .solver import SolveResult, SolverConfig, TraceRecord, TAG_LANCZOS, TAG_SUB
 
 ZB = 16  # bytes per complex128
 _TIMING = __import__("os").environ.get("BSE200_TIMING") == "1"
+
+
+logger = logging.getLogger("paper_2601_10557_b200.dist")
 
 
 class _Steps:
@@ -231,6 +235,15 @@ class CudaOps:
         self.ctx.call("bse_rr_pencil", _lib.dptr(w), _lib.dptr(g2), k, _lib.hptr(lam), _lib.dptr(wvec),
                       ctypes.byref(lmm))
         return lam, wvec, lmm.value
+
+    def rr_backup_pencil(self, g0, w, g2):
+        k = w.shape[0]
+        lam = np.zeros(k)
+        y = self.empty(k, k)
+        lmm = ctypes.c_double(0.0)
+        self.ctx.call("bse_rr_backup_pencil", _lib.dptr(g0), _lib.dptr(w), _lib.dptr(g2), k, _lib.hptr(lam),
+                      _lib.dptr(y), ctypes.byref(lmm))
+        return lam, y, lmm.value
 
     def colnorm2(self, x):
         out = self.torch.empty(x.shape[0], dtype=self.torch.float64, device=self.device)
@@ -508,22 +521,49 @@ class DistSolver:
         return self.cholqr(v_col)
 
     # ---- Rayleigh-Ritz + residuals ------------------------------------------------------------
-    def rayleigh_ritz(self, q_col, row_buf, fused_residuals: bool = False):
-        """rayleigh_ritz.py:98-143 distributed; returns (lam, v_col, lambda_min_m, residuals or None).
-        fused_residuals: H V = S T w / |Q w| from T = S H Q (rows R_I), no second H product."""
+    def rayleigh_ritz(self, q_col, row_buf, fused_residuals: bool = False, variant: str = "auto", it: int = 0,
+                      ledger: PhaseLedger | None = None):
+        """rayleigh_ritz.py:98-179 distributed, with the variant policy of solver.py:162-181.
+        Returns (lam, v_col, lambda_min_m, residuals or None, variant used, backup fallback taken).
+        One T = S H Q serves both projections: its halves give Q^H S H Q = G_top + G_bot (hermitian W,
+        backup G0) and Q^H H Q = G_top - G_bot (backup W), so a fallback costs no second H product.
+        fused_residuals: H V = S T y / |Q y| from T (rows R_I), no further H product."""
         k = q_col.shape[0]
+        n, nr = 2 * self.g.m, self.g.nr
         st = _Steps("rr", self.g.rank)
         t_row = row_buf[:k]
         self.forward(q_col, t_row, low_sign=-1.0)  # T = S H Q (rows R_I)
         st.mark("T = S H Q", k)
         q_full = self.assemble_from_col(q_col)
         st.mark("allgather Q", k)
-        w = self.ops.gram(self.row_rows(q_full), t_row)
-        self.c.sum_col(w)
+        q_rows = self.row_rows(q_full)
+        gtb = self.torch.stack([self.ops.gram(q_rows[:, :nr], t_row[:, :nr]),
+                                self.ops.gram(q_rows[:, nr:], t_row[:, nr:])])
+        self.c.sum_col(gtb)
         g2 = self.ops.gram(q_col[:, self.g.nc:], q_col[:, self.g.nc:])
         self.c.sum_row(g2)
-        st.mark("W, Q2^H Q2 + allreduce", k)
-        lam, wvec, lmm = self.ops.rr_pencil(w, g2)
+        st.mark("Q^H T halves, Q2^H Q2 + allreduce", k)
+        used, fallback, lam = "hermitian", False, None
+        if ledger is not None:
+            ledger.add_flops("rr", 8.0 * n * n * k)  # apply_h inside RR (hamiltonian.py:148-150)
+        if variant != "backup":
+            try:
+                lam, wvec, lmm = self.ops.rr_pencil(gtb[0] + gtb[1], g2.clone())
+                if ledger is not None:
+                    ledger.add_flops("rr", 8.0 * n * n * k + 12.0 * n * k * k + 16.0 * k**3)
+            except HermitianRqError as exc:
+                if variant == "hermitian":
+                    raise NumericalError(f"hermitian projection failed at iteration {it} with fallback "
+                                         f"disabled: {exc}") from exc
+                logger.warning("iteration %d: switching to backup projection (%s)", it, exc)
+                fallback = True
+                if ledger is not None:  # the reference's build_backup_rq applies H again
+                    ledger.add_flops("rr", 8.0 * n * n * k)
+        if lam is None:
+            used = "backup"
+            lam, wvec, lmm = self.ops.rr_backup_pencil(gtb[0] + gtb[1], gtb[0] - gtb[1], g2)
+            if ledger is not None:
+                ledger.add_flops("rr", 8.0 * n * n * k + 20.0 * n * k * k + 30.0 * k**3)
         st.mark("pencil", k)
         v = self.ops.nn(q_col, wvec)
         n2 = self.ops.colnorm2(v)
@@ -534,14 +574,14 @@ class DistSolver:
         if fused_residuals:
             torch = self.torch
             u_row = self.ops.nn(t_row, wvec)
-            vq_row = self.ops.nn(self.row_rows(q_full), wvec)
+            vq_row = self.ops.nn(q_rows, wvec)
             ones = torch.ones(k, dtype=torch.float64, device=v.device)
             lam_d = torch.as_tensor(np.ascontiguousarray(lam), dtype=torch.float64, device=v.device)
             r2 = self.ops.resid_partial(u_row, vq_row, self.g.nr, ones, lam_d)
             self.c.sum_col(r2)
             res = np.sqrt(r2.cpu().numpy() / n2.cpu().numpy())
             st.mark("residuals from S T w", k)
-        return lam, v, lmm, res
+        return lam, v, lmm, res, used, fallback
 
     def residuals(self, v_col, lam, row_buf) -> np.ndarray:
         k = v_col.shape[0]
@@ -623,8 +663,6 @@ class DistSolver:
         g = self.g
         n, nevex, nev, tol = 2 * g.m, cfg.nevex, cfg.nev, cfg.tol
         cfg.validate(n)
-        if cfg.rr_variant == "backup":
-            raise NumericalError("the backup projection is not distributed yet (rr_variant='backup')")
         ledger = PhaseLedger()
         with ledger.timing("lanczos"):
             bounds = self.lanczos(nevex, cfg.lanczos_steps, rng.substream(cfg.seed, TAG_LANCZOS), ledger)
@@ -633,7 +671,7 @@ class DistSolver:
         row_buf = self.ops.empty(nevex, 2 * g.nr)
         locked = self.ops.empty(nev, 2 * g.nc)
         nlock, lvals, lres, trace = 0, [], [], []
-        converged, it_used, current = False, 0, bounds
+        converged, it_used, current, backups = False, 0, bounds, 0
         lam = res = act = None
         for it in range(1, cfg.maxiter + 1):
             it_used = it
@@ -651,12 +689,9 @@ class DistSolver:
             from .solver import fused_residuals_for
 
             with ledger.timing("rr"):
-                try:
-                    lam, vecs, lmm, fres = self.rayleigh_ritz(v, row_buf, fused_residuals_for(cfg))
-                except HermitianRqError as exc:
-                    raise NumericalError(f"hermitian projection failed at iteration {it} (distributed backup "
-                                         f"projection not available): {exc}") from exc
-            ledger.add_flops("rr", 8.0 * n * n * k + 8.0 * n * n * k + 12.0 * n * k * k + 16.0 * k**3)
+                lam, vecs, lmm, fres, variant, fell_back = self.rayleigh_ritz(
+                    v, row_buf, fused_residuals_for(cfg), cfg.rr_variant, it, ledger)
+            backups += int(fell_back)
             with ledger.timing("residuals"):
                 res = fres if fres is not None else self.residuals(vecs, lam, row_buf)
             ledger.add_flops("residuals", 8.0 * n * n * k)
@@ -671,7 +706,7 @@ class DistSolver:
             unl = res[act]
             trace.append(TraceRecord(it=it, locked=nlock, k=k, max_res=float(res.max()),
                                      min_res_unlocked=float(unl.min()) if unl.size else 0.0,
-                                     mu_nevex=current.mu_nevex, variant="hermitian", lambda_min_m=lmm,
+                                     mu_nevex=current.mu_nevex, variant=variant, lambda_min_m=lmm,
                                      flops=ledger.total_flops() - before))
             if nlock >= nev:
                 converged = True
@@ -693,7 +728,7 @@ class DistSolver:
         order = np.argsort(vals, kind="stable")[:nev]
         full = self.assemble_from_col(blocks[torch.as_tensor(order, device=blocks.device)].contiguous())
         return SolveResult(lambdas=vals[order], v=full, residual_norms=resid[order], iterations_used=it_used,
-                           converged=converged, trace=trace, bounds=bounds, ledger=ledger, backup_events=0)
+                           converged=converged, trace=trace, bounds=bounds, ledger=ledger, backup_events=backups)
 
 
 def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):

@@ -59,6 +59,20 @@ class TorchOps:
             rdiag.copy_(torch.diagonal(r).abs())
         return torch.linalg.inv(r).T.contiguous(), 0
 
+    def rr_backup_pencil(self, g0, w, g2):
+        """rayleigh_ritz.py:160-175 on the summed k x k partials (storage = transposes)."""
+        k = w.shape[0]
+        mm = torch.eye(k, dtype=w.dtype) - 2 * g2.T
+        mm = (mm + mm.conj().T) / 2
+        lmm = float(torch.linalg.eigvalsh(mm).abs().min())
+        d = torch.real(torch.diagonal(mm)).clone()
+        d[d.abs() <= 1e-12] = 1.0
+        off = mm - torch.diag(torch.diagonal(mm))
+        g = (g0.T - off @ w.T) / d[:, None]
+        vals, y = np.linalg.eig(g.numpy())
+        order = np.argsort(vals.real, kind="stable")
+        return vals.real[order].copy(), torch.from_numpy(y[:, order]).T.contiguous(), lmm
+
     def rr_pencil(self, w, g2):
         from paper_2601_10557_b200.errors import HermitianRqError
 

@@ -41,12 +41,15 @@ def _worker(rank, world, port, key, pq, out):
     res = solve_distributed((a, b), SolverConfig(**kw), device=torch.device("cpu"), grid=grid, ops=TorchOps())
     if rank == 0:
         np.savez(out, lambdas=res.lambdas, v=res.v.numpy(), res=res.residual_norms, iters=res.iterations_used,
-                 converged=res.converged, locked=[t.locked for t in res.trace], k=[t.k for t in res.trace])
+                 converged=res.converged, locked=[t.locked for t in res.trace], k=[t.k for t in res.trace],
+                 variant=[t.variant for t in res.trace], flops=[t.flops for t in res.trace],
+                 backups=res.backup_events)
     dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world,pq,key", [(1, None, "m48_s12"), (2, None, "m48_s12"), (4, None, "m64_s21"),
-                                          (2, (2, 1), "m24_s100"), (4, (1, 4), "m32_s14"), (8, None, "m64_s40")])
+                                          (2, (2, 1), "m24_s100"), (4, (1, 4), "m32_s14"), (8, None, "m64_s40"),
+                                          (2, None, "m32_s6"), (4, None, "m32_s6")])
 def test_distributed_solve_matches_reference(tmp_path, world, pq, key):
     out = str(tmp_path / "r.npz")
     mp.spawn(_worker, args=(world, _port(), key, pq, out), nprocs=world, join=True)
@@ -56,6 +59,9 @@ def test_distributed_solve_matches_reference(tmp_path, world, pq, key):
     assert abs(int(r["iters"]) - int(g["iterations_used"])) <= 1
     if int(r["iters"]) == int(g["iterations_used"]):
         assert list(r["locked"]) == list(g["trace_locked"])
+        assert list(r["variant"]) == [str(x) for x in g["trace_variant"]]
+        np.testing.assert_allclose(r["flops"], g["trace_flops"], rtol=1e-12)
+    assert int(r["backups"]) == int(g["backup_events"])
     rel = np.abs(r["lambdas"] - g["lambdas"]) / np.abs(g["lambdas"])
     assert rel.max() <= 1e-10
     ov = np.abs(np.einsum("ij,ij->j", g["v"].conj(), r["v"]))

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-@pytest.mark.parametrize("key", ["m48_s12", "m64_s21", "m24_s100", "m32_s14"])
+@pytest.mark.parametrize("key", ["m48_s12", "m64_s21", "m24_s100", "m32_s14", "m32_s6"])
 def test_dist_path_single_gpu_matches_reference(key):
     from paper_2601_10557_b200 import SolverConfig
     from paper_2601_10557_b200.dist import solve_distributed
@@ -23,6 +23,9 @@ def test_dist_path_single_gpu_matches_reference(key):
     g = golden(f"solve_{key}.npz")
     assert res.converged == bool(g["converged"])
     assert abs(res.iterations_used - int(g["iterations_used"])) <= 1
+    assert res.backup_events == int(g["backup_events"])
+    if res.iterations_used == int(g["iterations_used"]):
+        assert [t.variant for t in res.trace] == [str(x) for x in g["trace_variant"]]
     rel = np.abs(res.lambdas - g["lambdas"]) / np.abs(g["lambdas"])
     assert rel.max() <= 1e-10
     v = res.v.T.contiguous().cpu().numpy().T

@@ -28,7 +28,7 @@ def main():
     dev = torch.device("cuda", local)
     fails = 0
     cases = json.loads((GOLDEN / "meta.json").read_text())["cases"]
-    for key in ["m48_s12", "m64_s21", "m24_s100", "m32_s14", "m48_s13"]:
+    for key in ["m48_s12", "m64_s21", "m24_s100", "m32_s14", "m48_s13", "m32_s6"]:
         m, seed = (int(t[1:]) for t in key.split("_"))
         a, b = golden_ham(m, seed)
         res = solve_distributed((a, b), SolverConfig(**cases[key]), device=dev)
