@@ -66,9 +66,11 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags);
 /* ---- Hamiltonian operator ------------------------------------------------ */
 /* y = H x  (low_sign = +1)  or  y = S H x  (low_sign = -1)
  * replaces apply_h hamiltonian.py:132-151 (and apply_s(apply_h(.)) at
- * rayleigh_ritz.py:112).  x, y: n x k (n = 2m), must not alias.            */
-int bse_apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_x, int64_t ldx, void* d_y,
-                int64_t ldy, int64_t k, double low_sign);
+ * rayleigh_ritz.py:112).  x, y: n x k (n = 2m), must not alias.
+ * d_sd (nullable): the (Pr + Pi, Pr - Pi) planes of d_ab (bse_make_sum_planes); when given, the
+ * product runs on the kernel selected by bse_set_filter_algorithm (3M), else on the 4M kernel. */
+int bse_apply_h(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_x, int64_t ldx,
+                void* d_y, int64_t ldy, int64_t k, double low_sign);
 
 /* One Chebyshev step y_next = alpha (H y - c y) - beta y_prev, fused in the
  * GEMM epilogue (chebyshev.py:68-74).  y_next may alias y_prev, not y.    */
@@ -108,12 +110,14 @@ int bse_fix_phases(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq);
  * *h_lam_min_m = |lambda|_min(Q*SQ).  BSE_EHERMITIAN_RQ when Q*SQ is
  * singular (< 1e-8), Q*SHQ is not positive definite, or theta ~ 0.
  * h_res (nullable): residual norms ||H v - lam v|| from the RR intermediate,
- * H V = S (S H Q) w / |Q w| (rayleigh_ritz.py:182-190 without a second H product). */
-int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
-                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m, double* h_res);
-/* Non-hermitian backup projection (Alg. 3, rayleigh_ritz.py:146-179). */
-int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
-                  double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m);
+ * H V = S (S H Q) w / |Q w| (rayleigh_ritz.py:182-190 without a second H product).
+ * d_sd (nullable): sum planes of d_ab, as for bse_apply_h (the T = S H Q product). */
+int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_q,
+                     int64_t ldq, int64_t k, double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m,
+                     double* h_res);
+/* Non-hermitian backup projection (Alg. 3, rayleigh_ritz.py:146-179); d_sd as above. */
+int bse_rr_backup(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_q,
+                  int64_t ldq, int64_t k, double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m);
 
 /* ---- Lanczos bounds (lanczos.py:53-88) ------------------------------------ */
 /* One S-inner-product Lanczos sweep from host start vector h_start (n):

@@ -54,7 +54,7 @@ _SIGS = {
     "bse_set_hamiltonian_flags": (C.c_int, [_vp, C.c_uint]),
     "bse_last_error": (C.c_char_p, [_vp]),
     "bse_launch_count": (_i64, [_vp]),
-    "bse_apply_h": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _dbl]),
+    "bse_apply_h": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _i64, _dbl]),
     "bse_filter_step": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _dbl]),
     "bse_chebyshev_filter": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
     "bse_make_sum_planes": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
@@ -62,8 +62,8 @@ _SIGS = {
     "bse_s_orthonormalize": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
     "bse_cholqr": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _ip]),
     "bse_fix_phases": (C.c_int, [_vp, _vp, _i64, _i64, _i64]),
-    "bse_rr_hermitian": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp, _dp]),
-    "bse_rr_backup": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
+    "bse_rr_hermitian": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp, _dp]),
+    "bse_rr_backup": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _vp, _i64, _dp]),
     "bse_lanczos_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _dp, _dp, _ip]),
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),

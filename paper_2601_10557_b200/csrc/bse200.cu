@@ -366,18 +366,26 @@ bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zva
   return a;
 }
 
+void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a);
+
+// y = H x / S H x; with the sum planes d_sd the product takes the filter kernel (3M), else 4M
 void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, zval* y, int64_t ldy,
-             int64_t k, double low_sign) {
+             int64_t k, double low_sign, const void* d_sd = nullptr) {
   if (k == 0 || m == 0) return;
   bse::HopArgs a = hop_args_single(d_ab, lda, m, x, ldx, k);
   a.y1 = y;
   a.y2 = y + m;
   a.ldy = ldy;
   a.low_sign = low_sign;
-  if (k == 1)
+  if (k == 1) {
     launch_gemv(ctx, a);
-  else
+  } else if (d_sd) {
+    a.sa = static_cast<const zval*>(d_sd);
+    a.sb = a.sa + m * lda;
+    launch_filter_hop(ctx, a);
+  } else {
     launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+  }
 }
 
 void filter_step(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const zval* y,
@@ -858,11 +866,11 @@ int bse_set_stream(bse_ctx* ctx, void* stream) {
 const char* bse_last_error(const bse_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int64_t bse_launch_count(const bse_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-int bse_apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_x, int64_t ldx, void* d_y,
-                int64_t ldy, int64_t k, double low_sign) {
+int bse_apply_h(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_x, int64_t ldx,
+                void* d_y, int64_t ldy, int64_t k, double low_sign) {
   return guarded(ctx, [&] {
     if (m < 0 || k < 0 || lda < m || ldx < 2 * m || ldy < 2 * m) throw BseError(BSE_EVALIDATION, "bad shapes");
-    apply_h(ctx, d_ab, lda, m, static_cast<const zval*>(d_x), ldx, static_cast<zval*>(d_y), ldy, k, low_sign);
+    apply_h(ctx, d_ab, lda, m, static_cast<const zval*>(d_x), ldx, static_cast<zval*>(d_y), ldy, k, low_sign, d_sd);
   });
 }
 
@@ -1016,8 +1024,9 @@ int bse_s_orthonormalize(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t 
   });
 }
 
-int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
-                     double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m, double* h_res) {
+int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_q,
+                     int64_t ldq, int64_t k, double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m,
+                     double* h_res) {
   return guarded(ctx, [&] {
     if (k == 0) return;
     const int64_t n = 2 * m;
@@ -1039,7 +1048,7 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, con
     zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
     StepTimer tm(ctx, "rr_hermitian");
     // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T ; Q2^H Q2
-    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0);
+    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0, d_sd);
     tm.mark("T = S H Q", k);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
     zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
@@ -1142,8 +1151,8 @@ void backup_pencil(bse_ctx* ctx, zval* g, const zval* w, zval* g2, int64_t k, do
   check_launch(ctx);
 }
 
-int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_q, int64_t ldq, int64_t k,
-                  double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
+int bse_rr_backup(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_q,
+                  int64_t ldq, int64_t k, double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
   return guarded(ctx, [&] {
     if (k == 0) return;
     const int64_t n = 2 * m;
@@ -1160,7 +1169,7 @@ int bse_rr_backup(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const 
     double* d_nrm = sc.take<double>(k);
     zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
     // rayleigh_ritz.py:160-168
-    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, 1.0);
+    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, 1.0, d_sd);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
     zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
     // g0 = Q^H (S T) = Q1^H T1 - Q2^H T2

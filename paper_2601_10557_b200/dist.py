@@ -532,7 +532,7 @@ class DistSolver:
         n, nr = 2 * self.g.m, self.g.nr
         st = _Steps("rr", self.g.rank)
         t_row = row_buf[:k]
-        self.forward(q_col, t_row, low_sign=-1.0)  # T = S H Q (rows R_I)
+        self.forward(q_col, t_row, low_sign=-1.0, filter=True)  # T = S H Q (rows R_I), filter kernel
         st.mark("T = S H Q", k)
         q_full = self.assemble_from_col(q_col)
         st.mark("allgather Q", k)

@@ -306,8 +306,8 @@ def _apply(ham: BseHamiltonian, x, low_sign: float, ledger, phase):
     y = colmajor_empty(ham.n, k, dev)
     ctx = _lib.Context.get(dev.index)
     ab = ham.device_blocks(dev)
-    ctx.call("bse_apply_h", _lib.dptr(ab), ld_of(ab), ham.m, _lib.dptr(xd), ld_of(xd), _lib.dptr(y), ld_of(y), k,
-             float(low_sign))
+    ctx.call("bse_apply_h", _lib.dptr(ab), None, ld_of(ab), ham.m, _lib.dptr(xd), ld_of(xd), _lib.dptr(y), ld_of(y),
+             k, float(low_sign))
     if ledger is not None:
         ledger.add_flops(phase, 8.0 * ham.n * ham.n * k)
     out = _host_like(x, y)

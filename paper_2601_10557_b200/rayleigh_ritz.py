@@ -60,11 +60,13 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     vout = colmajor_empty(n, k, q.device)
     lmm = ctypes.c_double(float("nan"))
     ab = ham.device_blocks(q.device)
+    # the T = (S) H Q product runs on the filter's kernel (3M) when the sum planes are in use
+    sd = _lib.dptr(ham.device_sum_planes(q.device)) if _lib.uses_sum_planes() else None
     ctx = _lib.Context.get(q.device.index)
     res = np.zeros(k) if fused_residuals else None
     extra = (_lib.hptr(res) if fused_residuals else None,) if entry == "bse_rr_hermitian" else ()
     try:
-        ctx.call(entry, _lib.dptr(ab), ld_of(ab), ham.m, _lib.dptr(q), ld_of(q), k, _lib.hptr(lam), _lib.dptr(vout),
+        ctx.call(entry, _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(q), ld_of(q), k, _lib.hptr(lam), _lib.dptr(vout),
                  ld_of(vout), ctypes.byref(lmm), *extra)
     finally:
         if ledger is not None:

@@ -48,7 +48,7 @@ def main(m, k, l):
     ctx = _lib.Context.get(0)
     ab = ham.device_blocks(dev)
     t = colmajor_empty(n, k, dev)
-    print(f"  apply_sh:                 {wall(lambda: ctx.call('bse_apply_h', _lib.dptr(ab), ld_of(ab), m, _lib.dptr(v), n, _lib.dptr(t), n, k, -1.0)):.1f} ms")
+    print(f"  apply_sh:                 {wall(lambda: ctx.call('bse_apply_h', _lib.dptr(ab), None, ld_of(ab), m, _lib.dptr(v), n, _lib.dptr(t), n, k, -1.0)):.1f} ms")
     w = torch.empty((k, k), dtype=torch.complex128, device=dev)
     g2 = torch.empty((k, k), dtype=torch.complex128, device=dev)
     wv = torch.empty((k, k), dtype=torch.complex128, device=dev)
