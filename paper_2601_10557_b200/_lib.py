@@ -101,7 +101,8 @@ _lib = None
 _lock = threading.Lock()
 # complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
 _ALGOS = {"4m": 4, "3m": 72, "3m-sync": 65, "3m-64x16": 6, "3m-onthefly": 3, "3m-xsum": 7, "3m-ahead": 8,
-          "3m-smem": 9, "3m-mb32": 67, "3m-mb3": 68, "3m-mb64x16": 69, "3m-mb128": 75}
+          "3m-smem": 9, "3m-mb32": 67, "3m-mb3": 68, "3m-mb64x16": 69, "3m-mb128": 75,
+          "3m-swz": 76, "3m-swz5": 77}
 # default 3M (Gauss) with precomputed operand-sum planes: 25% fewer DMMA, parity-checked at C1
 # (tests/test_gpu_parity.py); BSE200_FILTER=4m restores the 4M split
 _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "3m").lower()]
@@ -138,7 +139,7 @@ def filter_precision() -> str:
 
 
 def uses_sum_planes() -> bool:
-    return _FILTER_CM in (6, 7, 8, 81) or 61 <= _FILTER_CM <= 75
+    return _FILTER_CM in (6, 7, 8, 81) or 61 <= _FILTER_CM <= 77
 
 
 def load() -> C.CDLL:

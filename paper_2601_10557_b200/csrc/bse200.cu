@@ -224,17 +224,18 @@ void launch_hop(bse_ctx* ctx, const bse::HopArgs& a_in) {
   check_launch(ctx);
 }
 
-template <class C>
+template <class C, bool SW = false>
 void launch_hop_mb(bse_ctx* ctx, const bse::HopArgs& a_in) {
   bse::HopArgs a = a_in;
   a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
+  constexpr size_t smem = bse::MbLayout<C, SW>::SMEM;
   static bool configured = false;
   if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_mb_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_mb_kernel<C, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
-  bse::hop3m_mb_kernel<C><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
+  bse::hop3m_mb_kernel<C, SW><<<grid, C::THREADS, smem, ctx->stream>>>(a);
   check_launch(ctx);
 }
 
@@ -264,6 +265,7 @@ using Hop3MM_12 = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 1>;
 using Hop3MM_13 = bse::HopCfg<96, 16, 8, 6, 1, 3, 2, 1>;
 using Hop3MM_14 = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 using Hop3MM_15 = bse::HopCfg<128, 16, 8, 4, 1, 4, 1, 1>;
+using Hop3MM_16 = bse::HopCfg<64, 16, 8, 4, 1, 5, 2, 1>;  // swizzled X tile (codes 76-77)
 // 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
 using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
 // 3M with P sums from planes and X sums computed in shared memory one stage ahead (code 8, 81)
@@ -279,7 +281,7 @@ using Hop3MB_2 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 2, 2>;
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
   if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
-  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 75)) && (!a.sa || !a.sb))
+  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 77)) && (!a.sa || !a.sb))
     code = 3;  // no P sum planes
   switch (code) {
     case 9: launch_hop<Hop3MB, bse::HOP_AXPBY, 9>(ctx, a); break;
@@ -304,6 +306,8 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
     case 73: launch_hop_mb<Hop3MM_13>(ctx, a); break;
     case 74: launch_hop_mb<Hop3MM_14>(ctx, a); break;
     case 75: launch_hop_mb<Hop3MM_15>(ctx, a); break;
+    case 76: launch_hop_mb<Hop3MM_12, true>(ctx, a); break;
+    case 77: launch_hop_mb<Hop3MM_16, true>(ctx, a); break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
@@ -849,7 +853,7 @@ int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
                     complex_mults == 8 || complex_mults == 81 || complex_mults == 9 || complex_mults == 91 ||
                     complex_mults == 92 ||
                     (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
-                    (complex_mults >= 61 && complex_mults <= 75);
+                    (complex_mults >= 61 && complex_mults <= 77);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
   });

@@ -40,9 +40,24 @@ __device__ __forceinline__ void mbar_wait_cta(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Stage layout.  SW == false: hop_kernel's padded X tile (LDX = BK + 4).  SW == true: unpadded
+// X rows of BK = 8 complex with the two 4-wide K halves swapped on odd columns (k ^ 4), which keeps
+// every 8-lane phase of the fragment LDS.128 on 32 distinct banks and saves a third of the X tile
+// (room for one more stage at 2 CTAs/SM).
+template <class C, bool SW>
+struct MbLayout {
+  static_assert(!SW || C::BK == 8, "swizzled X tile assumes BK == 8");
+  static constexpr int LDX = SW ? C::BK : C::LDX;
+  static constexpr int X_ELEMS = C::BN * LDX;
+  static constexpr int STAGE_ELEMS = C::P_ELEMS + C::SD_ELEMS + 2 * X_ELEMS;
+  static constexpr size_t SMEM = size_t(C::STAGES) * STAGE_ELEMS * sizeof(zval);
+  __device__ __forceinline__ static int xk(int col, int k) { return SW ? (k ^ ((col & 1) << 2)) : k; }
+};
+
 // Per-thread copy slots of one stage: NP (P and sum-plane) slots and NX (X) slots.
-template <class C>
+template <class C, bool SW>
 struct MbLoader {
+  using L = MbLayout<C, SW>;
   static constexpr int NP = (C::BK * C::BM + C::THREADS - 1) / C::THREADS;
   static constexpr int NX = (2 * C::BN * C::BK + C::THREADS - 1) / C::THREADS;
   static constexpr bool X_ALL = (2 * C::BN * C::BK) % C::THREADS == 0;  // else the last X slot is partial
@@ -79,7 +94,7 @@ struct MbLoader {
       const int kk = id % C::BK, cc = (id / C::BK) % C::BN, which = id / (C::BK * C::BN);
       xcol[r] = c0 + cc < a.k;
       xk[r] = kk;
-      x_off[r] = which * (C::X_ELEMS) + cc * C::LDX + kk;
+      x_off[r] = which * L::X_ELEMS + cc * L::LDX + L::xk(cc, kk);
       x[r] = (which ? XB : XA) + (int64_t)(xcol[r] ? c0 + cc : 0) * a.ldx + kk;
     }
   }
@@ -107,8 +122,9 @@ struct MbLoader {
   }
 };
 
-template <class C>
+template <class C, bool SW = false>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const HopArgs a) {
+  using L = MbLayout<C, SW>;
   static_assert(C::PS == 1 && C::XS == 0, "hop3m_mb_kernel: 3M with P-side sum planes only");
   constexpr int CM = 6;
   constexpr int NWARPS = C::THREADS / 32;
@@ -134,12 +150,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
   }
   __syncthreads();
 
-  MbLoader<C> ld;
+  MbLoader<C, SW> ld;
   ld.init(a, 0, i0, c0);
   int lkt = 0;  // next stage to load
   auto load_next = [&](int buf) {
     if (lkt == nkt_part) ld.init(a, 1, i0, c0);
-    ld.issue(smem + buf * C::STAGE_ELEMS, a, (lkt >= nkt_part ? lkt - nkt_part : lkt) * C::BK);
+    ld.issue(smem + buf * L::STAGE_ELEMS, a, (lkt >= nkt_part ? lkt - nkt_part : lkt) * C::BK);
     cp_async_arrive_noinc(&full[buf]);
     ++lkt;
   };
@@ -159,10 +175,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
   for (int kt = 0; kt < nkt; ++kt) {
     const int s = kt % C::STAGES;
     mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
-    const zval* Ps = smem + s * C::STAGE_ELEMS;
+    const zval* Ps = smem + s * L::STAGE_ELEMS;
     const zval* SDs = Ps + C::P_ELEMS;
     const zval* Xas = SDs + C::SD_ELEMS;
-    const zval* Xbs = Xas + C::X_ELEMS;
+    const zval* Xbs = Xas + L::X_ELEMS;
 #pragma unroll
     for (int ks = 0; ks < C::BK / 4; ++ks) {
       zval pf[C::WM], sdf[C::WM], xa[C::WN], xb[C::WN];
@@ -174,8 +190,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
 #pragma unroll
       for (int j = 0; j < C::WN; ++j) {
         const int col = wn * (8 * C::WN) + j * 8 + g;
-        xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
-        xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
+        xa[j] = lds128(Xas + col * L::LDX + L::xk(col, ks * 4 + t));
+        xb[j] = lds128(Xbs + col * L::LDX + L::xk(col, ks * 4 + t));
       }
       double xas[C::WN], xbs[C::WN];
 #pragma unroll

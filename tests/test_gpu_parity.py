@@ -288,7 +288,7 @@ def test_c1_parity(bse, c1_instance):
 
 
 @pytest.mark.parametrize("algo", ["3m", "3m-sync", "3m-onthefly", "3m-xsum", "3m-ahead", "3m-smem", "3m-mb32", "3m-mb3",
-                                  "3m-mb64x16", "3m-mb128", "4m"])
+                                  "3m-mb64x16", "3m-mb128", "3m-swz", "3m-swz5", "4m"])
 def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
