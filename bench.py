@@ -408,7 +408,7 @@ def run_ours(args, world, rank, local):
                          "frac": (achieved / peak) if achieved else None, "traffic": ncu_traffic(algo)[0],
                          "traffic_source": ncu_traffic(algo)[1],
                          "kernel": ("bse::c64::step_kernel (tcgen05 3xTF32 complex64 filter step)" if algo.startswith("c64")
-                                    else "bse::hop3m_mb_kernel (fused H-operator 3M DMMA GEMM, mbarrier pipeline, Chebyshev epilogue)"
+                                    else "bse::hop3m_tma_kernel (fused H-operator 3M DMMA GEMM, TMA-fed by a producer warp, mbarrier rings, Chebyshev epilogue)"
                                     if algo == "3m" else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
                          "peak_source": peak_src,
                          "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model, BASELINE.md §3.5) "

@@ -224,6 +224,57 @@ void launch_hop(bse_ctx* ctx, const bse::HopArgs& a_in) {
   check_launch(ctx);
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p) throw BseError(BSE_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D FP64 tensor map, no swizzle (the box rows carry their own padding, hop_mb.cuh)
+CUtensorMap map2d_f64(const void* base, uint64_t d0, uint64_t d1, uint64_t stride1_bytes, uint32_t b0, uint32_t b1) {
+  CUtensorMap map;
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {stride1_bytes};
+  cuuint32_t box[2] = {b0, b1};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw BseError(BSE_ECUDA, "cuTensorMapEncodeTiled (f64) failed (" + std::to_string((int)r) + ")");
+  return map;
+}
+
+template <class C, bool PW = false>
+void launch_hop_tma(bse_ctx* ctx, const bse::HopArgs& a_in) {
+  bse::HopArgs a = a_in;
+  a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
+  constexpr size_t smem = bse::TmaLayout<C>::SMEM;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_tma_kernel<C, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  bse::HopMaps mp;
+  const uint64_t pr = 2 * (uint64_t)a.mr, xr = 2 * (uint64_t)a.kc;
+  const zval* pp[2] = {a.pa, a.pb};
+  const zval* ss[2] = {a.sa, a.sb};
+  const zval* xx[2] = {a.x1, a.x2};
+  for (int q = 0; q < 2; ++q) {
+    mp.p[q] = map2d_f64(pp[q], pr, a.kc, a.lda * 16, 2 * (C::BM + 2), C::BK);
+    mp.sd[q] = map2d_f64(ss[q], pr, a.kc, a.lda * 16, 2 * (C::BM + 2), C::BK);
+    mp.x[q] = map2d_f64(xx[q], xr, a.k, a.ldx * 16, 2 * (C::BK + 4), C::BN);
+  }
+  dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
+  bse::hop3m_tma_kernel<C, PW><<<grid, C::THREADS + (PW ? 32 : 0), smem, ctx->stream>>>(a, mp);
+  check_launch(ctx);
+}
+
 template <class C, bool SW = false>
 void launch_hop_mb(bse_ctx* ctx, const bse::HopArgs& a_in) {
   bse::HopArgs a = a_in;
@@ -266,6 +317,8 @@ using Hop3MM_13 = bse::HopCfg<96, 16, 8, 6, 1, 3, 2, 1>;
 using Hop3MM_14 = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 using Hop3MM_15 = bse::HopCfg<128, 16, 8, 4, 1, 4, 1, 1>;
 using Hop3MM_16 = bse::HopCfg<64, 16, 8, 4, 1, 5, 2, 1>;  // swizzled X tile (codes 76-77)
+using Hop3MM_18 = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
+using Hop3MM_19 = bse::HopCfg<64, 16, 8, 4, 1, 3, 2, 1>;
 // 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
 using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
 // 3M with P sums from planes and X sums computed in shared memory one stage ahead (code 8, 81)
@@ -281,7 +334,7 @@ using Hop3MB_2 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 2, 2>;
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
   if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
-  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 77)) && (!a.sa || !a.sb))
+  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 79) || (code >= 82 && code <= 88 && code != 85)) && (!a.sa || !a.sb))
     code = 3;  // no P sum planes
   switch (code) {
     case 9: launch_hop<Hop3MB, bse::HOP_AXPBY, 9>(ctx, a); break;
@@ -308,6 +361,22 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
     case 75: launch_hop_mb<Hop3MM_15>(ctx, a); break;
     case 76: launch_hop_mb<Hop3MM_12, true>(ctx, a); break;
     case 77: launch_hop_mb<Hop3MM_16, true>(ctx, a); break;
+    case 78: launch_hop_tma<Hop3MM_12>(ctx, a); break;
+    case 79: launch_hop_tma<Hop3MM_9>(ctx, a); break;
+    case 82: launch_hop_tma<Hop3MM_12, true>(ctx, a); break;
+    case 83: launch_hop_tma<Hop3MM_9, true>(ctx, a); break;
+    case 84: launch_hop_tma<Hop3MM_16, true>(ctx, a); break;
+    case 86: launch_hop_tma<Hop3MM_18, true>(ctx, a); break;
+    case 87: launch_hop_tma<Hop3MM_19, true>(ctx, a); break;
+    // default 3M: TMA-fed, producer warp; 64 x 32 CTA (8 consumer warps, 6 stages) for wide blocks,
+    // 64 x 16 (4 warps, 2 CTAs/SM) below 512 columns where the wider tile underfills the GPU.
+    // Both accumulate every output in the same K order: the choice never changes a bit.
+    case 88:
+      if (a.k >= 512)
+        launch_hop_tma<Hop3MM_18, true>(ctx, a);
+      else
+        launch_hop_tma<Hop3MM_12, true>(ctx, a);
+      break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
     case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
@@ -731,18 +800,6 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
 // ---------------------------------------------------------------------------------------------
 // complex64 filter on tcgen05 (c64.cuh): TMA tensor maps and the step driver
 // ---------------------------------------------------------------------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (!p) throw BseError(BSE_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 // 3-D fp32 tensor map with a 64-byte-swizzled box (b0 x b1 x b2), strides in bytes
 CUtensorMap map3d(const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1, uint64_t s2, uint32_t b0,
                   uint32_t b1, uint32_t b2) {
@@ -853,7 +910,8 @@ int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
                     complex_mults == 8 || complex_mults == 81 || complex_mults == 9 || complex_mults == 91 ||
                     complex_mults == 92 ||
                     (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
-                    (complex_mults >= 61 && complex_mults <= 77);
+                    (complex_mults >= 61 && complex_mults <= 79) ||
+                    (complex_mults >= 82 && complex_mults <= 88 && complex_mults != 85);
     if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
     ctx->filter_cm = complex_mults;
   });

@@ -14,7 +14,10 @@
 // Semantics are those of hop_kernel<C, HOP_AXPBY, 6> (hop.cuh): U = P Xa, L' = conj(P) Xb with
 // Gauss's 3M split on the precomputed (Pr + Pi, Pr - Pi) planes; same epilogue.
 #pragma once
+#include <cuda.h>
+
 #include "hop.cuh"
+#include "tc_common.cuh"
 
 namespace bse {
 
@@ -122,6 +125,46 @@ struct MbLoader {
   }
 };
 
+// the 3M DMMA work of one landed stage (identical arithmetic to hop_kernel CM == 6)
+template <class C, bool SW>
+__device__ __forceinline__ void mb_stage_mma(double (&acc)[6][C::WM][C::WN][2], const zval* Ps, const zval* SDs,
+                                             const zval* Xas, const zval* Xbs, int wm, int wn, int g, int t) {
+  using L = MbLayout<C, SW>;
+#pragma unroll
+  for (int ks = 0; ks < C::BK / 4; ++ks) {
+    zval pf[C::WM], sdf[C::WM], xa[C::WN], xb[C::WN];
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i) {
+      pf[i] = lds128(Ps + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
+      sdf[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
+    }
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j) {
+      const int col = wn * (8 * C::WN) + j * 8 + g;
+      xa[j] = lds128(Xas + col * L::LDX + L::xk(col, ks * 4 + t));
+      xb[j] = lds128(Xbs + col * L::LDX + L::xk(col, ks * 4 + t));
+    }
+    double xas[C::WN], xbs[C::WN];
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j) {
+      xas[j] = xa[j].re + xa[j].im;
+      xbs[j] = xb[j].re + xb[j].im;
+    }
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i) {
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j) {
+        dmma(acc[0][i][j], pf[i].re, xa[j].re);
+        dmma(acc[1][i][j], pf[i].im, xa[j].im);
+        dmma(acc[2][i][j], sdf[i].re, xas[j]);
+        dmma(acc[3][i][j], pf[i].re, xb[j].re);
+        dmma(acc[4][i][j], pf[i].im, xb[j].im);
+        dmma(acc[5][i][j], sdf[i].im, xbs[j]);
+      }
+    }
+  }
+}
+
 template <class C, bool SW = false>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const HopArgs a) {
   using L = MbLayout<C, SW>;
@@ -179,43 +222,131 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
     const zval* SDs = Ps + C::P_ELEMS;
     const zval* Xas = SDs + C::SD_ELEMS;
     const zval* Xbs = Xas + L::X_ELEMS;
-#pragma unroll
-    for (int ks = 0; ks < C::BK / 4; ++ks) {
-      zval pf[C::WM], sdf[C::WM], xa[C::WN], xb[C::WN];
-#pragma unroll
-      for (int i = 0; i < C::WM; ++i) {
-        pf[i] = lds128(Ps + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
-        sdf[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
-      }
-#pragma unroll
-      for (int j = 0; j < C::WN; ++j) {
-        const int col = wn * (8 * C::WN) + j * 8 + g;
-        xa[j] = lds128(Xas + col * L::LDX + L::xk(col, ks * 4 + t));
-        xb[j] = lds128(Xbs + col * L::LDX + L::xk(col, ks * 4 + t));
-      }
-      double xas[C::WN], xbs[C::WN];
-#pragma unroll
-      for (int j = 0; j < C::WN; ++j) {
-        xas[j] = xa[j].re + xa[j].im;
-        xbs[j] = xb[j].re + xb[j].im;
-      }
-#pragma unroll
-      for (int i = 0; i < C::WM; ++i) {
-#pragma unroll
-        for (int j = 0; j < C::WN; ++j) {
-          dmma(acc[0][i][j], pf[i].re, xa[j].re);
-          dmma(acc[1][i][j], pf[i].im, xa[j].im);
-          dmma(acc[2][i][j], sdf[i].re, xas[j]);
-          dmma(acc[3][i][j], pf[i].re, xb[j].re);
-          dmma(acc[4][i][j], pf[i].im, xb[j].im);
-          dmma(acc[5][i][j], sdf[i].im, xbs[j]);
-        }
-      }
-    }
+    mb_stage_mma<C, SW>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);
     if (lkt < nkt) {
       // the buffer of stage lkt last held stage lkt - STAGES == kt - 1: wait until every warp left it
+      const int b = lkt % C::STAGES;
+      if (kt >= 1) mbar_wait_cta(&empty[b], ((kt - 1) / C::STAGES) & 1);
+      load_next(b);
+    }
+  }
+  hop_epilogue_axpby<C, CM>(acc, a, i0, c0, wm, wn, g, t);
+}
+
+// ---------------------------------------------------------------------------------------------
+// TMA-fed variant.  The padded shared layouts above (LDP = BM + 2, LDX = BK + 4) are what make the
+// fragment LDS.128 conflict-free; a TMA box is written densely, so the boxes are made as wide as
+// the padded rows: P / sum-plane boxes of (BM + 2) complex x BK rows land with pitch LDP, X boxes
+// of (BK + 4) complex x BN columns land with pitch LDX (the extra rows / K values are neighbouring
+// data or TMA's zero fill, never read).  One elected thread issues 4 bulk-tensor copies per stage
+// against full[s] (arrive.expect_tx) instead of 8 cp.async per thread.
+struct HopMaps {
+  CUtensorMap p[2];   // [A | B] parts: (2 mr doubles) x kc, leading dim lda
+  CUtensorMap sd[2];  // their (Pr + Pi, Pr - Pi) planes
+  CUtensorMap x[2];   // x1, x2: (2 kc doubles) x k, leading dim ldx
+};
+
+template <class C>
+struct TmaLayout {
+  static_assert(C::PS == 1 && C::XS == 0, "TMA feed: 3M with P-side sum planes only");
+  static constexpr int P_BYTES = C::P_ELEMS * 16, X_BYTES = C::X_ELEMS * 16;
+  static constexpr int STAGE_BYTES = 2 * P_BYTES + 2 * X_BYTES;
+  static_assert(P_BYTES % 128 == 0 && X_BYTES % 128 == 0, "TMA destinations must stay 128-byte aligned");
+  static_assert(2 * (C::BM + 2) <= 256 && 2 * (C::BK + 4) <= 256 && C::BN <= 256 && C::BK <= 256,
+                "TMA box dimensions are limited to 256 elements");
+  static constexpr size_t SMEM = size_t(C::STAGES) * STAGE_BYTES + 128;  // + alignment slack
+};
+
+// PW == true: a dedicated producer warp (warp NWARPS) issues the copies, so no consumer warp ever
+// waits for the others; PW == false: thread 0 of the consumers does.
+template <class C, bool PW = false>
+__global__ void __launch_bounds__(C::THREADS + (PW ? 32 : 0), C::MINB)
+    hop3m_tma_kernel(const HopArgs a, const __grid_constant__ HopMaps maps) {
+  using T = TmaLayout<C>;
+  constexpr int CM = 6;
+  constexpr int NWARPS = C::THREADS / 32;  // consumer warps
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int c0 = blockIdx.x * C::BN;
+  const int i0 = blockIdx.y * C::BM;
+  const int nkt_part = (a.kc + C::BK - 1) / C::BK;
+  const int nkt = a.skip_b ? nkt_part : 2 * nkt_part;
+  const bool producer = PW ? threadIdx.x == C::THREADS : threadIdx.x == 0;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init_cta(&full[s], 1);
+      mbar_init_cta(&empty[s], NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    for (int q = 0; q < 2; ++q) {
+      tc::prefetch_tmap(&maps.p[q]);
+      tc::prefetch_tmap(&maps.sd[q]);
+      tc::prefetch_tmap(&maps.x[q]);
+    }
+  }
+  __syncthreads();
+
+  int lkt = 0;  // next stage to load (producer only)
+  auto load_next = [&](int buf) {
+    const int part = lkt >= nkt_part;
+    const int j0 = (lkt - part * nkt_part) * C::BK;
+    unsigned char* st = base + buf * T::STAGE_BYTES;
+    tc::mbar_arrive_expect_tx(&full[buf], T::STAGE_BYTES);
+    tc::tma_load_2d(st, &maps.p[part], &full[buf], 2 * i0, j0);
+    tc::tma_load_2d(st + T::P_BYTES, &maps.sd[part], &full[buf], 2 * i0, j0);
+    tc::tma_load_2d(st + 2 * T::P_BYTES, &maps.x[part], &full[buf], 2 * j0, c0);              // Xa
+    tc::tma_load_2d(st + 2 * T::P_BYTES + T::X_BYTES, &maps.x[1 - part], &full[buf], 2 * j0, c0);  // Xb
+    ++lkt;
+  };
+  if constexpr (PW) {
+    if (warp == NWARPS) {
+      if (producer) {
+        // run STAGES deep: the buffer of stage lkt last held stage lkt - STAGES
+        for (int s = 0; s < C::STAGES && lkt < nkt; ++s) load_next(s);
+        while (lkt < nkt) {
+          const int b = lkt % C::STAGES;
+          mbar_wait_cta(&empty[b], ((lkt - C::STAGES) / C::STAGES) & 1);
+          load_next(b);
+        }
+      }
+      return;
+    }
+  } else {
+    if (producer)
+      for (int s = 0; s < C::STAGES - 1 && lkt < nkt; ++s) load_next(s);
+  }
+
+  double acc[Acc<CM>::N][C::WM][C::WN][2];
+#pragma unroll
+  for (int q = 0; q < Acc<CM>::N; ++q)
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
+
+#pragma unroll 1
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int s = kt % C::STAGES;
+    mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
+    const zval* Ps = reinterpret_cast<const zval*>(base + s * T::STAGE_BYTES);
+    const zval* SDs = Ps + C::P_ELEMS;
+    const zval* Xas = SDs + C::P_ELEMS;
+    const zval* Xbs = Xas + C::X_ELEMS;
+    mb_stage_mma<C, false>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&empty[s]);
+    if (!PW && producer && lkt < nkt) {
+      // the buffer of stage lkt last held stage kt - 1: wait until every warp has left it
       const int b = lkt % C::STAGES;
       if (kt >= 1) mbar_wait_cta(&empty[b], ((kt - 1) / C::STAGES) & 1);
       load_next(b);

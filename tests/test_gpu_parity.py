@@ -287,8 +287,8 @@ def test_c1_parity(bse, c1_instance):
         assert np.abs(ov - 1).max() <= 1e-8
 
 
-@pytest.mark.parametrize("algo", ["3m", "3m-sync", "3m-onthefly", "3m-xsum", "3m-ahead", "3m-smem", "3m-mb32", "3m-mb3",
-                                  "3m-mb64x16", "3m-mb128", "3m-swz", "3m-swz5", "4m"])
+@pytest.mark.parametrize("algo", ["3m", "3m-mbcp", "3m-tmaw64x32", "3m-sync", "3m-onthefly", "3m-xsum", "3m-ahead", "3m-smem", "3m-mb32", "3m-mb3",
+                                  "3m-mb64x16", "3m-mb128", "3m-swz", "3m-swz5", "3m-tma", "3m-tma64x16", "3m-tmaw", "3m-tmaw64x16", "3m-tmaw5", "4m"])
 def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
@@ -308,6 +308,43 @@ def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     assert r.converged and abs(r.iterations_used - int(gc["abs_iters"])) <= 1
     assert (np.abs(r.lambdas - gc["abs_lambdas"]) / np.abs(gc["abs_lambdas"])).max() <= 1e-10
     assert r.residual_norms.max() <= 1e-10
+
+
+def test_filter_3m_variants_bitwise_identical(bse):
+    """Every 3M kernel variant (barrier / mbarrier / TMA feeds, all tile shapes, the k-dispatched
+    default) accumulates each output in the same K order: identical bits at ragged shapes."""
+    import torch
+    from paper_2601_10557_b200.hamiltonian import colmajor_empty, ld_of
+    from paper_2601_10557_b200 import _lib
+
+    dev = torch.device("cuda", 0)
+    ctx = _lib.Context.get(0)
+    m, k, deg = 203, 530, 4  # ragged in rows, K and columns; k >= 512 takes the wide default tile
+    gen = torch.Generator(device=dev).manual_seed(5)
+    ab = colmajor_empty(m, 2 * m, dev)
+    ab.copy_(torch.complex(torch.randn(m, 2 * m, generator=gen, device=dev, dtype=torch.float64),
+                           torch.randn(m, 2 * m, generator=gen, device=dev, dtype=torch.float64)))
+    sd = colmajor_empty(m, 2 * m, dev)
+    ctx.call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), m, 2 * m, _lib.dptr(sd))
+    v0 = colmajor_empty(2 * m, k, dev)
+    v0.copy_(torch.complex(torch.randn(2 * m, k, generator=gen, device=dev, dtype=torch.float64),
+                           torch.randn(2 * m, k, generator=gen, device=dev, dtype=torch.float64)))
+    work = torch.empty(2 * 2 * m * k, dtype=torch.complex128, device=dev)
+    outs = {}
+    default = bse.filter_algorithm()
+    try:
+        for algo in ("3m", "3m-sync", "3m-mbcp", "3m-mb64x16", "3m-tma", "3m-tmaw", "3m-tmaw64x32", "3m-tmaw3"):
+            bse.set_filter_algorithm(algo)
+            for kk in (k, 100):  # both sides of the default's column threshold
+                v = v0[:, :kk].clone()
+                v = v.T.contiguous().T
+                ctx.call("bse_chebyshev_filter", _lib.dptr(ab), _lib.dptr(sd), ld_of(ab), m, _lib.dptr(v), 2 * m, kk,
+                         deg, 0.5, 2.0, -3.0, _lib.dptr(work))
+                outs[(algo, kk)] = v.cpu()
+    finally:
+        bse.set_filter_algorithm(default)
+    for (algo, kk), v in outs.items():
+        assert torch.equal(v, outs[("3m-sync", kk)]), (algo, kk)
 
 
 def test_fused_residuals_match_explicit(bse, c1_instance):
