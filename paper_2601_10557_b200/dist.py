@@ -42,6 +42,7 @@ import numpy as np
 from . import _lib, rng
 from .chebyshev import FilterConfig
 from .errors import HermitianRqError, LanczosBreakdownError, NumericalError, RankDeficiencyError, ValidationError
+from .generate import EXACT_LIMIT
 from .lanczos import MAX_RESTARTS, SAFETY_INFLATION, SpectralBounds, _cutoff, update_cutoff
 from .metrics import PhaseLedger
 from .rayleigh_ritz import lock_converged, RitzSet
@@ -664,10 +665,13 @@ class DistSolver:
         n, nevex, nev, tol = 2 * g.m, cfg.nevex, cfg.nev, cfg.tol
         cfg.validate(n)
         ledger = PhaseLedger()
+        st = _Steps("solve", g.rank)
         with ledger.timing("lanczos"):
             bounds = self.lanczos(nevex, cfg.lanczos_steps, rng.substream(cfg.seed, TAG_LANCZOS), ledger)
+        st.mark("lanczos", nevex)
         normalizer = abs(bounds.mu_1) if cfg.rel_res else 1.0
         v = start_block_col(rng.substream(cfg.seed, TAG_SUBSPACE), n, nevex, g, self.ops)
+        st.mark("start block", nevex)
         row_buf = self.ops.empty(nevex, 2 * g.nr)
         locked = self.ops.empty(nev, 2 * g.nc)
         nlock, lvals, lres, trace = 0, [], [], []
@@ -725,17 +729,25 @@ class DistSolver:
             vals = np.concatenate([lvals, lam[act][:miss]])
             blocks = torch.cat([locked[:nlock], vecs[torch.as_tensor(act[:miss], device=vecs.device)]], dim=0)
             resid = np.concatenate([lres, res[act][:miss]])
+        st.mark("iterations", nev)
         order = np.argsort(vals, kind="stable")[:nev]
         full = self.assemble_from_col(blocks[torch.as_tensor(order, device=blocks.device)].contiguous())
+        st.mark("sort + assemble V", nev)
         return SolveResult(lambdas=vals[order], v=full, residual_norms=resid[order], iterations_used=it_used,
                            converged=converged, trace=trace, bounds=bounds, ledger=ledger, backup_events=backups)
 
 
 def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):
     """Rows C_J of both halves of the reference start block complex_normal_matrix(seed, n, cols)
-    (solver.py:139-141), drawn bit-exactly on the host for just this rank's rows."""
+    (solver.py:139-141): drawn bit-exactly on the host for just this rank's rows when m <=
+    EXACT_LIMIT, else the whole block on the device (generate.py's policy; bit-exact words,
+    Box-Muller within ~1 ulp) and this rank's rows sliced out (the host draw of every rank
+    competes for the same host cores: 0.77 s of a 12.8 s C3 solve at N = 4)."""
     torch = ops.torch
     m = grid.m
+    if m > EXACT_LIMIT and hasattr(ops, "ctx"):
+        full = rng.device_complex_normal_matrix(seed, n, cols, ops.device).T  # (cols, n) storage rows
+        return torch.cat([full[:, grid.c0:grid.c1], full[:, m + grid.c0:m + grid.c1]], dim=1).contiguous()
     rows = np.concatenate([np.arange(grid.c0, grid.c1), m + np.arange(grid.c0, grid.c1)])
     index = np.arange(cols, dtype=np.int64)[:, None] * n + rows[None, :]  # column-major fill (rng.py:78-81)
     return torch.from_numpy(rng.complex_normals_at(seed, index)).to(ops.device)

@@ -3,7 +3,10 @@
 (0, 1], Box-Muller complex normals, column-major matrix fill, tagged child
 streams.  Computed on the host with numpy so the start vectors of a solve are
 the very same bits the reference draws (GPU libm would differ in the last
-ulp and change the iteration trace)."""
+ulp and can change a small case's iteration trace).  Above EXACT_LIMIT
+(generate.py's policy, where the Hamiltonian itself comes from the device
+generator) the start block is drawn on the device: bit-exact words, Box-Muller
+within ~1 ulp, milliseconds instead of host seconds shared by all ranks."""
 
 from __future__ import annotations
 
@@ -110,6 +113,20 @@ def complex_normals_at(seed: int, index, threads: int | None = None) -> np.ndarr
     with ThreadPoolExecutor(nt) as ex:
         list(ex.map(work, range(nt)))
     return out.reshape(idx.shape)
+
+
+def device_complex_normal_matrix(seed: int, rows: int, cols: int, device):
+    """complex_normal_matrix drawn on the device (bse_complex_normals): column-major rows x cols."""
+    import ctypes
+
+    from . import _lib
+    from .hamiltonian import colmajor_empty
+
+    out = colmajor_empty(rows, cols, device)
+    if rows * cols:
+        _lib.Context.get(out.device.index).call("bse_complex_normals", _lib.dptr(out), ctypes.c_uint64(seed), 0,
+                                                rows * cols)
+    return out
 
 
 def complex_normal_matrix(seed: int, rows: int, cols: int) -> np.ndarray:

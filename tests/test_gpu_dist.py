@@ -31,3 +31,23 @@ def test_dist_path_single_gpu_matches_reference(key):
     v = res.v.T.contiguous().cpu().numpy().T
     ov = np.abs(np.einsum("ij,ij->j", g["v"].conj(), v))
     assert np.abs(ov - 1).max() <= 1e-8
+
+
+def test_start_block_device_policy_matches_host():
+    """Above EXACT_LIMIT the start block comes from the device rng (generate.py's policy): same
+    stream as the host draw (solver.py:139-141) to Box-Muller rounding, per-rank rows sliced right."""
+    from paper_2601_10557_b200 import rng
+    from paper_2601_10557_b200.dist import CudaOps, Grid, start_block_col
+    from paper_2601_10557_b200.generate import EXACT_LIMIT
+
+    m, cols, seed = EXACT_LIMIT + 3, 6, rng.substream(7, 3)
+    n = 2 * m
+    host = rng.complex_normal_matrix(seed, n, cols)
+    dev = rng.device_complex_normal_matrix(seed, n, cols, torch.device("cuda", 0)).cpu().numpy()
+    assert np.abs(dev - host).max() <= 1e-14 * np.abs(host).max()
+    ops = CudaOps(torch.device("cuda", 0))
+    for world, rank in ((2, 1), (4, 2), (8, 5)):
+        g = Grid(m, world, rank)
+        got = start_block_col(seed, n, cols, g, ops).cpu().numpy()  # (cols, 2 nc) storage
+        rows = np.concatenate([np.arange(g.c0, g.c1), m + np.arange(g.c0, g.c1)])
+        assert np.abs(got - host[rows].T).max() <= 1e-14 * np.abs(host).max()
