@@ -1,5 +1,8 @@
 """Multi-GPU parity check of the 2D-distributed solve (run under torchrun, NCCL):
-golden reference cases + C1, compared on rank 0 with the reference fixtures."""
+golden reference cases + C1, compared on rank 0 with the reference fixtures.
+
+BSE200_DIST_BACKEND=gloo runs more ranks than GPUs (rank r on GPU r % #GPUs, gloo collectives on
+the CUDA tensors): the 2 x 4 grid of an 8-GPU box with the real CUDA kernels on a 4-GPU box."""
 import json
 import os
 import sys
@@ -21,9 +24,14 @@ DistSolver.CHUNK_MIN = 8  # exercise the chunked, stream-overlapped filter on th
 
 
 def main():
-    local = int(os.environ["LOCAL_RANK"])
+    backend = os.environ.get("BSE200_DIST_BACKEND", "nccl")
+    local = int(os.environ["LOCAL_RANK"]) % torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+        DistSolver.CHUNK_MIN = 1 << 30  # no communication-stream overlap under gloo
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", local)
     fails = 0
