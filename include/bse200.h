@@ -54,9 +54,12 @@ const char* bse_last_error(const bse_ctx* ctx);
 /* number of bse200 kernels launched through this context (evidence counter) */
 int64_t bse_launch_count(const bse_ctx* ctx);
 const char* bse_version(void);
-/* Complex multiplication used by the Chebyshev-filter products: 4 (4M split, 8 real DMMA per
- * complex block pair, default) or 3 (3M / Gauss, 6 DMMA: 25% fewer FP64 tensor ops; error bound
- * grows to ~eps (|Re|+|Im|)^2).  RR and residual products always use 4M.          */
+/* Kernel of the Chebyshev-filter products (and of H products given sum planes): 4 = 4M split
+ * (8 real DMMA per complex block pair; the context default); 3M / Gauss (6 DMMA, 25% fewer FP64
+ * tensor ops, error bound ~eps (|Re|+|Im|)^2): 88 = TMA-fed producer-warp kernel
+ * (the Python default), 82 / 86 its narrow / wide tiles, 72 = cp.async + mbarrier rings,
+ * 65 = cp.async + CTA barrier, 3 = sums in registers.  65-88 need the sum planes (else 3 runs);
+ * all 3M codes give bitwise-identical results.  BSE_EVALIDATION for other codes.               */
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults);
 /* Properties of the Hamiltonian the following operator calls on this context act on
  * (BSE_HAM_* flags); the Python layer sets them before every operator call.                     */

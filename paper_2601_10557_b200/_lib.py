@@ -100,19 +100,18 @@ _STATUS = {
 _lib = None
 _lock = threading.Lock()
 # complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
-_ALGOS = {"4m": 4, "3m": 88, "3m-mbcp": 72, "3m-sync": 65, "3m-64x16": 6, "3m-onthefly": 3, "3m-xsum": 7, "3m-ahead": 8,
-          "3m-smem": 9, "3m-mb32": 67, "3m-mb3": 68, "3m-mb64x16": 69, "3m-mb128": 75,
-          "3m-swz": 76, "3m-swz5": 77, "3m-tma": 78, "3m-tma64x16": 79,
-          "3m-tmaw": 82, "3m-tmaw64x16": 83, "3m-tmaw5": 84,
-          "3m-tmaw64x32": 86, "3m-tmaw3": 87}
+_ALGOS = {"4m": 4, "3m": 88, "3m-tma-narrow": 82, "3m-tma-wide": 86, "3m-mbcp": 72, "3m-sync": 65,
+          "3m-onthefly": 3}
 # default 3M (Gauss) with precomputed operand-sum planes: 25% fewer DMMA, parity-checked at C1
 # (tests/test_gpu_parity.py); BSE200_FILTER=4m restores the 4M split
 _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "3m").lower()]
 
 
 def set_filter_algorithm(name: str) -> None:
-    """'3m' (default; Gauss: 25% fewer FP64 tensor ops in the filter, with the operand sums of A and B
-    precomputed once, +32 m^2 bytes), '3m-onthefly' (sums formed in registers) or '4m'."""
+    """'3m' (default: Gauss split, 25% fewer FP64 tensor ops in the filter, the operand sums of A and B
+    precomputed once (+32 m^2 bytes), TMA-fed producer-warp kernel), its fixed tiles '3m-tma-narrow' /
+    '3m-tma-wide', the earlier pipelines '3m-mbcp' / '3m-sync' (all bitwise identical),
+    '3m-onthefly' (sums formed in registers) or '4m'."""
     global _FILTER_CM
     cm = _ALGOS[name.lower()] if isinstance(name, str) else int(name)
     _FILTER_CM = cm
@@ -141,7 +140,7 @@ def filter_precision() -> str:
 
 
 def uses_sum_planes() -> bool:
-    return _FILTER_CM in (6, 7, 8, 81) or 61 <= _FILTER_CM <= 79 or 82 <= _FILTER_CM <= 88
+    return _FILTER_CM in (65, 72, 82, 86, 88)
 
 
 def load() -> C.CDLL:

@@ -433,18 +433,3 @@ __global__ void sum_planes_kernel(const zval* __restrict__ a, int64_t lda, int64
 }
 
 }  // namespace bse
-
-namespace bse {
-
-// s[:, j] = Re + Im of x[:, j] (rows x k): the X-side 3M sum plane of a filter input
-__global__ void re_plus_im_kernel(const zval* __restrict__ x, int64_t ldx, int64_t rows, int64_t k,
-                                  double* __restrict__ s, int64_t lds) {
-  const int64_t total = rows * k;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % rows, j = idx / rows;
-    const zval v = x[j * ldx + i];
-    s[j * lds + i] = v.re + v.im;
-  }
-}
-
-}  // namespace bse

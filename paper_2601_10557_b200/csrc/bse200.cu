@@ -250,14 +250,14 @@ CUtensorMap map2d_f64(const void* base, uint64_t d0, uint64_t d1, uint64_t strid
   return map;
 }
 
-template <class C, bool PW = false>
+template <class C>
 void launch_hop_tma(bse_ctx* ctx, const bse::HopArgs& a_in) {
   bse::HopArgs a = a_in;
   a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
   constexpr size_t smem = bse::TmaLayout<C>::SMEM;
   static bool configured = false;
   if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_tma_kernel<C, PW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   bse::HopMaps mp;
@@ -271,122 +271,59 @@ void launch_hop_tma(bse_ctx* ctx, const bse::HopArgs& a_in) {
     mp.x[q] = map2d_f64(xx[q], xr, a.k, a.ldx * 16, 2 * (C::BK + 4), C::BN);
   }
   dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
-  bse::hop3m_tma_kernel<C, PW><<<grid, C::THREADS + (PW ? 32 : 0), smem, ctx->stream>>>(a, mp);
+  bse::hop3m_tma_kernel<C><<<grid, C::THREADS + 32, smem, ctx->stream>>>(a, mp);
   check_launch(ctx);
 }
 
-template <class C, bool SW = false>
+template <class C>
 void launch_hop_mb(bse_ctx* ctx, const bse::HopArgs& a_in) {
   bse::HopArgs a = a_in;
   a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
-  constexpr size_t smem = bse::MbLayout<C, SW>::SMEM;
+  constexpr size_t smem = bse::MbLayout<C>::SMEM;
   static bool configured = false;
   if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_mb_kernel<C, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_mb_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
-  bse::hop3m_mb_kernel<C, SW><<<grid, C::THREADS, smem, ctx->stream>>>(a);
+  bse::hop3m_mb_kernel<C><<<grid, C::THREADS, smem, ctx->stream>>>(a);
   check_launch(ctx);
 }
 
-// tuning variants (selected with bse_set_filter_algorithm codes 40+v / 30+v)
-using Hop4M_1 = bse::HopCfg<64, 32, 8, 2, 2, 5, 2>;
-using Hop4M_2 = bse::HopCfg<128, 32, 8, 2, 2, 4, 1>;
-using Hop4M_3 = bse::HopCfg<64, 64, 8, 2, 2, 4, 1>;
-using Hop3M_1 = bse::HopCfg<64, 32, 8, 2, 2, 6, 1>;
-using Hop3M_2 = bse::HopCfg<64, 16, 8, 2, 1, 4, 2>;
-using Hop3M_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1>;
-using Hop3M_4 = bse::HopCfg<96, 32, 16, 2, 2, 4, 1>;
-// 3M with precomputed P-side sums (code 6 and tuning variants 61-63)
-using Hop3MS = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1>;
-using Hop3MS_1 = bse::HopCfg<64, 32, 8, 2, 2, 4, 1, 1>;
-using Hop3MS_2 = bse::HopCfg<64, 32, 16, 2, 2, 3, 1, 1>;
-using Hop3MS_3 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
-using Hop3MS_4 = bse::HopCfg<32, 32, 8, 2, 2, 4, 2, 1>;
-using Hop3MS_5 = bse::HopCfg<32, 32, 8, 2, 2, 4, 3, 1>;
-using Hop3MS_6 = bse::HopCfg<64, 16, 8, 2, 1, 3, 3, 1>;
-// mbarrier-pipelined 3M (hop_mb.cuh), codes 67-69
-using Hop3MM_7 = bse::HopCfg<32, 32, 8, 2, 2, 4, 2, 1>;
-using Hop3MM_8 = bse::HopCfg<32, 32, 8, 2, 2, 3, 3, 1>;
-using Hop3MM_9 = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1>;
-using Hop3MM_10 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 1>;
-using Hop3MM_11 = bse::HopCfg<64, 16, 8, 4, 1, 3, 3, 1>;
-using Hop3MM_12 = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 1>;
-using Hop3MM_13 = bse::HopCfg<96, 16, 8, 6, 1, 3, 2, 1>;
-using Hop3MM_14 = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
-using Hop3MM_15 = bse::HopCfg<128, 16, 8, 4, 1, 4, 1, 1>;
-using Hop3MM_16 = bse::HopCfg<64, 16, 8, 4, 1, 5, 2, 1>;  // swizzled X tile (codes 76-77)
-using Hop3MM_18 = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
-using Hop3MM_19 = bse::HopCfg<64, 16, 8, 4, 1, 3, 2, 1>;
-// 3M with P and X sums precomputed (code 7; single-GPU filter with epilogue-produced X sums)
-using Hop3MX = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 1>;
-// 3M with P sums from planes and X sums computed in shared memory one stage ahead (code 8, 81)
-using Hop3MA = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 1, 2>;
-using Hop3MA_1 = bse::HopCfg<64, 16, 8, 2, 1, 5, 2, 1, 2>;
-// 3M with P and X sums both computed in shared memory one stage ahead (code 9, 91, 92): no sum
-// planes in HBM, no add on the DMMA path
-using Hop3MB = bse::HopCfg<64, 16, 8, 2, 1, 4, 2, 2, 2>;
-using Hop3MB_1 = bse::HopCfg<64, 32, 8, 2, 2, 4, 1, 2, 2>;
-using Hop3MB_2 = bse::HopCfg<128, 16, 8, 2, 1, 4, 1, 2, 2>;
+// Filter-product variants (bse_set_filter_algorithm codes; the sweeps that chose them are in
+// profiles/r01/tune_*.txt):
+//   88  default 3M: TMA-fed, producer warp, mbarrier rings (hop_mb.cuh); tile by block width
+//   82 / 86  its two tiles alone (64 x 16, 4 consumer warps, 2 CTAs/SM / 64 x 32, 8 warps, 6 stages)
+//   72  3M, cp.async feed with mbarrier rings (hop3m_mb_kernel), 64 x 16, 4 warps of 32 x 8
+//   65  3M, cp.async feed with one __syncthreads per stage (hop_kernel CM 6), 32 x 32
+//    3  3M with the operand sums formed in registers (no sum planes needed)
+//    4  4M (HopMain)
+using Hop3MSync = bse::HopCfg<32, 32, 8, 2, 2, 4, 3, 1>;
+using Hop3MNarrow = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 1>;
+using Hop3MWide = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 
-// Chebyshev-step products: 4M (default) or 3M as selected by bse_set_filter_algorithm
+bool filter_code_needs_planes(int code) { return code == 65 || code == 72 || code == 82 || code == 86 || code == 88; }
+bool filter_code_valid(int code) { return code == 3 || code == 4 || filter_code_needs_planes(code); }
+
+// Chebyshev-step products, as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
-  if (code == 7 && (!a.xs1 || !a.xs2)) code = 6;                                  // no X sum planes
-  if ((code == 6 || code == 7 || code == 8 || code == 81 || (code >= 61 && code <= 79) || (code >= 82 && code <= 88 && code != 85)) && (!a.sa || !a.sb))
-    code = 3;  // no P sum planes
+  if (filter_code_needs_planes(code) && (!a.sa || !a.sb)) code = 3;  // no P sum planes: sums in registers
   switch (code) {
-    case 9: launch_hop<Hop3MB, bse::HOP_AXPBY, 9>(ctx, a); break;
-    case 91: launch_hop<Hop3MB_1, bse::HOP_AXPBY, 9>(ctx, a); break;
-    case 92: launch_hop<Hop3MB_2, bse::HOP_AXPBY, 9>(ctx, a); break;
-    case 8: launch_hop<Hop3MA, bse::HOP_AXPBY, 8>(ctx, a); break;
-    case 81: launch_hop<Hop3MA_1, bse::HOP_AXPBY, 8>(ctx, a); break;
-    case 7: launch_hop<Hop3MX, bse::HOP_AXPBY, 7>(ctx, a); break;
-    case 6: launch_hop<Hop3MS, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 61: launch_hop<Hop3MS_1, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 62: launch_hop<Hop3MS_2, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 63: launch_hop<Hop3MS_3, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 64: launch_hop<Hop3MS_4, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 65: launch_hop<Hop3MS_5, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 66: launch_hop<Hop3MS_6, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 67: launch_hop_mb<Hop3MM_7>(ctx, a); break;
-    case 68: launch_hop_mb<Hop3MM_8>(ctx, a); break;
-    case 69: launch_hop_mb<Hop3MM_9>(ctx, a); break;
-    case 70: launch_hop_mb<Hop3MM_10>(ctx, a); break;
-    case 71: launch_hop_mb<Hop3MM_11>(ctx, a); break;
-    case 72: launch_hop_mb<Hop3MM_12>(ctx, a); break;
-    case 73: launch_hop_mb<Hop3MM_13>(ctx, a); break;
-    case 74: launch_hop_mb<Hop3MM_14>(ctx, a); break;
-    case 75: launch_hop_mb<Hop3MM_15>(ctx, a); break;
-    case 76: launch_hop_mb<Hop3MM_12, true>(ctx, a); break;
-    case 77: launch_hop_mb<Hop3MM_16, true>(ctx, a); break;
-    case 78: launch_hop_tma<Hop3MM_12>(ctx, a); break;
-    case 79: launch_hop_tma<Hop3MM_9>(ctx, a); break;
-    case 82: launch_hop_tma<Hop3MM_12, true>(ctx, a); break;
-    case 83: launch_hop_tma<Hop3MM_9, true>(ctx, a); break;
-    case 84: launch_hop_tma<Hop3MM_16, true>(ctx, a); break;
-    case 86: launch_hop_tma<Hop3MM_18, true>(ctx, a); break;
-    case 87: launch_hop_tma<Hop3MM_19, true>(ctx, a); break;
-    // default 3M: TMA-fed, producer warp; 64 x 32 CTA (8 consumer warps, 6 stages) for wide blocks,
-    // 64 x 16 (4 warps, 2 CTAs/SM) below 512 columns where the wider tile underfills the GPU.
-    // Both accumulate every output in the same K order: the choice never changes a bit.
+    // default 3M: 64 x 32 CTA (8 consumer warps, 6 stages) for wide blocks, 64 x 16 (4 warps,
+    // 2 CTAs/SM) below 512 columns where the wider tile underfills the GPU.  Every variant
+    // accumulates each output in the same K order: the choice never changes a bit.
     case 88:
       if (a.k >= 512)
-        launch_hop_tma<Hop3MM_18, true>(ctx, a);
+        launch_hop_tma<Hop3MWide>(ctx, a);
       else
-        launch_hop_tma<Hop3MM_12, true>(ctx, a);
+        launch_hop_tma<Hop3MNarrow>(ctx, a);
       break;
+    case 82: launch_hop_tma<Hop3MNarrow>(ctx, a); break;
+    case 86: launch_hop_tma<Hop3MWide>(ctx, a); break;
+    case 72: launch_hop_mb<Hop3MNarrow>(ctx, a); break;
+    case 65: launch_hop<Hop3MSync, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
-    case 31: launch_hop<Hop3M_1, bse::HOP_AXPBY, 3>(ctx, a); break;
-    case 32: launch_hop<Hop3M_2, bse::HOP_AXPBY, 3>(ctx, a); break;
-    case 33: launch_hop<Hop3M_3, bse::HOP_AXPBY, 3>(ctx, a); break;
-    case 34: launch_hop<Hop3M_4, bse::HOP_AXPBY, 3>(ctx, a); break;
-    case 35: launch_hop<Hop3M, bse::HOP_AXPBY, 5>(ctx, a); break;    // timing experiment (no operand sums)
-    case 36: launch_hop<Hop3M_2, bse::HOP_AXPBY, 5>(ctx, a); break;  // timing experiment
-    case 41: launch_hop<Hop4M_1, bse::HOP_AXPBY, 4>(ctx, a); break;
-    case 42: launch_hop<Hop4M_2, bse::HOP_AXPBY, 4>(ctx, a); break;
-    case 43: launch_hop<Hop4M_3, bse::HOP_AXPBY, 4>(ctx, a); break;
     default: launch_hop<HopMain, bse::HOP_AXPBY, 4>(ctx, a); break;
   }
 }
@@ -462,20 +399,11 @@ void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval*
 }
 
 void filter_step(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const zval* y,
-                 const zval* yprev, zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta,
-                 const double* xs = nullptr, double* ys = nullptr, int64_t ldxs = 0) {
+                 const zval* yprev, zval* ynext, int64_t ld, int64_t k, double c, double alpha, double beta) {
   bse::HopArgs a = hop_args_single(d_ab, lda, m, y, ld, k);
   if (d_sd) {
     a.sa = static_cast<const zval*>(d_sd);
     a.sb = a.sa + m * lda;
-  }
-  if (xs && ys) {  // X sums of y in, Re + Im of y_next out (code 7)
-    a.xs1 = xs;
-    a.xs2 = xs + m;
-    a.ldxs = ldxs;
-    a.ys1 = ys;
-    a.ys2 = ys + m;
-    a.ldys = ldxs;
   }
   a.y1 = ynext;
   a.y2 = ynext + m;
@@ -906,13 +834,8 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
-    const bool ok = complex_mults == 3 || complex_mults == 4 || complex_mults == 6 || complex_mults == 7 ||
-                    complex_mults == 8 || complex_mults == 81 || complex_mults == 9 || complex_mults == 91 ||
-                    complex_mults == 92 ||
-                    (complex_mults >= 31 && complex_mults <= 36) || (complex_mults >= 41 && complex_mults <= 43) ||
-                    (complex_mults >= 61 && complex_mults <= 79) ||
-                    (complex_mults >= 82 && complex_mults <= 88 && complex_mults != 85);
-    if (!ok) throw BseError(BSE_EVALIDATION, "complex_mults must be 3 or 4 (tuning variants 31-34, 41-43)");
+    if (!filter_code_valid(complex_mults))
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 3, 4, 65, 72, 82, 86 or 88 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }
@@ -964,26 +887,16 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64
     if (k == 0 || m == 0) return;
     // chebyshev.py:58-74 with three rotating buffers {v, w0, w1}
     zval* bufs[3] = {static_cast<zval*>(d_v), static_cast<zval*>(d_work), static_cast<zval*>(d_work) + ld * k};
-    // code 7: the Re + Im planes of the three buffers (each step's epilogue writes the next one's)
-    const bool xsums = ctx->filter_cm == 7 && d_sd;
-    const int64_t n = 2 * m;
-    Scratch sc(ctx, xsums ? 3 * al((size_t)n * k * sizeof(double)) : 0);
-    double* sums[3] = {nullptr, nullptr, nullptr};
-    if (xsums) {
-      for (int i = 0; i < 3; ++i) sums[i] = sc.take<double>((size_t)n * k);
-      bse::re_plus_im_kernel<<<grid1d(n * k, 256, 148 * 16), 256, 0, ctx->stream>>>(bufs[0], ld, n, k, sums[0], n);
-      check_launch(ctx);
-    }
     const double sigma1 = e / (s - c);
     double sigma = sigma1;
     int prev = 0, cur = 1;
-    filter_step(ctx, d_ab, d_sd, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0, sums[0], sums[1], n);
+    filter_step(ctx, d_ab, d_sd, lda, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0);
     for (int step = 2; step <= deg; ++step) {
       const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
       const int nxt = 3 - prev - cur;
       // y_next = (2 s'/e)(H y - c y) - (s s') y_prev ; written over the free buffer
       filter_step(ctx, d_ab, d_sd, lda, m, bufs[cur], bufs[prev], bufs[nxt], ld, k, c, 2.0 * sigma_new / e,
-                  sigma * sigma_new, sums[cur], sums[nxt], n);
+                  sigma * sigma_new);
       prev = cur;
       cur = nxt;
       sigma = sigma_new;

@@ -31,11 +31,6 @@ struct HopArgs {
   // 3M with precomputed operand sums (CM == 6): (Pr + Pi, Pr - Pi) planes of the same tiles
   const zval* sa;
   const zval* sb;
-  // 3M with precomputed X sums too (CM == 7): Re + Im planes of x1 / x2 (leading dim ldxs),
-  // produced by the previous step's epilogue (ys1 / ys2 below)
-  const double* xs1;
-  const double* xs2;
-  int64_t ldxs;
   int mr;  // output rows per half
   int kc;  // contraction length per part
   int skip_b;  // B == 0 (TDA / hermitian limit): contract over the A part only (4 n^2 k flops)
@@ -59,19 +54,14 @@ struct HopArgs {
   // input block shares with its output block in the 2D layout); per-column shifts when set
   int shift_lo, shift_hi;
   const double* shift_col;
-  // optional Re + Im plane of the output (written by the AXPBY epilogue when non-null)
-  double* ys1;
-  double* ys2;
-  int64_t ldys;
   // residual mode
   const double* lam;  // per column
   double* partial;    // [gridDim.y][k]
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_, int PS_ = 0, int XS_ = 0>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_, int PS_ = 0>
 struct HopCfg {
-  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_, PS = PS_,
-                       XS = XS_;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_, PS = PS_;
   static constexpr int WARPS_M = BM / (8 * WM);
   static constexpr int WARPS_N = BN / (8 * WN);
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
@@ -80,11 +70,7 @@ struct HopCfg {
   static constexpr int P_ELEMS = BK * LDP;
   static constexpr int SD_ELEMS = PS ? BK * LDP : 0;  // (Pr+Pi, Pr-Pi) tile, same layout as P
   static constexpr int X_ELEMS = BN * LDX;
-  static constexpr int LDXS = BK + 4;  // doubles; == 12 (mod 16) for BK = 8: conflict-free LDS.64
-  static constexpr int XS_ELEMS = XS ? BN * LDXS : 0;  // in zval units: two planes of BN x LDXS doubles
-  // XS == 1: X sums loaded from global planes (code 7); XS == 2: computed in shared memory one
-  // stage ahead of the MMAs (code 8)
-  static constexpr int STAGE_ELEMS = P_ELEMS + SD_ELEMS + 2 * X_ELEMS + XS_ELEMS;
+  static constexpr int STAGE_ELEMS = P_ELEMS + SD_ELEMS + 2 * X_ELEMS;
   static constexpr size_t SMEM = size_t(STAGES) * STAGE_ELEMS * sizeof(zval);
   static_assert(BM % 8 == 0 && BK % 8 == 0 && BN % 8 == 0, "tile dims");
 };
@@ -125,11 +111,6 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
     const zval* X = which ? XB : XA;
     const zval* src = ok ? X + (int64_t)gc * a.ldx + gj : X;
     cp_async16((which ? Xbs : Xas) + cc * C::LDX + kk, src, ok);
-    if constexpr (C::XS == 1) {
-      const double* XSg = part ? (which ? a.xs1 : a.xs2) : (which ? a.xs2 : a.xs1);
-      double* XSs = reinterpret_cast<double*>(Xbs + C::X_ELEMS) + which * C::BN * C::LDXS;
-      cp_async8(XSs + cc * C::LDXS + kk, ok ? XSg + (int64_t)gc * a.ldxs + gj : XSg, ok);
-    }
   }
 }
 
@@ -139,13 +120,13 @@ __device__ __forceinline__ void hop_load_stage(zval* st, const HopArgs& a, int k
 //      Ur = T1 - T2, Ui = T3 - T1 - T2, L'r = S1 + S2, L'i = S3 - S1 + S2.
 template <int CM>
 struct Acc {
-  static constexpr int N = (CM == 3 || CM == 5 || CM == 6 || CM == 7 || CM == 8 || CM == 9) ? 6 : 4;
+  static constexpr int N = (CM == 3 || CM == 6) ? 6 : 4;
 };
 
 template <int CM, int WM, int WN>
 __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][WN][2], int i, int j, int h, double& ur,
                                            double& ui, double& lr, double& li) {
-  if constexpr (CM == 3 || CM == 5 || CM == 6 || CM == 7 || CM == 8 || CM == 9) {
+  if constexpr (CM == 3 || CM == 6) {
     const double t1 = acc[0][i][j][h], t2 = acc[1][i][j][h], t3 = acc[2][i][j][h];
     const double s1 = acc[3][i][j][h], s2 = acc[4][i][j][h], s3 = acc[5][i][j][h];
     ur = t1 - t2;
@@ -157,28 +138,6 @@ __device__ __forceinline__ void acc_values(const double (&acc)[Acc<CM>::N][WM][W
     ui = acc[1][i][j][h];
     lr = acc[2][i][j][h];
     li = acc[3][i][j][h];
-  }
-}
-
-// CM == 8 / 9: 3M operand sums of one landed stage, written into its XS planes (X side) and, with
-// PS == 2, its SD tile (P side: (re + im, re - im)); computed one stage ahead of the MMAs
-template <class C>
-__device__ __forceinline__ void hop_stage_xsums(zval* st) {
-  if constexpr (C::PS == 2) {
-    const zval* Ps = st;
-    zval* SDs = st + C::P_ELEMS;
-    for (int id = threadIdx.x; id < C::BK * C::BM; id += C::THREADS) {
-      const int ii = id % C::BM, jj = id / C::BM;
-      const zval v = Ps[jj * C::LDP + ii];
-      SDs[jj * C::LDP + ii] = zval{v.re + v.im, v.re - v.im};
-    }
-  }
-  zval* Xas = st + C::P_ELEMS + C::SD_ELEMS;
-  double* XS = reinterpret_cast<double*>(Xas + 2 * C::X_ELEMS);
-  for (int id = threadIdx.x; id < 2 * C::BN * C::BK; id += C::THREADS) {
-    const int kk = id % C::BK, cc = (id / C::BK) % C::BN, which = id / (C::BK * C::BN);
-    const zval v = Xas[which * C::X_ELEMS + cc * C::LDX + kk];
-    XS[which * C::BN * C::LDXS + cc * C::LDXS + kk] = v.re + v.im;
   }
 }
 
@@ -224,10 +183,6 @@ __device__ __forceinline__ void hop_epilogue_axpby(const double (&acc)[Acc<CM>::
         o2.im *= a.low_sign;
         a.y1[(int64_t)col * a.ldy + row] = o1;
         a.y2[(int64_t)col * a.ldy + row] = o2;
-        if (a.ys1) {
-          a.ys1[(int64_t)col * a.ldys + row] = o1.re + o1.im;
-          a.ys2[(int64_t)col * a.ldys + row] = o2.re + o2.im;
-        }
       }
     }
   }
@@ -261,25 +216,14 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
     if (s < nkt) hop_load_stage<C>(smem + s * C::STAGE_ELEMS, a, s, nkt_part, i0, c0);
     cp_async_commit();
   }
-  if constexpr (CM == 8 || CM == 9) {  // sums of stage 0 before the loop
-    cp_async_wait<C::STAGES - 2>();
-    __syncthreads();
-    hop_stage_xsums<C>(smem);
-  }
 
   for (int kt = 0; kt < nkt; ++kt) {
-    if constexpr (CM == 8 || CM == 9)
-      cp_async_wait<C::STAGES - 3>();  // stages kt and kt + 1 landed
-    else
-      cp_async_wait<C::STAGES - 2>();
+    cp_async_wait<C::STAGES - 2>();
     __syncthreads();
     {
       const int nxt = kt + C::STAGES - 1;
       if (nxt < nkt) hop_load_stage<C>(smem + (nxt % C::STAGES) * C::STAGE_ELEMS, a, nxt, nkt_part, i0, c0);
       cp_async_commit();
-    }
-    if constexpr (CM == 8 || CM == 9) {  // sums for the next stage, consumed after the next barrier
-      if (kt + 1 < nkt) hop_stage_xsums<C>(smem + ((kt + 1) % C::STAGES) * C::STAGE_ELEMS);
     }
     const zval* Ps = smem + (kt % C::STAGES) * C::STAGE_ELEMS;
     const zval* SDs = Ps + C::P_ELEMS;
@@ -296,24 +240,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
         xa[j] = lds128(Xas + col * C::LDX + ks * 4 + t);
         xb[j] = lds128(Xbs + col * C::LDX + ks * 4 + t);
       }
-      if constexpr (CM == 6 || CM == 7 || CM == 8 || CM == 9) {
-        // 3M with the P-side sums read from shared memory; with CM == 7 the X-side sums too, so
-        // no add sits on the DMMA critical path
+      if constexpr (CM == 6) {
+        // 3M with the P-side sums read from shared memory
         zval sd[C::WM];
 #pragma unroll
         for (int i = 0; i < C::WM; ++i) sd[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
         double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {
-          if constexpr (CM == 7 || CM == 8 || CM == 9) {
-            const double* XSa = reinterpret_cast<const double*>(Xbs + C::X_ELEMS);
-            const int col = wn * (8 * C::WN) + j * 8 + g;
-            xas[j] = XSa[col * C::LDXS + ks * 4 + t];
-            xbs[j] = XSa[C::BN * C::LDXS + col * C::LDXS + ks * 4 + t];
-          } else {
-            xas[j] = xa[j].re + xa[j].im;
-            xbs[j] = xb[j].re + xb[j].im;
-          }
+          xas[j] = xa[j].re + xa[j].im;
+          xbs[j] = xb[j].re + xb[j].im;
         }
 #pragma unroll
         for (int i = 0; i < C::WM; ++i) {
@@ -327,18 +263,18 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop_kernel(const HopArgs 
             dmma(acc[5][i][j], sd[i].im, xbs[j]);
           }
         }
-      } else if constexpr (CM == 3 || CM == 5) {
+      } else if constexpr (CM == 3) {
         double xas[C::WN], xbs[C::WN];
 #pragma unroll
         for (int j = 0; j < C::WN; ++j) {
-          xas[j] = CM == 5 ? xa[j].re : xa[j].re + xa[j].im;
-          xbs[j] = CM == 5 ? xb[j].im : xb[j].re + xb[j].im;
+          xas[j] = xa[j].re + xa[j].im;
+          xbs[j] = xb[j].re + xb[j].im;
         }
 #pragma unroll
         for (int i = 0; i < C::WM; ++i) {
           const double pr = pf[i].re, pi = pf[i].im;
-          const double ps = CM == 5 ? pf[i].im : pf[i].re + pf[i].im;
-          const double pd = CM == 5 ? pf[i].re : pf[i].re - pf[i].im;
+          const double ps = pf[i].re + pf[i].im;
+          const double pd = pf[i].re - pf[i].im;
 #pragma unroll
           for (int j = 0; j < C::WN; ++j) {
             dmma(acc[0][i][j], pr, xa[j].re);

@@ -43,24 +43,21 @@ __device__ __forceinline__ void mbar_wait_cta(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// Stage layout.  SW == false: hop_kernel's padded X tile (LDX = BK + 4).  SW == true: unpadded
-// X rows of BK = 8 complex with the two 4-wide K halves swapped on odd columns (k ^ 4), which keeps
-// every 8-lane phase of the fragment LDS.128 on 32 distinct banks and saves a third of the X tile
-// (room for one more stage at 2 CTAs/SM).
-template <class C, bool SW>
+// Stage layout: hop_kernel's padded tiles (LDP = BM + 2, LDX = BK + 4: conflict-free LDS.128).
+// (An unpadded X tile with the K halves swapped on odd columns is conflict free too and saves a
+// third of the X bytes; it measured no faster, profiles/r01/tune_3m_swizzle.txt.)
+template <class C>
 struct MbLayout {
-  static_assert(!SW || C::BK == 8, "swizzled X tile assumes BK == 8");
-  static constexpr int LDX = SW ? C::BK : C::LDX;
+  static constexpr int LDX = C::LDX;
   static constexpr int X_ELEMS = C::BN * LDX;
   static constexpr int STAGE_ELEMS = C::P_ELEMS + C::SD_ELEMS + 2 * X_ELEMS;
   static constexpr size_t SMEM = size_t(C::STAGES) * STAGE_ELEMS * sizeof(zval);
-  __device__ __forceinline__ static int xk(int col, int k) { return SW ? (k ^ ((col & 1) << 2)) : k; }
 };
 
 // Per-thread copy slots of one stage: NP (P and sum-plane) slots and NX (X) slots.
-template <class C, bool SW>
+template <class C>
 struct MbLoader {
-  using L = MbLayout<C, SW>;
+  using L = MbLayout<C>;
   static constexpr int NP = (C::BK * C::BM + C::THREADS - 1) / C::THREADS;
   static constexpr int NX = (2 * C::BN * C::BK + C::THREADS - 1) / C::THREADS;
   static constexpr bool X_ALL = (2 * C::BN * C::BK) % C::THREADS == 0;  // else the last X slot is partial
@@ -97,7 +94,7 @@ struct MbLoader {
       const int kk = id % C::BK, cc = (id / C::BK) % C::BN, which = id / (C::BK * C::BN);
       xcol[r] = c0 + cc < a.k;
       xk[r] = kk;
-      x_off[r] = which * L::X_ELEMS + cc * L::LDX + L::xk(cc, kk);
+      x_off[r] = which * L::X_ELEMS + cc * L::LDX + kk;
       x[r] = (which ? XB : XA) + (int64_t)(xcol[r] ? c0 + cc : 0) * a.ldx + kk;
     }
   }
@@ -126,10 +123,10 @@ struct MbLoader {
 };
 
 // the 3M DMMA work of one landed stage (identical arithmetic to hop_kernel CM == 6)
-template <class C, bool SW>
+template <class C>
 __device__ __forceinline__ void mb_stage_mma(double (&acc)[6][C::WM][C::WN][2], const zval* Ps, const zval* SDs,
                                              const zval* Xas, const zval* Xbs, int wm, int wn, int g, int t) {
-  using L = MbLayout<C, SW>;
+  using L = MbLayout<C>;
 #pragma unroll
   for (int ks = 0; ks < C::BK / 4; ++ks) {
     zval pf[C::WM], sdf[C::WM], xa[C::WN], xb[C::WN];
@@ -141,8 +138,8 @@ __device__ __forceinline__ void mb_stage_mma(double (&acc)[6][C::WM][C::WN][2], 
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
       const int col = wn * (8 * C::WN) + j * 8 + g;
-      xa[j] = lds128(Xas + col * L::LDX + L::xk(col, ks * 4 + t));
-      xb[j] = lds128(Xbs + col * L::LDX + L::xk(col, ks * 4 + t));
+      xa[j] = lds128(Xas + col * L::LDX + ks * 4 + t);
+      xb[j] = lds128(Xbs + col * L::LDX + ks * 4 + t);
     }
     double xas[C::WN], xbs[C::WN];
 #pragma unroll
@@ -165,10 +162,10 @@ __device__ __forceinline__ void mb_stage_mma(double (&acc)[6][C::WM][C::WN][2], 
   }
 }
 
-template <class C, bool SW = false>
+template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const HopArgs a) {
-  using L = MbLayout<C, SW>;
-  static_assert(C::PS == 1 && C::XS == 0, "hop3m_mb_kernel: 3M with P-side sum planes only");
+  using L = MbLayout<C>;
+  static_assert(C::PS == 1, "hop3m_mb_kernel: 3M with P-side sum planes only");
   constexpr int CM = 6;
   constexpr int NWARPS = C::THREADS / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -193,7 +190,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
   }
   __syncthreads();
 
-  MbLoader<C, SW> ld;
+  MbLoader<C> ld;
   ld.init(a, 0, i0, c0);
   int lkt = 0;  // next stage to load
   auto load_next = [&](int buf) {
@@ -222,7 +219,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
     const zval* SDs = Ps + C::P_ELEMS;
     const zval* Xas = SDs + C::SD_ELEMS;
     const zval* Xbs = Xas + L::X_ELEMS;
-    mb_stage_mma<C, SW>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
+    mb_stage_mma<C>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);
     if (lkt < nkt) {
@@ -240,8 +237,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const Hop
 // fragment LDS.128 conflict-free; a TMA box is written densely, so the boxes are made as wide as
 // the padded rows: P / sum-plane boxes of (BM + 2) complex x BK rows land with pitch LDP, X boxes
 // of (BK + 4) complex x BN columns land with pitch LDX (the extra rows / K values are neighbouring
-// data or TMA's zero fill, never read).  One elected thread issues 4 bulk-tensor copies per stage
-// against full[s] (arrive.expect_tx) instead of 8 cp.async per thread.
+// data or TMA's zero fill, never read).  A producer warp issues 4 bulk-tensor copies per stage
+// against full[s] (arrive.expect_tx) instead of 8 cp.async per thread, and waits only on the
+// empty barriers, so no consumer warp ever waits for another (with one consumer thread as the
+// producer, warp 0 is throttled by the slowest warp: 7% slower, profiles/r01/tune_3m_tma.txt).
 struct HopMaps {
   CUtensorMap p[2];   // [A | B] parts: (2 mr doubles) x kc, leading dim lda
   CUtensorMap sd[2];  // their (Pr + Pi, Pr - Pi) planes
@@ -250,7 +249,7 @@ struct HopMaps {
 
 template <class C>
 struct TmaLayout {
-  static_assert(C::PS == 1 && C::XS == 0, "TMA feed: 3M with P-side sum planes only");
+  static_assert(C::PS == 1, "TMA feed: 3M with P-side sum planes only");
   static constexpr int P_BYTES = C::P_ELEMS * 16, X_BYTES = C::X_ELEMS * 16;
   static constexpr int STAGE_BYTES = 2 * P_BYTES + 2 * X_BYTES;
   static_assert(P_BYTES % 128 == 0 && X_BYTES % 128 == 0, "TMA destinations must stay 128-byte aligned");
@@ -259,10 +258,9 @@ struct TmaLayout {
   static constexpr size_t SMEM = size_t(C::STAGES) * STAGE_BYTES + 128;  // + alignment slack
 };
 
-// PW == true: a dedicated producer warp (warp NWARPS) issues the copies, so no consumer warp ever
-// waits for the others; PW == false: thread 0 of the consumers does.
-template <class C, bool PW = false>
-__global__ void __launch_bounds__(C::THREADS + (PW ? 32 : 0), C::MINB)
+// C::THREADS consumer threads + one producer warp (warp C::THREADS / 32)
+template <class C>
+__global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
     hop3m_tma_kernel(const HopArgs a, const __grid_constant__ HopMaps maps) {
   using T = TmaLayout<C>;
   constexpr int CM = 6;
@@ -279,7 +277,7 @@ __global__ void __launch_bounds__(C::THREADS + (PW ? 32 : 0), C::MINB)
   const int i0 = blockIdx.y * C::BM;
   const int nkt_part = (a.kc + C::BK - 1) / C::BK;
   const int nkt = a.skip_b ? nkt_part : 2 * nkt_part;
-  const bool producer = PW ? threadIdx.x == C::THREADS : threadIdx.x == 0;
+  const bool producer = threadIdx.x == C::THREADS;
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -308,22 +306,17 @@ __global__ void __launch_bounds__(C::THREADS + (PW ? 32 : 0), C::MINB)
     tc::tma_load_2d(st + 2 * T::P_BYTES + T::X_BYTES, &maps.x[1 - part], &full[buf], 2 * j0, c0);  // Xb
     ++lkt;
   };
-  if constexpr (PW) {
-    if (warp == NWARPS) {
-      if (producer) {
-        // run STAGES deep: the buffer of stage lkt last held stage lkt - STAGES
-        for (int s = 0; s < C::STAGES && lkt < nkt; ++s) load_next(s);
-        while (lkt < nkt) {
-          const int b = lkt % C::STAGES;
-          mbar_wait_cta(&empty[b], ((lkt - C::STAGES) / C::STAGES) & 1);
-          load_next(b);
-        }
+  if (warp == NWARPS) {
+    if (producer) {
+      // run STAGES deep: the buffer of stage lkt last held stage lkt - STAGES
+      for (int s = 0; s < C::STAGES && lkt < nkt; ++s) load_next(s);
+      while (lkt < nkt) {
+        const int b = lkt % C::STAGES;
+        mbar_wait_cta(&empty[b], ((lkt - C::STAGES) / C::STAGES) & 1);
+        load_next(b);
       }
-      return;
     }
-  } else {
-    if (producer)
-      for (int s = 0; s < C::STAGES - 1 && lkt < nkt; ++s) load_next(s);
+    return;
   }
 
   double acc[Acc<CM>::N][C::WM][C::WN][2];
@@ -342,15 +335,9 @@ __global__ void __launch_bounds__(C::THREADS + (PW ? 32 : 0), C::MINB)
     const zval* SDs = Ps + C::P_ELEMS;
     const zval* Xas = SDs + C::P_ELEMS;
     const zval* Xbs = Xas + C::X_ELEMS;
-    mb_stage_mma<C, false>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
+    mb_stage_mma<C>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);
-    if (!PW && producer && lkt < nkt) {
-      // the buffer of stage lkt last held stage kt - 1: wait until every warp has left it
-      const int b = lkt % C::STAGES;
-      if (kt >= 1) mbar_wait_cta(&empty[b], ((kt - 1) / C::STAGES) & 1);
-      load_next(b);
-    }
   }
   hop_epilogue_axpby<C, CM>(acc, a, i0, c0, wm, wn, g, t);
 }

@@ -287,8 +287,7 @@ def test_c1_parity(bse, c1_instance):
         assert np.abs(ov - 1).max() <= 1e-8
 
 
-@pytest.mark.parametrize("algo", ["3m", "3m-mbcp", "3m-tmaw64x32", "3m-sync", "3m-onthefly", "3m-xsum", "3m-ahead", "3m-smem", "3m-mb32", "3m-mb3",
-                                  "3m-mb64x16", "3m-mb128", "3m-swz", "3m-swz5", "3m-tma", "3m-tma64x16", "3m-tmaw", "3m-tmaw64x16", "3m-tmaw5", "4m"])
+@pytest.mark.parametrize("algo", ["3m", "3m-tma-narrow", "3m-tma-wide", "3m-mbcp", "3m-sync", "3m-onthefly", "4m"])
 def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
@@ -333,7 +332,7 @@ def test_filter_3m_variants_bitwise_identical(bse):
     outs = {}
     default = bse.filter_algorithm()
     try:
-        for algo in ("3m", "3m-sync", "3m-mbcp", "3m-mb64x16", "3m-tma", "3m-tmaw", "3m-tmaw64x32", "3m-tmaw3"):
+        for algo in ("3m", "3m-sync", "3m-mbcp", "3m-tma-narrow", "3m-tma-wide"):
             bse.set_filter_algorithm(algo)
             for kk in (k, 100):  # both sides of the default's column threshold
                 v = v0[:, :kk].clone()
