@@ -196,6 +196,32 @@ int bse_c64_prepare(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void
 int bse_chebyshev_filter_c64(bse_ctx* ctx, const void* d_pplanes, int64_t m, void* d_v, int64_t ldv, int64_t k, int deg,
                              double c, double e, double s, void* d_work);
 
+/* complex64 filter on a tile of the 2D grid (dist.py).  A "plane set" of an n = 2 rows x k block
+ * is 8 consecutive fp32 planes (Re hi, Re lo, Im hi, Im lo, then their negations) of
+ * 2 pad4(rows) k floats each (column-major, lower half at row pad4(rows)).
+ * bse_c64_tile_planes: the 4 P planes of a tile with output rows mo and contraction kc per part,
+ *   read from the columns of the transposed blocks (src_a = A^H block, src_b = B^T block, kc x mo,
+ *   leading dim lds): the fwd tile's planes come from the trn tile and vice versa.
+ * bse_c64_tile_step: out = alpha (tile x - shift x[rows + s_off] on rows [shift_lo, shift_hi))
+ *   - beta prev; raw != 0 writes the unsplit fp32 Re / Im planes (2 planes) for an allreduce,
+ *   bse_c64_split turns them into the next step's plane set.                                   */
+typedef struct {
+  const void* pplanes; /* bse_c64_tile_planes of this tile */
+  int64_t mo, kc, k;   /* output rows per half, contraction per part (input rows per half), columns */
+  const void* x;       /* input plane set (kc rows per half) */
+  const void* prev;    /* y_prev plane set (mo rows; nullable when beta == 0) */
+  void* out;           /* output plane set, or the 2 raw planes when raw != 0 */
+  double alpha, beta, shift;
+  int64_t shift_lo, shift_hi, s_off;
+  int raw;
+} bse_c64_tile_args;
+int bse_c64_tile_planes(bse_ctx* ctx, const void* d_src_a, const void* d_src_b, int64_t lds, int64_t mo, int64_t kc,
+                        void* d_pplanes);
+int bse_c64_tile_step(bse_ctx* ctx, const bse_c64_tile_args* args);
+int bse_c64_split(bse_ctx* ctx, const void* d_raw, int64_t rows, int64_t k, void* d_planes);
+int bse_c64_to_planes(bse_ctx* ctx, const void* d_v, int64_t ldv, int64_t rows, int64_t k, void* d_planes);
+int bse_c64_from_planes(bse_ctx* ctx, const void* d_planes, int64_t rows, int64_t k, void* d_v, int64_t ldv);
+
 /* ---- synthetic inputs (generate.py:60-83 on the device) -------------------- */
 /* complex normals start_index .. +count of stream `seed` (rng.py:63-81):
  * bit-exact splitmix64 words, device libm Box-Muller (<= ~1 ulp from host). */

@@ -44,6 +44,17 @@ class HopTileArgs(C.Structure):
     ]
 
 
+class C64TileArgs(C.Structure):
+    """bse_c64_tile_args (include/bse200.h)."""
+
+    _fields_ = [
+        ("pplanes", _vp), ("mo", _i64), ("kc", _i64), ("k", _i64),
+        ("x", _vp), ("prev", _vp), ("out", _vp),
+        ("alpha", _dbl), ("beta", _dbl), ("shift", _dbl),
+        ("shift_lo", _i64), ("shift_hi", _i64), ("s_off", _i64), ("raw", C.c_int),
+    ]
+
+
 # name -> (restype, argtypes); mirrors include/bse200.h
 _SIGS = {
     "bse_version": (C.c_char_p, []),
@@ -67,6 +78,11 @@ _SIGS = {
     "bse_lanczos_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _dp, _dp, _ip]),
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
+    "bse_c64_tile_planes": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "bse_c64_tile_step": (C.c_int, [_vp, C.POINTER(C64TileArgs)]),
+    "bse_c64_split": (C.c_int, [_vp, _vp, _i64, _i64, _vp]),
+    "bse_c64_to_planes": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "bse_c64_from_planes": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "bse_chol_rinv": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _vp, _ip]),
     "bse_rr_pencil": (C.c_int, [_vp, _vp, _vp, _i64, _dp, _vp, _dp]),
     "bse_rr_backup_pencil": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _dp, _vp, _dp]),

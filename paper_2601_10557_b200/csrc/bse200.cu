@@ -745,45 +745,66 @@ CUtensorMap map3d(const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint
 
 inline int64_t pad4(int64_t m) { return (m + 3) & ~int64_t(3); }
 
-// P planes: 4 x [m rows][2 mp] fp32;  view (j < m, row i, part) -> strides (2 mp * 4, mp * 4)
-void c64_p_maps(bse::c64::Maps& mp_, const float* pplanes, int64_t m) {
-  const int64_t mp = pad4(m), plane = m * 2 * mp;
+// P planes: 4 x [mo rows][2 mpi] fp32 (mpi = pad4(kc));  view (j < kc, row i < mo, part)
+void c64_p_maps(bse::c64::Maps& mp_, const float* pplanes, int64_t mo, int64_t kc) {
+  const int64_t mpi = pad4(kc), plane = mo * 2 * mpi;
   for (int q = 0; q < 4; ++q)
-    mp_.p[q] = map3d(pplanes + q * plane, m, m, 2, 2 * mp * 4, mp * 4, bse::c64::BKE, bse::c64::BM, 1);
+    mp_.p[q] = map3d(pplanes + q * plane, kc, mo, 2, 2 * mpi * 4, mpi * 4, bse::c64::BKE, bse::c64::BM, 1);
 }
 
-// X planes of one block: 8 x [k cols][2 mp] fp32;  view (j < m, half, col)
-void c64_x_maps(bse::c64::Maps& mp_, float* const planes[8], int64_t m, int64_t k) {
-  const int64_t mp = pad4(m);
+// X planes of one block: 8 x [k cols][2 mpi] fp32;  view (j < kc, half, col); rows >= kc zero-filled
+void c64_x_maps(bse::c64::Maps& mp_, const float* const planes[8], int64_t kc, int64_t k) {
+  const int64_t mpi = pad4(kc);
   for (int q = 0; q < 8; ++q)
-    mp_.x[q] = map3d(planes[q], m, 2, k, mp * 4, 2 * mp * 4, bse::c64::BKE, 1, bse::c64::BN);
+    mp_.x[q] = map3d(planes[q], kc, 2, k, mpi * 4, 2 * mpi * 4, bse::c64::BKE, 1, bse::c64::BN);
 }
 
-void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const float* pplanes, int64_t m, int64_t k, float* const x[8],
-              float* const prev[8], float* const out[8], double alpha, double beta, double shift) {
+struct C64Step {
+  int64_t mo, kc, k;
+  const float* x[8];     // input planes (input layout)
+  const float* prev[4];  // y_prev planes (output layout), null: beta = 0
+  float* out[8];         // output planes, or raw (out[0] = Re, out[1] = Im)
+  double alpha, beta, shift;
+  int64_t shift_lo, shift_hi, s_off;
+  bool raw;
+};
+
+void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const C64Step& st) {
   static bool configured = false;
   if (!configured) {
     CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bse::c64::SMEM));
     configured = true;
   }
-  c64_x_maps(maps, x, m, k);
+  c64_x_maps(maps, st.x, st.kc, st.k);
   bse::c64::StepArgs a{};
-  a.m = (int)m;
-  a.mp = (int)pad4(m);
-  a.k = (int)k;
+  a.mo = (int)st.mo;
+  a.mpo = (int)pad4(st.mo);
+  a.kc = (int)st.kc;
+  a.mpi = (int)pad4(st.kc);
+  a.k = (int)st.k;
   a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
   for (int q = 0; q < 4; ++q) {
-    a.x[q] = x[q];
-    a.p[q] = prev ? prev[q] : nullptr;
+    a.x[q] = st.x[q];
+    a.p[q] = st.prev[q];
   }
-  for (int q = 0; q < 8; ++q) a.out[q] = out[q];
-  a.alpha = (float)alpha;
-  a.beta = prev ? (float)beta : 0.f;
-  a.shift = (float)shift;
-  dim3 grid((unsigned)((k + bse::c64::BN - 1) / bse::c64::BN), (unsigned)((m + bse::c64::BM - 1) / bse::c64::BM));
+  for (int q = 0; q < 8; ++q) a.out[q] = st.out[q];
+  a.alpha = (float)st.alpha;
+  a.beta = st.prev[0] ? (float)st.beta : 0.f;
+  a.shift = (float)st.shift;
+  a.shift_lo = (int)st.shift_lo;
+  a.shift_hi = (int)st.shift_hi;
+  a.s_off = (int)st.s_off;
+  a.raw = st.raw ? 1 : 0;
+  dim3 grid((unsigned)((st.k + bse::c64::BN - 1) / bse::c64::BN), (unsigned)((st.mo + bse::c64::BM - 1) / bse::c64::BM));
   bse::c64::step_kernel<<<grid, bse::c64::THREADS, bse::c64::SMEM, ctx->stream>>>(maps, a);
   check_launch(ctx);
+}
+
+// the 8 planes of a plane set: consecutive blocks of 2 pad4(rows) k floats
+void plane_set(float* base, int64_t rows, int64_t k, float* (&q)[8]) {
+  const int64_t blk = 2 * pad4(rows) * k;
+  for (int i = 0; i < 8; ++i) q[i] = base + i * blk;
 }
 
 }  // namespace
@@ -1385,8 +1406,95 @@ int bse_c64_prepare(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void
     if (m <= 0) return;
     const int64_t mp = pad4(m), plane = m * 2 * mp;
     float* pl = static_cast<float*>(d_pplanes);
+    const zval* ab = static_cast<const zval*>(d_ab);
     bse::c64::p_planes_kernel<<<grid1d(plane, 256, 148 * 32), 256, 0, ctx->stream>>>(
-        static_cast<const zval*>(d_ab), lda, (int)m, (int)mp, pl, pl + plane, pl + 2 * plane, pl + 3 * plane);
+        ab, ab + m * lda, lda, (int)m, (int)m, (int)mp, pl, pl + plane, pl + 2 * plane, pl + 3 * plane);
+    check_launch(ctx);
+  });
+}
+
+int bse_c64_tile_planes(bse_ctx* ctx, const void* d_src_a, const void* d_src_b, int64_t lds, int64_t mo, int64_t kc,
+                        void* d_pplanes) {
+  return guarded(ctx, [&] {
+    if (mo <= 0 || kc <= 0) return;
+    if (lds < kc) throw BseError(BSE_EVALIDATION, "bad shapes");
+    const int64_t mp = pad4(kc), plane = mo * 2 * mp;
+    float* pl = static_cast<float*>(d_pplanes);
+    bse::c64::p_planes_kernel<<<grid1d(plane, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        static_cast<const zval*>(d_src_a), static_cast<const zval*>(d_src_b), lds, (int)mo, (int)kc, (int)mp, pl,
+        pl + plane, pl + 2 * plane, pl + 3 * plane);
+    check_launch(ctx);
+  });
+}
+
+int bse_c64_tile_step(bse_ctx* ctx, const bse_c64_tile_args* t) {
+  return guarded(ctx, [&] {
+    if (!t) throw BseError(BSE_EVALIDATION, "null args");
+    if (t->k <= 0 || t->mo <= 0) return;
+    if (t->kc <= 0) throw BseError(BSE_EVALIDATION, "bad shapes");
+    C64Step st{};
+    st.mo = t->mo;
+    st.kc = t->kc;
+    st.k = t->k;
+    float* xs[8];
+    plane_set(static_cast<float*>(const_cast<void*>(t->x)), t->kc, t->k, xs);
+    for (int q = 0; q < 8; ++q) st.x[q] = xs[q];
+    float* ps[8];
+    if (t->prev && t->beta != 0.0) {
+      plane_set(static_cast<float*>(const_cast<void*>(t->prev)), t->mo, t->k, ps);
+      for (int q = 0; q < 4; ++q) st.prev[q] = ps[q];
+    }
+    float* os[8];
+    plane_set(static_cast<float*>(t->out), t->mo, t->k, os);
+    for (int q = 0; q < 8; ++q) st.out[q] = os[q];
+    st.alpha = t->alpha;
+    st.beta = t->beta;
+    st.shift = t->shift;
+    st.shift_lo = t->shift_lo;
+    st.shift_hi = t->shift_hi;
+    st.s_off = t->s_off;
+    st.raw = t->raw != 0;
+    bse::c64::Maps maps;
+    c64_p_maps(maps, static_cast<const float*>(t->pplanes), t->mo, t->kc);
+    c64_step(ctx, maps, st);
+  });
+}
+
+int bse_c64_split(bse_ctx* ctx, const void* d_raw, int64_t rows, int64_t k, void* d_planes) {
+  return guarded(ctx, [&] {
+    if (rows <= 0 || k <= 0) return;
+    const int64_t blk = 2 * pad4(rows) * k;
+    const float* raw = static_cast<const float*>(d_raw);
+    float* os[8];
+    plane_set(static_cast<float*>(d_planes), rows, k, os);
+    bse::c64::Planes8 q;
+    for (int i = 0; i < 8; ++i) q.p[i] = os[i];
+    bse::c64::split_planes_kernel<<<grid1d(blk, 256, 148 * 32), 256, 0, ctx->stream>>>(raw, raw + blk, (int)rows,
+                                                                                       (int)pad4(rows), (int)k, q);
+    check_launch(ctx);
+  });
+}
+
+int bse_c64_to_planes(bse_ctx* ctx, const void* d_v, int64_t ldv, int64_t rows, int64_t k, void* d_planes) {
+  return guarded(ctx, [&] {
+    if (rows <= 0 || k <= 0) return;
+    float* os[8];
+    plane_set(static_cast<float*>(d_planes), rows, k, os);
+    bse::c64::Planes8 q;
+    for (int i = 0; i < 8; ++i) q.p[i] = os[i];
+    bse::c64::to_planes_kernel<<<grid1d(2 * pad4(rows) * k, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        static_cast<const zval*>(d_v), ldv, (int)rows, (int)pad4(rows), (int)k, q);
+    check_launch(ctx);
+  });
+}
+
+int bse_c64_from_planes(bse_ctx* ctx, const void* d_planes, int64_t rows, int64_t k, void* d_v, int64_t ldv) {
+  return guarded(ctx, [&] {
+    if (rows <= 0 || k <= 0) return;
+    float* os[8];
+    plane_set(static_cast<float*>(const_cast<void*>(d_planes)), rows, k, os);
+    bse::c64::from_planes_kernel<<<grid1d(2 * rows * k, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        os[0], os[1], os[2], os[3], (int)rows, (int)pad4(rows), (int)k, static_cast<zval*>(d_v), ldv);
     check_launch(ctx);
   });
 }
@@ -1408,17 +1516,31 @@ int bse_chebyshev_filter_c64(bse_ctx* ctx, const void* d_pplanes, int64_t m, voi
         static_cast<const zval*>(d_v), ldv, (int)m, (int)mp, (int)k, p0);
     check_launch(ctx);
     bse::c64::Maps maps;
-    c64_p_maps(maps, static_cast<const float*>(d_pplanes), m);
+    c64_p_maps(maps, static_cast<const float*>(d_pplanes), m, m);
+    auto step_on = [&](int in, int pv, int out, double alpha, double beta) {
+      C64Step st{};
+      st.mo = st.kc = m;
+      st.k = k;
+      for (int q = 0; q < 8; ++q) st.x[q] = bufs[in][q];
+      for (int q = 0; q < 4; ++q) st.prev[q] = pv >= 0 ? bufs[pv][q] : nullptr;
+      for (int q = 0; q < 8; ++q) st.out[q] = bufs[out][q];
+      st.alpha = alpha;
+      st.beta = beta;
+      st.shift = c;
+      st.shift_lo = 0;
+      st.shift_hi = m;
+      st.s_off = 0;
+      c64_step(ctx, maps, st);
+    };
     // chebyshev.py:58-74 on three rotating plane blocks
     const double sigma1 = e / (s - c);
     double sigma = sigma1;
     int prev = 0, cur = 1;
-    c64_step(ctx, maps, static_cast<const float*>(d_pplanes), m, k, bufs[0], nullptr, bufs[1], sigma1 / e, 0.0, c);
+    step_on(0, -1, 1, sigma1 / e, 0.0);
     for (int step = 2; step <= deg; ++step) {
       const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
       const int nxt = 3 - prev - cur;
-      c64_step(ctx, maps, static_cast<const float*>(d_pplanes), m, k, bufs[cur], bufs[prev], bufs[nxt],
-               2.0 * sigma_new / e, sigma * sigma_new, c);
+      step_on(cur, prev, nxt, 2.0 * sigma_new / e, sigma * sigma_new);
       prev = cur;
       cur = nxt;
       sigma = sigma_new;

@@ -63,13 +63,19 @@ struct Maps {
 };
 
 struct StepArgs {
-  int m, mp, k;            // rows per half, padded half stride (multiple of 4), columns
+  int mo, mpo;             // output rows per half, their padded half stride (multiple of 4)
+  int kc, mpi;             // contraction length per part (= input rows per half), input half stride
+  int k;                   // columns
   int skip_b;              // B == 0: contract over the A part only
-  // planes (fp32, column-major n x k with ld = 2 mp, lower half at row mp)
-  const float* x[4];       // step input y (hi/lo, re/im) - shift operand
-  const float* p[4];       // y_prev (may alias out)
-  float* out[8];           // y_next (hi/lo, re/im, then the negated planes)
+  // planes (fp32, column-major with ld = 2 mp, lower half at row mp)
+  const float* x[4];       // step input y (hi/lo, re/im; input layout) - shift operand
+  const float* p[4];       // y_prev (output layout; may alias out)
+  float* out[8];           // y_next (hi/lo, re/im, then the negated planes); raw: out[0] = Re, out[1] = Im
   float alpha, beta, shift;
+  // the shift applies to output rows [shift_lo, shift_hi) with input row = output row + s_off
+  // (a tile of the 2D grid: only the rows its input block shares with its output block)
+  int shift_lo, shift_hi, s_off;
+  int raw;                 // write unsplit fp32 partials (summed across the grid before the split)
 };
 
 __device__ __forceinline__ float tf32_hi(float x) {
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int c0 = blockIdx.x * BN, i0 = blockIdx.y * BM;
-  const int nk_part = (a.m + BKE - 1) / BKE;
+  const int nk_part = (a.kc + BKE - 1) / BKE;
   const int nk = a.skip_b ? nk_part : 2 * nk_part;
   const int nchunks = (nk + CHUNK - 1) / CHUNK;
 
@@ -235,19 +241,21 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
     }
     // y+ = alpha (H y - c y) - beta y-   with  H y = [U ; -L']
     const int row = i0 + quad * 32 + lane;
-    const int64_t ld = 2 * (int64_t)a.mp;
-    if (row < a.m) {
+    const int64_t ld = 2 * (int64_t)a.mpo, ldi = 2 * (int64_t)a.mpi;
+    const bool shifted = a.shift != 0.f && row >= a.shift_lo && row < a.shift_hi;
+    if (row < a.mo) {
 #pragma unroll 4
       for (int c = 0; c < 32; ++c) {
         const int col = c0 + colh * 32 + c;
         if (col >= a.k) break;
-        const int64_t up = (int64_t)col * ld + row, lo = up + a.mp;
+        const int64_t up = (int64_t)col * ld + row, lo = up + a.mpo;
         float hur = acc[0][c], hui = acc[1][c], hlr = -acc[2][c], hli = -acc[3][c];
-        if (a.shift != 0.f) {
-          hur -= a.shift * (a.x[0][up] + a.x[1][up]);
-          hui -= a.shift * (a.x[2][up] + a.x[3][up]);
-          hlr -= a.shift * (a.x[0][lo] + a.x[1][lo]);
-          hli -= a.shift * (a.x[2][lo] + a.x[3][lo]);
+        if (shifted) {
+          const int64_t xu = (int64_t)col * ldi + row + a.s_off, xl = xu + a.mpi;
+          hur -= a.shift * (a.x[0][xu] + a.x[1][xu]);
+          hui -= a.shift * (a.x[2][xu] + a.x[3][xu]);
+          hlr -= a.shift * (a.x[0][xl] + a.x[1][xl]);
+          hli -= a.shift * (a.x[2][xl] + a.x[3][xl]);
         }
         float yur = a.alpha * hur, yui = a.alpha * hui, ylr = a.alpha * hlr, yli = a.alpha * hli;
         if (a.beta != 0.f) {
@@ -256,8 +264,15 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
           ylr -= a.beta * (a.p[0][lo] + a.p[1][lo]);
           yli -= a.beta * (a.p[2][lo] + a.p[3][lo]);
         }
-        store_planes(a.out, up, yur, yui);
-        store_planes(a.out, lo, ylr, yli);
+        if (a.raw) {
+          a.out[0][up] = yur;
+          a.out[1][up] = yui;
+          a.out[0][lo] = ylr;
+          a.out[1][lo] = yli;
+        } else {
+          store_planes(a.out, up, yur, yui);
+          store_planes(a.out, lo, ylr, yli);
+        }
       }
     }
   }
@@ -267,21 +282,25 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
 }
 
 // ---------------------------------------------------------------- layout conversions
-// P planes from [A | B] (complex128, column-major m x 2m, lda): plane[q][i * (2 mp) + part * mp + j]
-// = hi/lo of Re/Im P[i, part m + j], with P rows of A read as conj(column i) (A hermitian) and
-// rows of B as column i (B symmetric): coalesced reads and writes.
-__global__ void p_planes_kernel(const zval* __restrict__ ab, int64_t lda, int m, int mp, float* __restrict__ pl0,
-                                float* __restrict__ pl1, float* __restrict__ pl2, float* __restrict__ pl3) {
-  const int64_t total = (int64_t)m * 2 * mp;
+// P planes of an operator tile with output rows i < mo and contraction index j < kc per part:
+// plane[q][i * (2 mp) + part * mp + j] = hi/lo of Re/Im P[i, part, j], mp = pad4(kc).  The rows are
+// read as columns of the *transposed* blocks src_a / src_b (column-major, leading dim lds, column i
+// = entries j): P_A[i, j] = conj(src_a[j, i]) (A^H block), P_B[i, j] = src_b[j, i] (B^T block).
+// One GPU: src = [A | B] itself (A hermitian, B symmetric); 2D grid: the fwd tile's planes come
+// from the trn tile's columns and vice versa.  Coalesced reads and writes.
+__global__ void p_planes_kernel(const zval* __restrict__ src_a, const zval* __restrict__ src_b, int64_t lds, int mo,
+                                int kc, int mp, float* __restrict__ pl0, float* __restrict__ pl1,
+                                float* __restrict__ pl2, float* __restrict__ pl3) {
+  const int64_t total = (int64_t)mo * 2 * mp;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx / (2 * mp);
     const int J = int(idx % (2 * mp));
     const int part = J >= mp, j = J - part * mp;
     float re = 0.f, im = 0.f;
-    if (j < m) {
-      const zval v = ab[(int64_t)(part * m + i) * lda + j];  // column i of A (or B), entry j
+    if (j < kc) {
+      const zval v = (part ? src_b : src_a)[i * lds + j];  // column i of the transposed block, entry j
       re = (float)v.re;
-      im = part ? (float)v.im : -(float)v.im;  // row i of A = conj(column i)
+      im = part ? (float)v.im : -(float)v.im;
     }
     const float rh = tf32_hi(re), ih = tf32_hi(im);
     pl0[idx] = rh;
@@ -309,6 +328,17 @@ __global__ void to_planes_kernel(const zval* __restrict__ v, int64_t ldv, int m,
       im = (float)z.im;
     }
     store_planes(q.p, idx, re, im);
+  }
+}
+
+// raw fp32 (re, im) partial sums (ld = 2 mp) -> the 8 hi/lo planes of the next step's input
+__global__ void split_planes_kernel(const float* __restrict__ re, const float* __restrict__ im, int m, int mp, int k,
+                                    Planes8 q) {
+  const int64_t ld = 2 * (int64_t)mp, total = ld * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = int(idx % ld);
+    const int rr = r >= mp ? r - mp : r;
+    store_planes(q.p, idx, rr < m ? re[idx] : 0.f, rr < m ? im[idx] : 0.f);
   }
 }
 

@@ -201,6 +201,49 @@ class CudaOps:
         args.filter = 1 if filter else 0
         self.ctx.call("bse_hop_tile", ctypes.byref(args))
 
+    # ---- complex64 filter (tcgen05, c64.cuh): plane sets of 8 fp32 planes ----------------------
+    @staticmethod
+    def _pad4(rows: int) -> int:
+        return (rows + 3) // 4 * 4
+
+    def c64_planes(self, rows: int, k: int):
+        """Plane set of a (k, 2 rows) block: 8 x 2 pad4(rows) k fp32."""
+        return self.torch.empty(8 * 2 * self._pad4(rows) * k, dtype=self.torch.float32, device=self.device)
+
+    def c64_raw(self, rows: int, k: int):
+        """Unsplit fp32 (Re, Im) planes of a (k, 2 rows) block, the allreduce payload."""
+        return self.torch.empty(2 * 2 * self._pad4(rows) * k, dtype=self.torch.float32, device=self.device)
+
+    def c64_raw_view(self, raw, rows: int, k: int):
+        return raw[:2 * 2 * self._pad4(rows) * k]
+
+    def c64_tile_planes(self, tile, src):
+        """P planes of `tile` (mo = tile.mr, kc = tile.kc) from the columns of its transposed tile."""
+        pl = self.torch.empty(4 * tile.mr * 2 * self._pad4(tile.kc), dtype=self.torch.float32, device=self.device)
+        self.ctx.call("bse_c64_tile_planes", src.pa, src.pb, src.lda, tile.mr, tile.kc, pl.data_ptr())
+        return pl
+
+    def c64_to_planes(self, v, rows: int, planes):
+        self.ctx.call("bse_c64_to_planes", v.data_ptr(), v.stride(0), rows, v.shape[0], planes.data_ptr())
+
+    def c64_from_planes(self, planes, rows: int, v):
+        self.ctx.call("bse_c64_from_planes", planes.data_ptr(), rows, v.shape[0], v.data_ptr(), v.stride(0))
+
+    def c64_step(self, pplanes, tile, k: int, x, out, *, alpha, shift, shift_rows, s_off, beta=0.0, prev=None):
+        """raw out = alpha (tile product of x - shift x on shift_rows) - beta prev (unsplit fp32)."""
+        a = _lib.C64TileArgs()
+        a.pplanes, a.mo, a.kc, a.k = pplanes.data_ptr(), tile.mr, tile.kc, k
+        a.x, a.out = x.data_ptr(), out.data_ptr()
+        a.prev = prev.data_ptr() if (prev is not None and beta != 0.0) else None
+        a.alpha, a.beta, a.shift = alpha, beta, shift
+        lo, hi = shift_rows
+        a.shift_lo, a.shift_hi, a.s_off = (lo, hi, s_off) if hi > lo else (0, 0, 0)
+        a.raw = 1
+        self.ctx.call("bse_c64_tile_step", ctypes.byref(a))
+
+    def c64_split(self, raw, rows: int, k: int, planes):
+        self.ctx.call("bse_c64_split", raw.data_ptr(), rows, k, planes.data_ptr())
+
     def gram(self, a, b):
         """a^H b for storage blocks with equal rows -> (k2, k1) storage of the k1 x k2 result."""
         k1, rows = a.shape
@@ -434,6 +477,46 @@ class DistSolver:
             for ev in reduced:
                 comp.wait_event(ev)
         return v_col  # even degree: the result is back in the col buffer
+
+    def chebyshev_c64(self, v_col, cfg: FilterConfig):
+        """p(H) v in place (col layout) with the complex64 tcgen05 filter (c64.cuh) on the 2D grid.
+        Each step: the tile product writes unsplit fp32 partials (the -beta Y_prev term on the
+        reduction group's owner, the shift on the rows the tile's input and output blocks share),
+        one fp32 allreduce over the row / column communicator, then the split into the hi/lo
+        planes the next step's TMA boxes read.  chebyshev.py:58-74, as chebyshev() above."""
+        g = self.g
+        ops = self.ops
+        k = v_col.shape[0]
+        if not hasattr(self, "_c64_pl"):
+            self._c64_pl = (ops.c64_tile_planes(self.fwd, self.trn), ops.c64_tile_planes(self.trn, self.fwd))
+        pl_fwd, pl_trn = self._c64_pl
+        col, row = ops.c64_planes(g.nc, k), ops.c64_planes(g.nr, k)
+        raw = ops.c64_raw(max(g.nr, g.nc), k)
+        ops.c64_to_planes(v_col, g.nc, col)
+        lo, hi = g.diag
+        c, e = cfg.center, cfg.half_width
+        s1 = e / (cfg.scale_ref - c)
+        s = s1
+        for step in range(1, cfg.degree + 1):
+            fwd = step % 2 == 1
+            if step == 1:
+                alpha, beta = s1 / e, 0.0
+            else:
+                sn = 1.0 / (2.0 / s1 - s)
+                alpha, beta = 2.0 * sn / e, (s * sn) if self._beta_owner(step) else 0.0
+                s = sn
+            if fwd:  # col -> row: rows R_I, contraction over C_J, summed over the row communicator
+                tile, pl, x, out, rows = self.fwd, pl_fwd, col, row, g.nr
+                shift_rows, s_off, reduce = (lo - g.r0, hi - g.r0), g.r0 - g.c0, self.c.sum_row
+            else:
+                tile, pl, x, out, rows = self.trn, pl_trn, row, col, g.nc
+                shift_rows, s_off, reduce = (lo - g.c0, hi - g.c0), g.c0 - g.r0, self.c.sum_col
+            ops.c64_step(pl, tile, k, x, raw, alpha=alpha, shift=c, shift_rows=shift_rows, s_off=s_off, beta=beta,
+                         prev=out if beta != 0.0 else None)
+            reduce(ops.c64_raw_view(raw, rows, k))
+            ops.c64_split(raw, rows, k, out)
+        ops.c64_from_planes(col, g.nc, v_col)  # even degree: back in the col layout
+        return v_col
 
     def _step_async(self, src, dst, fwd, kw, comp, prev_event):
         """One chunk step: tile GEMM on the compute stream (after the chunk's previous reduction),
@@ -676,14 +759,24 @@ class DistSolver:
         locked = self.ops.empty(nev, 2 * g.nc)
         nlock, lvals, lres, trace = 0, [], [], []
         converged, it_used, current, backups = False, 0, bounds, 0
+        from .solver import MIXED_SWITCH, mixed_precision
+
+        mixed, base_precision, filter_precisions = mixed_precision(), _lib.filter_precision(), []
         lam = res = act = None
         for it in range(1, cfg.maxiter + 1):
             it_used = it
             before = ledger.total_flops()
             k = nevex - nlock
             fcfg = FilterConfig.from_bounds(current, cfg.deg, cfg.plain_kernel_only)
+            # precision policy of solver.py (complex64 filter, or the opt-in mixed policy)
+            use_c64 = base_precision == "c64" or (
+                mixed and (not trace or trace[-1].min_res_unlocked > MIXED_SWITCH * abs(bounds.mu_1)))
+            filter_precisions.append("c64" if use_c64 else "c128")
             with ledger.timing("filter"):
-                self.chebyshev(v, fcfg, row_buf)
+                if use_c64:
+                    self.chebyshev_c64(v, fcfg)
+                else:
+                    self.chebyshev(v, fcfg, row_buf)
             ledger.add_flops("filter", cfg.deg * 8.0 * n * n * k)
             with ledger.timing("ortho"):
                 v, _ = self.s_orthonormalize(v, locked[:nlock] if nlock else None)
@@ -733,8 +826,10 @@ class DistSolver:
         order = np.argsort(vals, kind="stable")[:nev]
         full = self.assemble_from_col(blocks[torch.as_tensor(order, device=blocks.device)].contiguous())
         st.mark("sort + assemble V", nev)
-        return SolveResult(lambdas=vals[order], v=full, residual_norms=resid[order], iterations_used=it_used,
-                           converged=converged, trace=trace, bounds=bounds, ledger=ledger, backup_events=backups)
+        out = SolveResult(lambdas=vals[order], v=full, residual_norms=resid[order], iterations_used=it_used,
+                          converged=converged, trace=trace, bounds=bounds, ledger=ledger, backup_events=backups)
+        out.filter_precisions = filter_precisions
+        return out
 
 
 def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):

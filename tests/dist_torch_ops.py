@@ -39,6 +39,36 @@ class TorchOps:
         y[:, :mr] = up.T
         y[:, mr:2 * mr] = low.T
 
+    # complex64 filter emulation (dist.DistSolver.chebyshev_c64): a "plane set" is a complex64
+    # (k, 2 rows) block, the product is formed in complex128 and rounded to complex64 like the
+    # fp32 tile product; the raw buffer is a flat complex64 array (contiguous views for gloo)
+    def c64_planes(self, rows, k):
+        return torch.empty((k, 2 * rows), dtype=torch.complex64)
+
+    def c64_raw(self, rows, k):
+        return torch.empty(k * 2 * rows, dtype=torch.complex64)
+
+    def c64_raw_view(self, raw, rows, k):
+        return raw[:k * 2 * rows].view(k, 2 * rows)
+
+    def c64_tile_planes(self, tile, src):
+        return tile
+
+    def c64_to_planes(self, v, rows, planes):
+        planes.copy_(v.to(torch.complex64))
+
+    def c64_from_planes(self, planes, rows, v):
+        v.copy_(planes.to(torch.complex128))
+
+    def c64_step(self, pplanes, tile, k, x, out, *, alpha, shift, shift_rows, s_off, beta=0.0, prev=None):
+        y = torch.empty((k, 2 * tile.mr), dtype=torch.complex128)
+        self.hop(tile, x.to(torch.complex128), y, alpha=alpha, shift=shift, shift_rows=shift_rows, s_off=s_off,
+                 beta=beta, p=prev.to(torch.complex128) if prev is not None else None)
+        self.c64_raw_view(out, tile.mr, k).copy_(y.to(torch.complex64))
+
+    def c64_split(self, raw, rows, k, planes):
+        planes.copy_(self.c64_raw_view(raw, rows, k))
+
     def gram(self, a, b):
         return (a.conj() @ b.T).T.contiguous()  # storage (k2, k1) of a^H b
 

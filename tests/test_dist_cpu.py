@@ -82,3 +82,45 @@ def test_grid_shapes_and_diag_cover():
                     lo, hi = gr.diag
                     cover[lo:hi] += 1
                 assert (cover[gr.r0:gr.r1] == 1).all() and cover.sum() == gr.nr
+
+
+def _c64_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from dist_torch_ops import TorchOps
+    from paper_2601_10557_b200 import rng
+    from paper_2601_10557_b200.chebyshev import FilterConfig
+    from paper_2601_10557_b200.dist import DistributedSolver, start_block_col
+    from paper_2601_10557_b200.metrics import PhaseLedger
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.set_num_threads(1)
+    a, b = golden_ham(48, 12)
+    ops = TorchOps()
+    ds = DistributedSolver((a, b), device=torch.device("cpu"), ops=ops)
+    inner = ds.inner
+    g = inner.g
+    bounds = inner.lanczos(12, 24, rng.substream(12, 2), PhaseLedger())
+    fcfg = FilterConfig.from_bounds(bounds, 10, False)
+    v = start_block_col(rng.substream(12, 3), 96, 12, g, ops)
+    v64 = v.clone()
+    inner.chebyshev(v, fcfg, ops.empty(12, 2 * g.nr))
+    inner.chebyshev_c64(v64, fcfg)
+    f128, f64 = inner.assemble_from_col(v), inner.assemble_from_col(v64)
+    if rank == 0:
+        np.savez(out, f128=f128.numpy(), f64=f64.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_distributed_c64_filter_matches_fp64(tmp_path, world):
+    """dist.DistSolver.chebyshev_c64 (raw partials -> allreduce -> split, beta on the reduction
+    group's owner, shift on the diagonal rows) against the FP64 distributed filter: equal to the
+    complex64 rounding of each step (deg 10, columns scaled by their norm)."""
+    out = str(tmp_path / "c.npz")
+    mp.spawn(_c64_worker, args=(world, _port(), out), nprocs=world, join=True)
+    r = np.load(out)
+    f128, f64 = r["f128"], r["f64"]
+    err = np.abs(f64 - f128).max(axis=1) / np.abs(f128).max(axis=1)
+    assert err.max() <= 2e-5, err.max()

@@ -51,3 +51,37 @@ def test_start_block_device_policy_matches_host():
         got = start_block_col(seed, n, cols, g, ops).cpu().numpy()  # (cols, 2 nc) storage
         rows = np.concatenate([np.arange(g.c0, g.c1), m + np.arange(g.c0, g.c1)])
         assert np.abs(got - host[rows].T).max() <= 1e-14 * np.abs(host).max()
+
+
+def test_dist_c64_filter_matches_single_gpu_c64():
+    """DistSolver.chebyshev_c64 on one GPU (tile kernel in raw mode, split, the grid's planes built
+    from the transposed tile) is bitwise the single-GPU complex64 filter (bse_chebyshev_filter_c64),
+    and within the FP32 accuracy of the FP64 filter."""
+    from paper_2601_10557_b200 import rng
+    from paper_2601_10557_b200.chebyshev import FilterConfig, filter_inplace
+    from paper_2601_10557_b200 import BseHamiltonian, _lib
+    from paper_2601_10557_b200.dist import DistributedSolver
+    from paper_2601_10557_b200.hamiltonian import colmajor_empty
+
+    dev = torch.device("cuda", 0)
+    a, b = golden_ham(64, 21)
+    m, n, k = 64, 128, 70
+    ham = BseHamiltonian(a, b)
+    fcfg = FilterConfig(10, 300.0, 250.0, -600.0)
+    v0 = torch.from_numpy(rng.complex_normal_matrix(rng.substream(5, 3), n, k)).to(dev)
+    single = colmajor_empty(n, k, dev)
+    single.copy_(v0)
+    prec = _lib.filter_precision()
+    try:
+        _lib.set_filter_precision("c64")
+        filter_inplace(ham, single, fcfg)
+    finally:
+        _lib.set_filter_precision(prec)
+    ds = DistributedSolver((a, b), device=dev)
+    vd = v0.T.contiguous()  # (k, n) storage = col layout at world 1
+    ds.inner.chebyshev_c64(vd, fcfg)
+    assert torch.equal(vd.T.cpu(), single.cpu())
+    v128 = v0.T.contiguous()
+    ds.inner.chebyshev(v128, fcfg, ds.inner.ops.empty(k, n))
+    err = ((vd - v128).abs().amax(dim=1) / v128.abs().amax(dim=1)).max().item()
+    assert err <= 2e-5, err

@@ -49,6 +49,40 @@ def main():
             fails += not ok
             print(f"[world {world}] {key}: iters {res.iterations_used}/{int(g['iterations_used'])} "
                   f"max rel dlambda {rel:.2e} subspace {ov:.2e} {'OK' if ok else 'FAIL'}", flush=True)
+    # complex64 filter on the grid (raw partials -> fp32 allreduce -> split) vs the FP64 filter
+    from paper_2601_10557_b200 import rng as _rng
+    from paper_2601_10557_b200.chebyshev import FilterConfig
+    from paper_2601_10557_b200.dist import DistributedSolver, start_block_col
+
+    a, b = golden_ham(64, 21)
+    ds = DistributedSolver((a, b), device=dev)
+    fcfg = FilterConfig(10, 300.0, 250.0, -600.0)
+    v = start_block_col(_rng.substream(5, 3), 128, 70, ds.inner.g, ds.inner.ops)
+    v64 = v.clone()
+    ds.inner.chebyshev(v, fcfg, ds.inner.ops.empty(70, 2 * ds.inner.g.nr))
+    ds.inner.chebyshev_c64(v64, fcfg)
+    f128, f64 = ds.inner.assemble_from_col(v), ds.inner.assemble_from_col(v64)
+    if rank == 0:
+        err = float(((f64 - f128).abs().amax(dim=1) / f128.abs().amax(dim=1)).max())
+        ok = err <= 2e-5
+        fails += not ok
+        print(f"[world {world}] c64 filter vs FP64 (m=64, deg 10): max rel {err:.2e} {'OK' if ok else 'FAIL'}",
+              flush=True)
+    # mixed-precision policy (complex64 filters while residuals are large) on the grid
+    from paper_2601_10557_b200.solver import set_mixed_precision
+
+    set_mixed_precision(True)
+    try:
+        a, b, g = rebuild_c1()
+        res = solve_distributed((a, b), SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0), device=dev)
+    finally:
+        set_mixed_precision(False)
+    if rank == 0:
+        rel = float(np.max(np.abs(res.lambdas - g["abs_lambdas"]) / np.abs(g["abs_lambdas"])))
+        ok = rel <= 1e-10 and res.converged and res.residual_norms.max() <= 1e-10 and "c64" in res.filter_precisions
+        fails += not ok
+        print(f"[world {world}] C1 mixed policy: iters {res.iterations_used} filters {''.join(p[1] for p in res.filter_precisions)} "
+              f"max rel dlambda {rel:.2e} {'OK' if ok else 'FAIL'}", flush=True)
     a, b, g = rebuild_c1()
     res = solve_distributed((a, b), SolverConfig(nev=50, nex=20, deg=20, tol=1e-10, seed=0), device=dev)
     if rank == 0:
