@@ -769,11 +769,20 @@ struct C64Step {
   bool raw;
 };
 
+// CTA-pair (cta_group::2) variant of the c64 step for wide blocks: 13% faster at k = 1200, 5-7%
+// slower at k = 300-600 (profiles/r01/c64_pair_vs_single.txt).  BSE200_C64_PAIR=0 / 1 forces it.
+bool c64_pair(int64_t k) {
+  const char* v = std::getenv("BSE200_C64_PAIR");
+  return v && v[0] ? v[0] != '0' : k >= 900;
+}
+
 void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const C64Step& st) {
   static bool configured = false;
   if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)bse::c64::SMEM));
+    CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)bse::c64::PAIR_SMEM));
     configured = true;
   }
   c64_x_maps(maps, st.x, st.kc, st.k);
@@ -796,8 +805,26 @@ void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const C64Step& st) {
   a.shift_hi = (int)st.shift_hi;
   a.s_off = (int)st.s_off;
   a.raw = st.raw ? 1 : 0;
-  dim3 grid((unsigned)((st.k + bse::c64::BN - 1) / bse::c64::BN), (unsigned)((st.mo + bse::c64::BM - 1) / bse::c64::BM));
-  bse::c64::step_kernel<<<grid, bse::c64::THREADS, bse::c64::SMEM, ctx->stream>>>(maps, a);
+  const unsigned nt = (unsigned)((st.k + bse::c64::BN - 1) / bse::c64::BN);
+  const unsigned mt = (unsigned)((st.mo + bse::c64::BM - 1) / bse::c64::BM);
+  if (c64_pair(st.k)) {
+    // CTA pairs along x over the row tiles (an odd count gets one all-padding CTA)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((mt + 1) / 2 * 2, nt);
+    cfg.blockDim = dim3(bse::c64::THREADS);
+    cfg.dynamicSmemBytes = bse::c64::PAIR_SMEM;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_OK(cudaLaunchKernelEx(&cfg, bse::c64::step_kernel<true>, maps, a));
+  } else {
+    bse::c64::step_kernel<false><<<dim3(nt, mt), bse::c64::THREADS, bse::c64::SMEM, ctx->stream>>>(maps, a);
+  }
   check_launch(ctx);
 }
 

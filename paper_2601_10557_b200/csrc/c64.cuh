@@ -35,6 +35,60 @@ constexpr int STAGE_BYTES = 4 * PLANE_TILE_P + 4 * STACK;              // 80 KB
 constexpr int EPI_WARPS = 8;          // 2 per TMEM lane quadrant, 32 columns each
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
 constexpr size_t SMEM = 1024 + size_t(STAGES) * STAGE_BYTES + 256;
+// CTA-pair variant (cta_group::2, cluster 2 x 1 along M): the leader issues M = 256 UMMAs; each
+// CTA stages its own 128 P rows and only its half of every N = 128 window, i.e. stack tiles
+// [rank, rank + 1] -- 2 of the 3 -- so each SM's shared-memory operand reads per MMA drop from
+// 8 KB to 6 KB (the single-CTA kernel is bound by that port).
+constexpr int PAIR_STACK = 2 * PLANE_TILE_X;                           // 8 KB
+constexpr int PAIR_STAGE_BYTES = 4 * PLANE_TILE_P + 4 * PAIR_STACK;    // 64 KB
+constexpr int PAIR_STAGES = 3;
+constexpr size_t PAIR_SMEM = 1024 + size_t(PAIR_STAGES) * PAIR_STAGE_BYTES + 256;
+
+template <bool PAIR>
+struct Geo {
+  static constexpr int stages = PAIR ? PAIR_STAGES : STAGES;
+  static constexpr int stage_bytes = PAIR ? PAIR_STAGE_BYTES : STAGE_BYTES;
+  static constexpr int stack = PAIR ? PAIR_STACK : STACK;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// TMA into this CTA's shared memory, completing on the leader CTA's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];\n" ::"r"(tc::smem_addr(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(tc::smem_addr(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, bool acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc ? 1u : 0u));
+}
+// arrive on the barrier at this offset in both CTAs of the pair when the issued MMAs complete
+__device__ __forceinline__ void commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          tc::smem_addr(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+// arrive on the leader CTA's copy of this barrier
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, 0;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(tc::smem_addr(bar))
+      : "memory");
+}
 
 // K-major operand in the 64-byte swizzle canonical layout: rows of 64 B (16 fp32), 8-row groups
 // 512 B apart; tile base 512-byte aligned.
@@ -102,7 +156,10 @@ __device__ __forceinline__ void store_planes(float* const (&q)[8], int64_t idx, 
 // add: 1.6e-4 relative at K = 8000).  The K loop is therefore cut into chunks of CHUNK stages
 // accumulated in one of two TMEM buffers; the 8 epilogue warps drain each finished chunk into
 // round-to-nearest FP32 register accumulators while the MMA warp fills the other buffer.
+template <bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant__ Maps maps, const StepArgs a) {
+  using G = Geo<PAIR>;
+  constexpr int STAGES = G::stages, STAGE_BYTES = G::stage_bytes, STACK = G::stack;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -113,7 +170,9 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
   uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int c0 = blockIdx.x * BN, i0 = blockIdx.y * BM;
+  // single CTA: grid (column tiles, row tiles); pair: grid (row tiles (even), column tiles)
+  const int c0 = (PAIR ? blockIdx.y : blockIdx.x) * BN, i0 = (PAIR ? blockIdx.x : blockIdx.y) * BM;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const int nk_part = (a.kc + BKE - 1) / BKE;
   const int nk = a.skip_b ? nk_part : 2 * nk_part;
   const int nchunks = (nk + CHUNK - 1) / CHUNK;
@@ -125,7 +184,7 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
-      tc::mbar_init(&acc_empty[b], EPI_WARPS);
+      tc::mbar_init(&acc_empty[b], PAIR ? 2 * EPI_WARPS : EPI_WARPS);  // pair: both CTAs' drains (leader copy)
     }
     tc::fence_barrier_init();
     for (int q = 0; q < 4; ++q) {
@@ -133,9 +192,20 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
       tc::prefetch_tmap(&maps.x[q]);
     }
   }
-  if (warp == 0) tc::tmem_alloc(tslot, 512);  // 2 buffers x 4 accumulators x 64 fp32 columns
+  if (warp == 0) {  // 2 buffers x [U_r | U_i], [L'_r | L'_i] x 128 fp32 columns
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc::smem_addr(tslot)),
+                   "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::);
+    } else {
+      tc::tmem_alloc(tslot, 512);
+    }
+  }
   tc::fence_before_sync();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any remote use
+  else
+    __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tslot;
 
@@ -147,28 +217,35 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
         const int part = kb >= nk_part;
         const int j = (kb - part * nk_part) * BKE;
         tc::mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], PAIR ? 2 * STAGE_BYTES : STAGE_BYTES);
         unsigned char* st = base + s * STAGE_BYTES;
-        for (int q = 0; q < 4; ++q) tma_load_3d(st + q * PLANE_TILE_P, &maps.p[q], &full[s], j, i0, part);
+        auto load = [&](void* dst, const CUtensorMap* map, int x0, int x1, int x2) {
+          if constexpr (PAIR)
+            tma_load_3d_pair(dst, map, &full[s], x0, x1, x2);
+          else
+            tma_load_3d(dst, map, &full[s], x0, x1, x2);
+        };
+        for (int q = 0; q < 4; ++q) load(st + q * PLANE_TILE_P, &maps.p[q], j, i0, part);
         unsigned char* sx = st + 4 * PLANE_TILE_P;
         // Xa = half `part`, Xb = the other half (part 0: X1, X2; part 1: X2, X1)
         // plane index: re = 0 + hl, im = 2 + hl, -re = 4 + hl, -im = 6 + hl (hl: 0 hi, 1 lo)
+        // a stack: [-Xi | Xr | Xi], b stack: [Xr | Xi | -Xr]; a pair CTA holds stack tiles [rank, rank + 1]
         for (int hl = 0; hl < 2; ++hl) {
-          unsigned char* sa = sx + hl * STACK;        // a stack: [-Xi | Xr | Xi]
-          unsigned char* sb = sx + (2 + hl) * STACK;  // b stack: [Xr | Xi | -Xr]
-          tma_load_3d(sa, &maps.x[6 + hl], &full[s], j, part, c0);
-          tma_load_3d(sa + PLANE_TILE_X, &maps.x[0 + hl], &full[s], j, part, c0);
-          tma_load_3d(sa + 2 * PLANE_TILE_X, &maps.x[2 + hl], &full[s], j, part, c0);
-          tma_load_3d(sb, &maps.x[0 + hl], &full[s], j, 1 - part, c0);
-          tma_load_3d(sb + PLANE_TILE_X, &maps.x[2 + hl], &full[s], j, 1 - part, c0);
-          tma_load_3d(sb + 2 * PLANE_TILE_X, &maps.x[4 + hl], &full[s], j, 1 - part, c0);
+          const int a_pl[3] = {6 + hl, 0 + hl, 2 + hl}, b_pl[3] = {0 + hl, 2 + hl, 4 + hl};
+          unsigned char* sa = sx + hl * STACK;
+          unsigned char* sb = sx + (2 + hl) * STACK;
+          for (int t = 0; t < (PAIR ? 2 : 3); ++t) {
+            const int tile = t + (int)rank;
+            load(sa + t * PLANE_TILE_X, &maps.x[a_pl[tile]], j, part, c0);
+            load(sb + t * PLANE_TILE_X, &maps.x[b_pl[tile]], j, 1 - part, c0);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // -------------------------------------------------------------- MMA issuer
-      constexpr uint32_t idesc = tc::idesc_tf32(BM, 2 * BN, false, false);  // N = 128 windows
+    if (lane == 0 && rank == 0) {
+      // -------------------------------------------------------------- MMA issuer (pair: the leader)
+      constexpr uint32_t idesc = tc::idesc_tf32(PAIR ? 2 * BM : BM, 2 * BN, false, false);  // N = 128 windows
       for (int ch = 0; ch < nchunks; ++ch) {
         const int b = ch & 1;
         if (ch >= 2) tc::mbar_wait(&acc_empty[b], ((ch >> 1) - 1) & 1);
@@ -195,19 +272,31 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
             const uint64_t b_l0 = sdesc_k_sw64(sx + 3 * STACK + off), b_l1 = sdesc_k_sw64(sx + 3 * STACK + PLANE_TILE_X + off);
             const bool first = (kb == ch * CHUNK && kk == 0);
             // 3xTF32 real product  acc += (ph, pl) x (xh, xl)
+            auto mma = [&](uint32_t acc, uint64_t pa, uint64_t xb, bool accumulate) {
+              if constexpr (PAIR)
+                mma_tf32_pair(acc, pa, xb, idesc, accumulate);
+              else
+                tc::mma_tf32(acc, pa, xb, idesc, accumulate);
+            };
             auto prod = [&](uint32_t acc, uint64_t ph, uint64_t pl, uint64_t xh, uint64_t xl, bool init) {
-              tc::mma_tf32(acc, ph, xh, idesc, !init);
-              tc::mma_tf32(acc, ph, xl, idesc, true);
-              tc::mma_tf32(acc, pl, xh, idesc, true);
+              mma(acc, ph, xh, !init);
+              mma(acc, ph, xl, true);
+              mma(acc, pl, xh, true);
             };
             prod(acc_u, prh, prl, a_h1, a_l1, first);  // Pr [Xar | Xai]
             prod(acc_u, pih, pil, a_h0, a_l0, false);  // Pi [-Xai | Xar]
             prod(acc_l, prh, prl, b_h0, b_l0, first);  // Pr [Xbr | Xbi]
             prod(acc_l, pih, pil, b_h1, b_l1, false);  // Pi [Xbi | -Xbr]
           }
-          tc::mma_commit(&empty[s]);
+          if constexpr (PAIR)
+            commit_pair(&empty[s]);
+          else
+            tc::mma_commit(&empty[s]);
         }
-        tc::mma_commit(&acc_full[b]);
+        if constexpr (PAIR)
+          commit_pair(&acc_full[b]);
+        else
+          tc::mma_commit(&acc_full[b]);
       }
     }
   } else {
@@ -237,7 +326,12 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
       }
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&acc_empty[b]);
+      if (lane == 0) {
+        if constexpr (PAIR)
+          arrive_leader(&acc_empty[b]);
+        else
+          tc::mbar_arrive(&acc_empty[b]);
+      }
     }
     // y+ = alpha (H y - c y) - beta y-   with  H y = [U ; -L']
     const int row = i0 + quad * 32 + lane;
@@ -277,8 +371,13 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
     }
   }
   tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if constexpr (PAIR) {
+    cluster_sync();  // the leader's MMAs wrote this CTA's TMEM, the peer's arrivals hit the leader
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  } else {
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  }
 }
 
 // ---------------------------------------------------------------- layout conversions

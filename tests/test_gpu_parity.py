@@ -390,9 +390,13 @@ def test_pchb_device_reader_and_cli_solve(bse, tmp_path):
     assert (tmp_path / "trace.csv").exists() and (tmp_path / "manifest.json").exists()
 
 
-def test_c64_tcgen05_filter_accuracy(bse):
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_c64_tcgen05_filter_accuracy(bse, monkeypatch, pair):
     """complex64 filter on tcgen05 (3xTF32): the filter output within FP32 accuracy of the
-    reference's complex128 filter (golden), and of the oracle on a ragged shape."""
+    reference's complex128 filter (golden), and of the oracle on a ragged shape; with the
+    single-CTA kernel and the CTA-pair (cta_group::2) kernel (m = 300: 3 row tiles, so the
+    last pair holds an all-padding CTA)."""
+    monkeypatch.setenv("BSE200_C64_PAIR", pair)
     a, b = golden_ham(16, 5)
     g = golden("ops_m16_s5.npz")
     ham = bse.BseHamiltonian(a, b)
