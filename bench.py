@@ -371,7 +371,8 @@ def run_ours(args, world, rank, local):
     algo = _lib.filter_algorithm() if _lib.filter_precision() == "c128" else "c64-3xtf32-tcgen05"
     exec_ratio = 0.75 if algo.startswith("3m") else 1.0  # 3M: 6 real DMMA per complex block pair instead of 8
     if algo.startswith("c64"):
-        peak, peak_src = 1100.0, "nominal dense TF32 tcgen05 peak (no measured TF32 figure; probe GEMM 437 TF/s)"
+        peak, peak_src = 1177.7, ("dense tf32 tcgen05 peak as ncu reports it at 1965 MHz (sm__ops_path_tensor_op_utchmma_"
+                                  "src_tf32 peak); measured probe GEMMs: 433 TF/s (1 CTA), 663 TF/s (CTA pair)")
         exec_ratio = 3.0  # 3 TF32 MMAs per real product
     if ham.flags & 1 and achieved:  # B = 0: the B half is skipped, count 4 n^2 k
         achieved *= 0.5
