@@ -85,3 +85,28 @@ def test_dist_c64_filter_matches_single_gpu_c64():
     ds.inner.chebyshev(v128, fcfg, ds.inner.ops.empty(k, n))
     err = ((vd - v128).abs().amax(dim=1) / v128.abs().amax(dim=1)).max().item()
     assert err <= 2e-5, err
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_dist_c64_filter_b_zero(monkeypatch, pair):
+    """B = 0 (the TDA limit, BSE_HAM_B_ZERO: the B half of the contraction is skipped) through the
+    complex64 grid filter, single-CTA and CTA-pair kernels: within FP32 accuracy of the FP64 filter."""
+    from paper_2601_10557_b200 import rng
+    from paper_2601_10557_b200.chebyshev import FilterConfig
+    from paper_2601_10557_b200.dist import DistributedSolver
+
+    monkeypatch.setenv("BSE200_C64_PAIR", pair)
+    dev = torch.device("cuda", 0)
+    a, _ = golden_ham(64, 21)
+    b = np.zeros_like(a)
+    k = 70
+    ds = DistributedSolver((a, b), device=dev)
+    assert ds.flags & 1  # B == 0 detected
+    ds.inner.ops.ctx.set_ham_flags(ds.flags)
+    fcfg = FilterConfig(10, 300.0, 250.0, -600.0)
+    v0 = torch.from_numpy(rng.complex_normal_matrix(rng.substream(9, 3), 128, k)).to(dev).T.contiguous()
+    v64, v128 = v0.clone(), v0.clone()
+    ds.inner.chebyshev_c64(v64, fcfg)
+    ds.inner.chebyshev(v128, fcfg, ds.inner.ops.empty(k, 128))
+    err = ((v64 - v128).abs().amax(dim=1) / v128.abs().amax(dim=1)).max().item()
+    assert err <= 2e-5, err
