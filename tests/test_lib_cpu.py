@@ -35,7 +35,10 @@ def test_sass_has_dmma_and_no_cpu_path():
         pytest.skip("cuobjdump missing")
     sass = subprocess.run(["cuobjdump", "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "DMMA.8x8x4" in sass
-    assert "LDGSTS" in sass  # cp.async staging
+    assert "LDGSTS" in sass  # cp.async staging (the barrier / mbarrier 3M kernels, zgemm)
+    assert "UTMALDG" in sass  # TMA loads (default FP64 filter kernel, complex64 kernel)
+    assert "UTCHMMA" in sass  # tcgen05.mma (complex64 filter)
+    assert "SYNCS" in sass  # mbarrier pipelines
 
 
 def test_rng_bit_exact_vs_reference_fixture():
