@@ -170,6 +170,12 @@ int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv
 /* Small pencil of the hermitian RR (rayleigh_ritz.py:113-137) from the summed W = Q^H S H Q
  * and G2 = Q2^H Q2: ascending Ritz values (host) and the sorted back-transform L^{-H} y (device). */
 int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec, double* h_lam_min_m);
+/* The two independent halves of bse_rr_pencil, for two GPUs of a grid to solve concurrently:
+ * part 1 only writes |lambda|_min(M) to *h_lam_min_m (no check; h_lam / d_wvec unused);
+ * part 2 is the pencil without the eigenvalues of M (the caller checks |lambda|_min(M) >= 1e-8
+ * first, as rayleigh_ritz.py:116-126 orders the errors).                                        */
+int bse_rr_pencil_part(bse_ctx* ctx, int part, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec,
+                       double* h_lam_min_m);
 /* Small problem of the backup RR (rayleigh_ritz.py:160-175) from summed partials G0 = Q^H S H Q
  * (overwritten), W = Q^H H Q and G2 = Q2^H Q2 (overwritten), all k x k: ascending real parts of the
  * eigenvalues (host) and the matching eigenvectors y (device, k x k); V = Q y / |Q y| is the caller's. */

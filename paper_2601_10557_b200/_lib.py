@@ -85,6 +85,7 @@ _SIGS = {
     "bse_c64_from_planes": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64]),
     "bse_chol_rinv": (C.c_int, [_vp, _vp, _i64, _dbl, _vp, _vp, _ip]),
     "bse_rr_pencil": (C.c_int, [_vp, _vp, _vp, _i64, _dp, _vp, _dp]),
+    "bse_rr_pencil_part": (C.c_int, [_vp, C.c_int, _vp, _vp, _i64, _dp, _vp, _dp]),
     "bse_rr_backup_pencil": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _dp, _vp, _dp]),
     "bse_resid_partial": (C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp]),
     "bse_colnorm2": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),

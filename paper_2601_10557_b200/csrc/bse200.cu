@@ -661,8 +661,10 @@ size_t pencil_ws_bytes(int64_t k) { return 3 * al((size_t)k * k * sizeof(zval)) 
 // Small hermitian pencil of the oblique RR (rayleigh_ritz.py:113-137) on k x k device data:
 // w = Q^H S H Q and g2 = Q2^H Q2 (raw sums, overwritten).  Returns ascending Ritz values on the
 // host and the sorted back-transform wvec = L^{-H} y[:, order] on the device.
+// mode 0: the whole pencil (rayleigh_ritz.py:113-137); mode 1: only |lambda|_min(M) into
+// *h_lam_min_m (no check); mode 2: the pencil without the eigenvalues of M (the caller has them)
 void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* wvec, double* h_lam_min_m,
-               Scratch& sc) {
+               Scratch& sc, int mode = 0) {
   const size_t kk = (size_t)k * k;
   StepTimer tm(ctx, "rr_pencil");
   zval* mm = sc.take<zval>(kk);
@@ -677,16 +679,20 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   check_launch(ctx);
   bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
   check_launch(ctx);
-  // :116-120  |lambda|_min(M) >= 1e-8
-  CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
-  heevd(ctx, tmp, (int)k, d_w, false, d_info);
   std::vector<double> hw(k);
-  to_host(ctx, hw.data(), d_w, k);
-  tm.mark("eigvalsh(M)", k);
-  double lmm = INFINITY;
-  for (double v : hw) lmm = std::min(lmm, std::fabs(v));
-  if (h_lam_min_m) *h_lam_min_m = lmm;
-  if (!(lmm >= 1e-8)) throw BseError(BSE_EHERMITIAN_RQ, "|lambda_min(Q*SQ)| = " + std::to_string(lmm) + " below 1e-8");
+  if (mode != 2) {
+    // :116-120  |lambda|_min(M) >= 1e-8
+    CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
+    heevd(ctx, tmp, (int)k, d_w, false, d_info);
+    to_host(ctx, hw.data(), d_w, k);
+    tm.mark("eigvalsh(M)", k);
+    double lmm = INFINITY;
+    for (double v : hw) lmm = std::min(lmm, std::fabs(v));
+    if (h_lam_min_m) *h_lam_min_m = lmm;
+    if (mode == 1) return;
+    if (!(lmm >= 1e-8))
+      throw BseError(BSE_EHERMITIAN_RQ, "|lambda_min(Q*SQ)| = " + std::to_string(lmm) + " below 1e-8");
+  }
   // :121-126  L = chol(W)
   if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0)
     throw BseError(BSE_EHERMITIAN_RQ, "Cholesky of Q*SHQ failed; S*H is not definite on the subspace");
@@ -1372,6 +1378,17 @@ int bse_rr_pencil(bse_ctx* ctx, void* d_w, void* d_g2, int64_t k, double* h_lam,
     Scratch sc(ctx, pencil_ws_bytes(k) + 4096);
     rr_pencil(ctx, static_cast<zval*>(d_w), static_cast<zval*>(d_g2), k, h_lam, static_cast<zval*>(d_wvec),
               h_lam_min_m, sc);
+  });
+}
+
+int bse_rr_pencil_part(bse_ctx* ctx, int part, void* d_w, void* d_g2, int64_t k, double* h_lam, void* d_wvec,
+                       double* h_lam_min_m) {
+  return guarded(ctx, [&] {
+    if (part != 1 && part != 2) throw BseError(BSE_EVALIDATION, "part must be 1 or 2");
+    if (k <= 0) return;
+    Scratch sc(ctx, pencil_ws_bytes(k) + 4096);
+    rr_pencil(ctx, static_cast<zval*>(d_w), static_cast<zval*>(d_g2), k, h_lam, static_cast<zval*>(d_wvec),
+              h_lam_min_m, sc, part);
   });
 }
 

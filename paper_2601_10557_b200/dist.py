@@ -146,6 +146,14 @@ class Comm:
         if self.g.p > 1:
             self.dist.all_reduce(self._real(t), group=self.col)
 
+    def sum_all(self, t) -> None:
+        if self.g.world > 1:
+            self.dist.all_reduce(self._real(t))
+
+    def bcast_all(self, t, src: int) -> None:
+        if self.g.world > 1:
+            self.dist.broadcast(self._real(t), src=src)
+
     def max_all(self, t) -> None:
         if self.g.world > 1:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
@@ -279,6 +287,16 @@ class CudaOps:
         self.ctx.call("bse_rr_pencil", _lib.dptr(w), _lib.dptr(g2), k, _lib.hptr(lam), _lib.dptr(wvec),
                       ctypes.byref(lmm))
         return lam, wvec, lmm.value
+
+    def rr_pencil_part(self, part, w, g2):
+        """bse_rr_pencil_part: part 1 -> |lambda|_min(M); part 2 -> (lam, wvec) without M's spectrum."""
+        k = w.shape[0]
+        lam = np.zeros(k)
+        wvec = self.empty(k, k)
+        lmm = ctypes.c_double(0.0)
+        self.ctx.call("bse_rr_pencil_part", part, _lib.dptr(w), _lib.dptr(g2), k, _lib.hptr(lam), _lib.dptr(wvec),
+                      ctypes.byref(lmm))
+        return lmm.value if part == 1 else (lam, wvec)
 
     def rr_backup_pencil(self, g0, w, g2):
         k = w.shape[0]
@@ -632,7 +650,7 @@ class DistSolver:
             ledger.add_flops("rr", 8.0 * n * n * k)  # apply_h inside RR (hamiltonian.py:148-150)
         if variant != "backup":
             try:
-                lam, wvec, lmm = self.ops.rr_pencil(gtb[0] + gtb[1], g2.clone())
+                lam, wvec, lmm = self._pencil(gtb[0] + gtb[1], g2)
                 if ledger is not None:
                     ledger.add_flops("rr", 8.0 * n * n * k + 12.0 * n * k * k + 16.0 * k**3)
             except HermitianRqError as exc:
@@ -666,6 +684,40 @@ class DistSolver:
             res = np.sqrt(r2.cpu().numpy() / n2.cpu().numpy())
             st.mark("residuals from S T w", k)
         return lam, v, lmm, res, used, fallback
+
+    _PENCIL_ERRORS = {1: "Cholesky of Q*SHQ failed; S*H is not definite on the subspace",
+                      2: "reduced spectrum touches zero; cannot invert"}
+
+    def _pencil(self, w, g2):
+        """The k x k pencil of the hermitian RR (rayleigh_ritz.py:113-137).  On one GPU as a whole; on a
+        grid its two independent halves run concurrently on ranks 1 (eigenvalues of M) and 0 (chol(W),
+        G, eigh(G), back-transform), then one small allreduce and two broadcasts share the results.
+        Errors keep the reference's order: a singular M first, then the Cholesky / theta ~ 0 failures."""
+        g = self.g
+        if g.world == 1 or not hasattr(self.ops, "rr_pencil_part"):
+            return self.ops.rr_pencil(w, g2.clone())
+        torch = self.torch
+        k = w.shape[0]
+        info = torch.zeros(2, dtype=torch.float64, device=w.device)  # [lambda_min(M), error code]
+        lam_d = torch.zeros(k, dtype=torch.float64, device=w.device)
+        wvec = self.ops.empty(k, k)
+        if g.rank == 1:
+            info[0] = self.ops.rr_pencil_part(1, w, g2.clone())
+        elif g.rank == 0:
+            try:
+                lam, wvec = self.ops.rr_pencil_part(2, w, g2.clone())
+                lam_d.copy_(torch.from_numpy(lam))
+            except HermitianRqError as exc:
+                info[1] = 1.0 if "Cholesky" in str(exc) else 2.0
+        self.c.sum_all(info)
+        lmm, code = float(info[0].item()), int(info[1].item())
+        if not lmm >= 1e-8:
+            raise HermitianRqError(f"|lambda_min(Q*SQ)| = {lmm:.6e} below 1e-8")
+        if code:
+            raise HermitianRqError(self._PENCIL_ERRORS[code])
+        self.c.bcast_all(lam_d, src=0)
+        self.c.bcast_all(wvec, src=0)
+        return lam_d.cpu().numpy(), wvec, lmm
 
     def residuals(self, v_col, lam, row_buf) -> np.ndarray:
         k = v_col.shape[0]

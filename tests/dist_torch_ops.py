@@ -103,7 +103,16 @@ class TorchOps:
         order = np.argsort(vals.real, kind="stable")
         return vals.real[order].copy(), torch.from_numpy(y[:, order]).T.contiguous(), lmm
 
-    def rr_pencil(self, w, g2):
+    def rr_pencil_part(self, part, w, g2):
+        """The two halves of rr_pencil (bse_rr_pencil_part)."""
+        if part == 1:
+            k = w.shape[0]
+            mm = torch.eye(k, dtype=w.dtype) - 2 * g2.T
+            return float(torch.linalg.eigvalsh((mm + mm.conj().T) / 2).abs().min())
+        lam, wv, _ = self.rr_pencil(w, g2, check_m=False)
+        return lam, wv
+
+    def rr_pencil(self, w, g2, check_m=True):
         from paper_2601_10557_b200.errors import HermitianRqError
 
         wm = w.T
@@ -111,12 +120,12 @@ class TorchOps:
         k = wm.shape[0]
         mm = torch.eye(k, dtype=wm.dtype) - 2 * g2.T
         mm = (mm + mm.conj().T) / 2
-        lmm = float(torch.linalg.eigvalsh(mm).abs().min())
-        if lmm < 1e-8:
+        lmm = float(torch.linalg.eigvalsh(mm).abs().min()) if check_m else float("nan")
+        if check_m and lmm < 1e-8:
             raise HermitianRqError("M singular")
         ell, info = torch.linalg.cholesky_ex(wm)
         if int(info):
-            raise HermitianRqError("W not definite")
+            raise HermitianRqError("Cholesky of Q*SHQ failed (W not definite)")
         gg = torch.linalg.solve_triangular(ell, mm, upper=False)
         gg = torch.linalg.solve_triangular(ell, gg.conj().T, upper=False).conj().T
         gg = (gg + gg.conj().T) / 2
