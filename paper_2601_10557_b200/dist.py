@@ -390,7 +390,8 @@ class DistSolver:
 
     # filter column chunking (allreduce overlapped with the next chunk's GEMM) from this block width
     # on.  Off by default: at C3 the allreduces are ~1-2% of a step and two half-width GEMMs lose
-    # more (4 GPUs: filter 13.0 s chunked vs 12.5 s, profiles/r01/); BSE200_CHUNK_MIN enables it.
+    # more (4 GPUs: filter 13.0 s chunked vs 12.5 s with the first kernels, 10.97 s vs 10.74 s with the
+    # TMA kernel, profiles/r01/); BSE200_CHUNK_MIN enables it.
     CHUNK_MIN = int(__import__("os").environ.get("BSE200_CHUNK_MIN", str(1 << 30)))
 
     def __init__(self, grid: Grid, comm: Comm, ops, fwd: Tile, trn: Tile):
