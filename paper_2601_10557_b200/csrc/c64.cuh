@@ -4,15 +4,17 @@
 // x = hi + lo (hi = tf32(x), lo = x - hi):  a b ~= a_hi b_hi + a_hi b_lo + a_lo b_hi.
 // The operator is the same as the FP64 hop kernel (hop.cuh): with P the K-slab of [A | B],
 //   U = P Xa,  L' = conj(P) Xb,  H x = [U ; -L'],
-// as four real accumulators in TMEM (U_r, U_i, L'_r, L'_i; 128 lanes x 64 fp32 columns each):
-//   U_r = Pr Xar - Pi Xai   U_i = Pr Xai + Pi Xar   L'_r = Pr Xbr + Pi Xbi   L'_i = Pr Xbi - Pi Xbr
-// i.e. 8 real products x 3 = 24 UMMA (128 x 64 x 8) per K step; negation through the
-// instruction descriptor.  Operands live in HBM as fp32 hi/lo planes in K-major layouts
-// (P planes row-major over K, X planes = the column-major vectors) and are fed by 3-D TMA
-// boxes (64-byte swizzle) whose out-of-range rows are zero-filled by the hardware, so the A/B
-// part and upper/lower half boundaries need no special casing.  Warp 0 = TMA producer,
-// warp 1 = MMA issuer, warps 2-9 = accumulation drain + epilogue:
-// y+ = alpha (H y - c y) - beta y-, written back as hi/lo planes for the next step.
+// accumulated in TMEM as [U_r | U_i] and [L'_r | L'_i] (128 lanes x 128 fp32 columns each): each
+// complex product is two N = 128 UMMAs over overlapping windows of stacked X tiles
+// ([-Xi | Xr | Xi] and [Xr | Xi | -Xr]), x 3 for 3xTF32.  Operands live in HBM as fp32 hi/lo
+// planes in K-major layouts (P planes row-major over K, X planes = the column-major vectors) and
+// are fed by 3-D TMA boxes (64-byte swizzle) whose out-of-range rows are zero-filled, so the A/B
+// part and upper/lower half boundaries need no special casing.  Warp 0 = TMA producer, warp 1 =
+// MMA issuer, warps 2-9 = chunked accumulation drain (round-to-nearest fp32) + epilogue:
+// y+ = alpha (H y - c y) - beta y-, written back as hi/lo planes for the next step, or as raw fp32
+// partials (raw mode) for the 2D grid's allreduce.  The operator may be a tile of the grid
+// (output rows mo, contraction kc, the shift on a window of rows with an input offset).
+// step_kernel<true> is the CTA-pair variant (cta_group::2, M = 256 over two SMs; see Geo below).
 #pragma once
 #include "common.cuh"
 #include "tc_common.cuh"
