@@ -444,14 +444,24 @@ size_t resid_part_count(int64_t m, int64_t k) { return (size_t)((m + HopMain::BM
 // ----------------------------------------------------------------------------
 using GemmMain = bse::GemmCfg<64, 64, 8, 4, 2, 4>;
 
+// Split-K factor: enough CTAs to fill the GPU and little wave quantisation (the last wave of a
+// 361-tile Gram at k = 1200 ran 78% idle without a split), keeping >= 16 k-tiles per split.
 int splitk_for(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ((M + GemmMain::BM - 1) / GemmMain::BM) * ((N + GemmMain::BN - 1) / GemmMain::BN);
-  const int64_t want = 148 * 2;
-  if (tiles >= want) return 1;
-  int64_t s = (want + tiles - 1) / tiles;
+  const int64_t slots = 148 * 2;  // resident CTAs (2 per SM)
   const int64_t kt = (K + GemmMain::BK - 1) / GemmMain::BK;
-  s = std::min<int64_t>(s, std::max<int64_t>(1, kt / 16));  // keep >= 16 k-tiles per split
-  return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, kt / 16));
+  auto fill = [&](int64_t s) {  // fraction of the launched waves' CTA slots that do work
+    const int64_t ctas = tiles * s;
+    return (double)ctas / (double)(((ctas + slots - 1) / slots) * slots);
+  };
+  if (tiles >= 8 * slots || fill(1) >= 0.9) return 1;  // many waves: quantisation is negligible
+  int64_t best = 1;
+  for (int64_t s = 1; s <= smax; ++s) {
+    if (tiles * s >= slots && fill(s) >= 0.9) return (int)s;
+    if (fill(s) > fill(best) + 1e-9) best = s;
+  }
+  return (int)best;
 }
 
 size_t gemm_ws_bytes(int64_t M, int64_t N, int64_t K) {
