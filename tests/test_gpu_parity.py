@@ -449,3 +449,24 @@ def test_mixed_precision_solve_parity(bse, c1_instance, monkeypatch):
         assert abs(r.iterations_used - int(g[f"{tag}_iters"])) <= 1
         assert (np.abs(r.lambdas - g[f"{tag}_lambdas"]) / np.abs(g[f"{tag}_lambdas"])).max() <= 1e-10
         assert r.residual_norms.max() <= 1e-10 * (abs(r.bounds.mu_1) if rel else 1.0)
+
+
+def test_abi_validation_errors(bse):
+    """Status codes of the entry points added for the grid and kernel selection map onto the
+    reference exception classes (errors.py:8-38) and fire before any device work."""
+    import ctypes
+
+    from paper_2601_10557_b200 import _lib
+
+    ctx = _lib.Context.get(0)
+    with pytest.raises(bse.ValidationError):
+        ctx.call("bse_set_filter_algorithm", 99)
+    with pytest.raises(bse.ValidationError):
+        ctx.call("bse_rr_pencil_part", 3, None, None, 4, None, None, None)
+    args = _lib.C64TileArgs()
+    args.mo, args.kc, args.k = 8, 0, 4
+    with pytest.raises(bse.ValidationError):
+        ctx.call("bse_c64_tile_step", ctypes.byref(args))
+    with pytest.raises(bse.ValidationError):
+        ctx.call("bse_c64_tile_planes", None, None, 2, 8, 4, None)  # lds < kc
+    ctx.call("bse_set_filter_algorithm", _lib._ALGOS[bse.filter_algorithm()])  # context stays usable
