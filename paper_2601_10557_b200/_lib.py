@@ -240,7 +240,17 @@ class Context:
 
 
 def dptr(t) -> _vp:
-    return _vp(t.data_ptr())
+    return _vp(None) if t is None else _vp(t.data_ptr())
+
+
+def planes_fit(nbytes: int, device, reserve: int = 0) -> bool:
+    """Whether an optional operand copy of nbytes (the 3M sum planes: +32 m^2 bytes) still leaves
+    `reserve` bytes of HBM for the solve's vectors.  Counts memory torch has cached but not used."""
+    import torch
+
+    free, _ = torch.cuda.mem_get_info(device)
+    cached = torch.cuda.memory_reserved(device) - torch.cuda.memory_allocated(device)
+    return free + cached >= nbytes + reserve + (1 << 30)
 
 
 def hptr(a) -> _dp:

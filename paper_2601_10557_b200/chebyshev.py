@@ -52,7 +52,9 @@ def filter_inplace(ham: BseHamiltonian, v, cfg: FilterConfig, work=None, ledger:
 
         work = torch.empty(2 * ld_of(v) * k, dtype=torch.complex128, device=v.device)
     ab = ham.device_blocks(v.device)
-    sd = _lib.dptr(ham.device_sum_planes(v.device)) if _lib.uses_sum_planes() else None
+    # the planes must leave room for the RR's T and residual blocks (2 n k) next to the filter's buffers
+    sdt = ham.device_sum_planes(v.device, reserve=2 * 16 * ld_of(v) * k) if _lib.uses_sum_planes() else None
+    sd = _lib.dptr(sdt) if sdt is not None else None
     ctx = _lib.Context.get(v.device.index)
     ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(v), ld_of(v), k, cfg.degree,
              cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))

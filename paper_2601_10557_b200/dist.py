@@ -350,9 +350,14 @@ class Tile:
     sb: int = 0
 
 
-def add_sum_planes(ops, tile: Tile) -> Tile:
-    """Attach the 3M (re+im, re-im) planes of the tile (CUDA ops only)."""
+def add_sum_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
+    """Attach the 3M (re+im, re-im) planes of the tile (CUDA ops only), if they leave `reserve` bytes
+    of HBM for the solve; else the tile product forms the operand sums in registers."""
     if not hasattr(ops, "ctx"):
+        return tile
+    if not _lib.planes_fit(tile.buf.numel() * 16, ops.device, reserve):
+        logger.warning("3M sum planes of a %d x %d tile do not fit; forming the operand sums in registers",
+                       tile.mr, 2 * tile.kc)
         return tile
     sd = ops.torch.empty_like(tile.buf)
     ops.ctx.call("bse_make_sum_planes", tile.buf.data_ptr(), tile.lda, tile.mr, 2 * tile.kc, sd.data_ptr())
@@ -958,9 +963,12 @@ class DistributedSolver:
         if hasattr(self.ops, "ctx"):
             self.ops.ctx.set_ham_flags(self.flags)
         if _lib.uses_sum_planes():
+            g = self.inner.g
+            # vectors of the solve: col / row blocks, locked block, the RR's T and products (~6 blocks)
+            reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
             for t in (self.fwd, self.trn):
                 if t.sd is None:
-                    add_sum_planes(self.ops, t)
+                    add_sum_planes(self.ops, t, reserve)
         res = self.inner.solve(cfg)
         res.v = res.v.T  # (n, nev) column-major view
         return res

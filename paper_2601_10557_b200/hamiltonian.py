@@ -178,14 +178,24 @@ class BseHamiltonian:
     def flags(self) -> int:
         return 1 if self.b_is_zero else 0  # BSE_HAM_B_ZERO
 
-    def device_sum_planes(self, device):
-        """(re+im, re-im) planes of [A | B] for the 3M filter (bse_make_sum_planes), built once per device."""
+    def device_sum_planes(self, device, reserve: int = 0):
+        """(re+im, re-im) planes of [A | B] for the 3M filter (bse_make_sum_planes), built once per device.
+        None when they would not leave `reserve` bytes of HBM (e.g. n = 100k on one GPU: 80 GB of planes
+        on top of 80 GB of blocks): the products then form the operand sums in registers (3M, same bits
+        per output, ~7% slower)."""
         torch = _torch()
         device = torch.device(device)
         sd_cache = self.__dict__.setdefault("_sd", {})
         sd = sd_cache.get(device)
+        if sd is False:
+            return None
         if sd is None:
             ab = self.device_blocks(device)
+            if not _lib.planes_fit(ab.numel() * 16, device, reserve):
+                logger.warning("3M sum planes (%.1f GB) do not fit next to the solve; forming the operand sums "
+                               "in registers", ab.numel() * 16 / 1e9)
+                sd_cache[device] = False
+                return None
             sd = colmajor_empty(ab.shape[0], ab.shape[1], device)
             _lib.Context.get(device.index).call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), ab.shape[0],
                                                 ab.shape[1], _lib.dptr(sd))

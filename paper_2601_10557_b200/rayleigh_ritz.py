@@ -61,7 +61,8 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     lmm = ctypes.c_double(float("nan"))
     ab = ham.device_blocks(q.device)
     # the T = (S) H Q product runs on the filter's kernel (3M) when the sum planes are in use
-    sd = _lib.dptr(ham.device_sum_planes(q.device)) if _lib.uses_sum_planes() else None
+    sdt = ham.device_sum_planes(q.device, reserve=2 * 16 * n * k) if _lib.uses_sum_planes() else None
+    sd = _lib.dptr(sdt) if sdt is not None else None
     ctx = _lib.Context.get(q.device.index)
     res = np.zeros(k) if fused_residuals else None
     extra = (_lib.hptr(res) if fused_residuals else None,) if entry == "bse_rr_hermitian" else ()

@@ -470,3 +470,27 @@ def test_abi_validation_errors(bse):
     with pytest.raises(bse.ValidationError):
         ctx.call("bse_c64_tile_planes", None, None, 2, 8, 4, None)  # lds < kc
     ctx.call("bse_set_filter_algorithm", _lib._ALGOS[bse.filter_algorithm()])  # context stays usable
+
+
+def test_filter_without_sum_planes_when_hbm_is_short(bse, monkeypatch):
+    """When the 3M sum planes (+32 m^2 bytes) would not fit next to the solve (n = 100k on one GPU),
+    the filter and the RR product form the operand sums in registers instead: same 3M arithmetic,
+    same results."""
+    from paper_2601_10557_b200 import _lib
+    from paper_2601_10557_b200.dist import DistributedSolver
+
+    a, b = golden_ham(64, 21)
+    cfg = bse.FilterConfig(10, 300.0, 250.0, -600.0)
+    x = np.random.default_rng(3).standard_normal((128, 40)) + 1j * np.random.default_rng(4).standard_normal((128, 40))
+    with_planes = bse.chebyshev_filter(bse.BseHamiltonian(a, b), x, cfg)
+    monkeypatch.setattr(_lib, "planes_fit", lambda *args, **kw: False)
+    ham = bse.BseHamiltonian(a, b)
+    without = bse.chebyshev_filter(ham, x, cfg)
+    assert ham.device_sum_planes(0) is None
+    assert _rel(without, with_planes) <= 1e-13
+    r = bse.solve(bse.BseHamiltonian(a, b), bse.SolverConfig(nev=8, seed=21))
+    g = golden("solve_m64_s21.npz")
+    assert (np.abs(r.lambdas - g["lambdas"]) / np.abs(g["lambdas"])).max() <= 1e-10
+    ds = DistributedSolver((a, b))
+    rd = ds.solve(bse.SolverConfig(nev=8, seed=21))
+    assert ds.fwd.sd is None and (np.abs(rd.lambdas - g["lambdas"]) / np.abs(g["lambdas"])).max() <= 1e-10
