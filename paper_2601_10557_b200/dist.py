@@ -20,8 +20,11 @@ The scheme of PAPER.md:723-740 (not shipped by the reference):
   step, with two buffers (one per layout) and no copies.
 * CholQR Grams, the projection against the locked vectors, W = Q^H S H Q,
   Q2^H Q2 and the residual norms are local partial products plus ONE
-  allreduce each; the k x k pencil is solved redundantly on every GPU
-  (PAPER.md:725).  Q is allgathered once per iteration for the RR.
+  allreduce each.  The k x k pencil (solved redundantly in PAPER.md:725) is
+  split into its two independent halves on ranks 0 and 1.  Q is allgathered
+  once per iteration for the RR; the backup projection reuses the same T.
+* The complex64 filter (configs[4]) runs the same recurrence on the tcgen05
+  tile kernel: raw fp32 partials, an fp32 allreduce, then the hi/lo split.
 
 Everything device-side goes through an ``ops`` object: ``CudaOps`` (the bse200
 C ABI) in production; the CPU gloo tests substitute a torch reference.
