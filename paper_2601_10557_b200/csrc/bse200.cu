@@ -267,7 +267,7 @@ void launch_hop_tma(bse_ctx* ctx, const bse::HopArgs& a_in) {
   const zval* xx[2] = {a.x1, a.x2};
   for (int q = 0; q < 2; ++q) {
     mp.p[q] = map2d_f64(pp[q], pr, a.kc, a.lda * 16, 2 * (C::BM + 2), C::BK);
-    mp.sd[q] = map2d_f64(ss[q], pr, a.kc, a.lda * 16, 2 * (C::BM + 2), C::BK);
+    mp.sd[q] = C::PS ? map2d_f64(ss[q], pr, a.kc, a.lda * 16, 2 * (C::BM + 2), C::BK) : mp.p[q];
     mp.x[q] = map2d_f64(xx[q], xr, a.k, a.ldx * 16, 2 * (C::BK + 4), C::BN);
   }
   dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
@@ -301,6 +301,9 @@ void launch_hop_mb(bse_ctx* ctx, const bse::HopArgs& a_in) {
 using Hop3MSync = bse::HopCfg<32, 32, 8, 2, 2, 4, 3, 1>;
 using Hop3MNarrow = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 1>;
 using Hop3MWide = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
+// the default's tiles without sum planes (HBM too short for them): operand sums formed in registers
+using Hop3MNarrowNP = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 0>;
+using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 
 bool filter_code_needs_planes(int code) { return code == 65 || code == 72 || code == 82 || code == 86 || code == 88; }
 bool filter_code_valid(int code) { return code == 3 || code == 4 || filter_code_needs_planes(code); }
@@ -308,8 +311,15 @@ bool filter_code_valid(int code) { return code == 3 || code == 4 || filter_code_
 // Chebyshev-step products, as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm;
-  if (filter_code_needs_planes(code) && (!a.sa || !a.sb)) code = 3;  // no P sum planes: sums in registers
+  if (filter_code_needs_planes(code) && (!a.sa || !a.sb))  // no P sum planes: sums in registers
+    code = code == 88 ? 98 : 3;
   switch (code) {
+    case 98:  // the default's TMA kernel forming the operand sums in registers (same bits)
+      if (a.k >= 512)
+        launch_hop_tma<Hop3MWideNP>(ctx, a);
+      else
+        launch_hop_tma<Hop3MNarrowNP>(ctx, a);
+      break;
     // default 3M: 64 x 32 CTA (8 consumer warps, 6 stages) for wide blocks, 64 x 16 (4 warps,
     // 2 CTAs/SM) below 512 columns where the wider tile underfills the GPU.  Every variant
     // accumulates each output in the same K order: the choice never changes a bit.

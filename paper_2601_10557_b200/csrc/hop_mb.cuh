@@ -133,7 +133,10 @@ __device__ __forceinline__ void mb_stage_mma(double (&acc)[6][C::WM][C::WN][2], 
 #pragma unroll
     for (int i = 0; i < C::WM; ++i) {
       pf[i] = lds128(Ps + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
-      sdf[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
+      if constexpr (C::PS == 1)
+        sdf[i] = lds128(SDs + (ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g);
+      else  // no sum planes: the same FP64 adds as sum_planes_kernel, in registers
+        sdf[i] = zval{pf[i].re + pf[i].im, pf[i].re - pf[i].im};
     }
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
@@ -249,9 +252,11 @@ struct HopMaps {
 
 template <class C>
 struct TmaLayout {
-  static_assert(C::PS == 1, "TMA feed: 3M with P-side sum planes only");
+  // PS == 1: P and its sum planes staged; PS == 0: P only, the sums formed in registers
+  static_assert(C::PS == 0 || C::PS == 1, "TMA feed: 3M with or without P-side sum planes");
   static constexpr int P_BYTES = C::P_ELEMS * 16, X_BYTES = C::X_ELEMS * 16;
-  static constexpr int STAGE_BYTES = 2 * P_BYTES + 2 * X_BYTES;
+  static constexpr int NP = C::PS ? 2 : 1;  // P tiles per stage
+  static constexpr int STAGE_BYTES = NP * P_BYTES + 2 * X_BYTES;
   static_assert(P_BYTES % 128 == 0 && X_BYTES % 128 == 0, "TMA destinations must stay 128-byte aligned");
   static_assert(2 * (C::BM + 2) <= 256 && 2 * (C::BK + 4) <= 256 && C::BN <= 256 && C::BK <= 256,
                 "TMA box dimensions are limited to 256 elements");
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     for (int q = 0; q < 2; ++q) {
       tc::prefetch_tmap(&maps.p[q]);
-      tc::prefetch_tmap(&maps.sd[q]);
+      if constexpr (C::PS == 1) tc::prefetch_tmap(&maps.sd[q]);
       tc::prefetch_tmap(&maps.x[q]);
     }
   }
@@ -301,9 +306,9 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
     unsigned char* st = base + buf * T::STAGE_BYTES;
     tc::mbar_arrive_expect_tx(&full[buf], T::STAGE_BYTES);
     tc::tma_load_2d(st, &maps.p[part], &full[buf], 2 * i0, j0);
-    tc::tma_load_2d(st + T::P_BYTES, &maps.sd[part], &full[buf], 2 * i0, j0);
-    tc::tma_load_2d(st + 2 * T::P_BYTES, &maps.x[part], &full[buf], 2 * j0, c0);              // Xa
-    tc::tma_load_2d(st + 2 * T::P_BYTES + T::X_BYTES, &maps.x[1 - part], &full[buf], 2 * j0, c0);  // Xb
+    if constexpr (C::PS == 1) tc::tma_load_2d(st + T::P_BYTES, &maps.sd[part], &full[buf], 2 * i0, j0);
+    tc::tma_load_2d(st + T::NP * T::P_BYTES, &maps.x[part], &full[buf], 2 * j0, c0);                  // Xa
+    tc::tma_load_2d(st + T::NP * T::P_BYTES + T::X_BYTES, &maps.x[1 - part], &full[buf], 2 * j0, c0);  // Xb
     ++lkt;
   };
   if (warp == NWARPS) {
@@ -332,8 +337,8 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
     const int s = kt % C::STAGES;
     mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
     const zval* Ps = reinterpret_cast<const zval*>(base + s * T::STAGE_BYTES);
-    const zval* SDs = Ps + C::P_ELEMS;
-    const zval* Xas = SDs + C::P_ELEMS;
+    const zval* SDs = Ps + C::P_ELEMS;  // unused when C::PS == 0
+    const zval* Xas = Ps + T::NP * C::P_ELEMS;
     const zval* Xbs = Xas + C::X_ELEMS;
     mb_stage_mma<C>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
     __syncwarp();
