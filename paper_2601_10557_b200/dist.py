@@ -20,7 +20,7 @@ The scheme of PAPER.md:723-740 (not shipped by the reference):
   step, with two buffers (one per layout) and no copies.
 * CholQR Grams, the projection against the locked vectors, W = Q^H S H Q,
   Q2^H Q2 and the residual norms are local partial products plus ONE
-  allreduce each.  The k x k pencil (solved redundantly in PAPER.md:725) is
+  allreduce each; the replicas of a layout split the rows between them.  The k x k pencil (solved redundantly in PAPER.md:725) is
   split into its two independent halves on ranks 0 and 1.  Q is allgathered
   once per iteration for the RR; the backup projection reuses the same T.
 * The complex64 filter (configs[4]) runs the same recurrence on the tcgen05
@@ -573,11 +573,28 @@ class DistSolver:
         # the -beta Y_prev term is added once per reduction group
         return (self.g.I == 0) if step % 2 == 0 else (self.g.J == 0)
 
-    # ---- orthonormalisation -----------------------------------------------------------------
+    # ---- replicated layouts ------------------------------------------------------------------
+    # A col-layout block is replicated on the p ranks of its column group, a row-layout block on the
+    # q ranks of its row group.  Reductions over its rows (Grams, column norms, residual partials)
+    # therefore let each replica take one contiguous share of the rows and sum over ALL ranks:
+    # 1/p (1/q) of the work for the same single allreduce.
+    def _share(self, width: int, layout: str) -> tuple[int, int]:
+        parts, idx = (self.g.p, self.g.I) if layout == "col" else (self.g.q, self.g.J)
+        e = split(width, parts)
+        return e[idx], e[idx + 1]
+
     def _gram_row(self, a, b=None):
-        gm = self.ops.gram(a, a if b is None else b)
-        self.c.sum_row(gm)
+        """a^H b over the rows of col-layout blocks (summed over all their rows, every rank gets it)."""
+        lo, hi = self._share(a.shape[1], "col")
+        gm = self.ops.gram(a[:, lo:hi], (a if b is None else b)[:, lo:hi])
+        self.c.sum_all(gm)
         return gm
+
+    def _colnorm2(self, x, layout: str):
+        lo, hi = self._share(x.shape[1], layout)
+        n2 = self.ops.colnorm2(x[:, lo:hi])
+        self.c.sum_all(n2)
+        return n2
 
     def cholqr(self, q_col):
         """Distributed CholQR2 (+ shifted CholQR3 fallback) of a col-layout block; returns (q, method)."""
@@ -600,8 +617,7 @@ class DistSolver:
             return q, "cholqr"
         st.mark("FALLBACK", q.shape[0])
         # shifted CholQR3 on the original block
-        n2 = self.ops.colnorm2(x0)
-        self.c.sum_row(n2)
+        n2 = self._colnorm2(x0, "col")
         k = x0.shape[0]
         n = 2 * self.g.m
         shift = 11.0 * (n * k + k * (k + 1)) * 2.0**-53 * float(n2.sum().item())
@@ -648,11 +664,11 @@ class DistSolver:
         q_full = self.assemble_from_col(q_col)
         st.mark("allgather Q", k)
         q_rows = self.row_rows(q_full)
-        gtb = self.torch.stack([self.ops.gram(q_rows[:, :nr], t_row[:, :nr]),
-                                self.ops.gram(q_rows[:, nr:], t_row[:, nr:])])
-        self.c.sum_col(gtb)
-        g2 = self.ops.gram(q_col[:, self.g.nc:], q_col[:, self.g.nc:])
-        self.c.sum_row(g2)
+        rlo, rhi = self._share(nr, "row")  # this replica's share of the rows of each half
+        gtb = self.torch.stack([self.ops.gram(q_rows[:, rlo:rhi], t_row[:, rlo:rhi]),
+                                self.ops.gram(q_rows[:, nr + rlo:nr + rhi], t_row[:, nr + rlo:nr + rhi])])
+        self.c.sum_all(gtb)
+        g2 = self._gram_row(q_col[:, self.g.nc:])
         st.mark("Q^H T halves, Q2^H Q2 + allreduce", k)
         used, fallback, lam = "hermitian", False, None
         if ledger is not None:
@@ -677,19 +693,21 @@ class DistSolver:
                 ledger.add_flops("rr", 8.0 * n * n * k + 20.0 * n * k * k + 30.0 * k**3)
         st.mark("pencil", k)
         v = self.ops.nn(q_col, wvec)
-        n2 = self.ops.colnorm2(v)
-        self.c.sum_row(n2)
+        n2 = self._colnorm2(v, "col")
         self.ops.colscale_rsqrt(v, n2)
         st.mark("V = Q w, normalise", k)
         res = None
         if fused_residuals:
             torch = self.torch
-            u_row = self.ops.nn(t_row, wvec)
-            vq_row = self.ops.nn(q_rows, wvec)
             ones = torch.ones(k, dtype=torch.float64, device=v.device)
             lam_d = torch.as_tensor(np.ascontiguousarray(lam), dtype=torch.float64, device=v.device)
-            r2 = self.ops.resid_partial(u_row, vq_row, self.g.nr, ones, lam_d)
-            self.c.sum_col(r2)
+            r2 = torch.zeros(k, dtype=torch.float64, device=v.device)
+            for off, half in ((0, rhi - rlo), (nr, 0)):  # upper share (no sign flip), lower share (S: negated)
+                sl = slice(off + rlo, off + rhi)
+                if rhi > rlo:
+                    r2 += self.ops.resid_partial(self.ops.nn(t_row[:, sl], wvec), self.ops.nn(q_rows[:, sl], wvec),
+                                                 half, ones, lam_d)
+            self.c.sum_all(r2)
             res = np.sqrt(r2.cpu().numpy() / n2.cpu().numpy())
             st.mark("residuals from S T w", k)
         return lam, v, lmm, res, used, fallback
@@ -733,8 +751,7 @@ class DistSolver:
         r_row = row_buf[:k]
         lam_d = self.torch.as_tensor(np.ascontiguousarray(lam), dtype=self.torch.float64, device=v_col.device)
         self.forward(v_col, r_row, shift_col=lam_d)  # R = H V - V Lambda (rows R_I)
-        n2 = self.ops.colnorm2(r_row)
-        self.c.sum_col(n2)
+        n2 = self._colnorm2(r_row, "row")
         return np.sqrt(n2.cpu().numpy())
 
     # ---- Lanczos (lanczos.py:53-142) ------------------------------------------------------------

@@ -1,5 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_dist.py -q -m gpu 2>&1 | tail -1
 for NG in 2 4; do
 TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $NG --master-addr 127.0.0.1 --master-port 2952$NG"
 timeout 600 $TR tools/dist_check.py > gpurun_out/dist_check_n$NG.log 2>&1; echo "dist_check n$NG rc=$?"; grep "world" gpurun_out/dist_check_n$NG.log | tail -8
