@@ -375,7 +375,11 @@ def run_ours(args, world, rank, local):
     peak, peak_src = fp64_peak()
     achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
     algo = _lib.filter_algorithm() if _lib.filter_precision() == "c128" else "c64-3xtf32-tcgen05"
+    if algo.startswith("rs") and (world > 1 or ham.flags & 1):
+        algo = "3m"  # the 2D-grid tiles and B = 0 run the 3M kernel (the real-split planes are single-GPU, B != 0)
     exec_ratio = 0.75 if algo.startswith("3m") else 1.0  # 3M: 6 real DMMA per complex block pair instead of 8
+    if algo.startswith("rs"):
+        exec_ratio = 0.5  # real split: 4 n^2 k DMMA flops per step (csrc/hop_rs.cuh)
     if algo.startswith("c64"):
         peak, peak_src = 1177.7, ("dense tf32 tcgen05 peak as ncu reports it at 1965 MHz (sm__ops_path_tensor_op_utchmma_"
                                   "src_tf32 peak); measured probe GEMMs: 433 TF/s (1 CTA), 663 TF/s (CTA pair)")
@@ -416,12 +420,14 @@ def run_ours(args, world, rank, local):
                          "traffic_source": ncu_traffic(algo)[1],
                          "kernel": ("bse::c64::step_kernel (tcgen05 3xTF32 complex64 filter step)" if algo.startswith("c64")
                                     else "bse::hop3m_tma_kernel (fused H-operator 3M DMMA GEMM, TMA-fed by a producer warp, mbarrier rings, Chebyshev epilogue)"
-                                    if algo == "3m" else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
+                                    if algo == "3m" else
+                                    "bse::hop_rs_tma_kernel (real-split H operator: folded block, four real planes, 4 n^2 k DMMA flops per step, TMA-fed by a producer warp, Chebyshev epilogue)"
+                                    if algo.startswith("rs") else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
                          "peak_source": peak_src,
                          "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model, BASELINE.md §3.5) "
                                         "per GPU, summed over the solve's filter calls / CUDA-event (1 GPU) or "
                                         "synchronised (N GPUs) time of those calls; with the 3M filter the DMMA pipe "
-                                        "executes 6 n^2 k (filter_executed_*)"},
+                                        "executes 6 n^2 k, with the real-split filter 4 n^2 k (filter_executed_*)"},
             "filter_tflops_per_gpu": achieved, "filter_frac_of_fp64_peak": (achieved / peak) if achieved else None,
             "filter_algorithm": algo,
             "filter_executed_tflops_per_gpu": achieved * exec_ratio if achieved else None,

@@ -91,6 +91,16 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64
  * critical path (+32 m^2 bytes).  d_sd may be NULL everywhere (sums formed on the fly).      */
 int bse_make_sum_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int64_t cols, void* d_sd);
 
+/* Real-split filter planes (csrc/hop_rs.cuh): d_g (m x 4m doubles, leading dim ldg, even, >= m)
+ * <- [Ai + Bi | Ar - Br | Ar + Br | Ai - Bi] of d_ab = [A | B] (32 m^2 bytes, built once).      */
+int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_g, int64_t ldg);
+/* bse_chebyshev_filter (chebyshev.py:51-75) on the real-split planes: the block is folded to
+ * (X1 + X2, X1 - X2), where H acts through four real m x m planes (4 n^2 k executed flops per
+ * step instead of 6 n^2 k for 3M), filtered, and unfolded.  Same arguments and results as
+ * bse_chebyshev_filter up to rounding; requires B != 0 (BSE_HAM_B_ZERO unset).              */
+int bse_chebyshev_filter_rs(bse_ctx* ctx, const void* d_g, int64_t ldg, int64_t m, void* d_v, int64_t ld, int64_t k,
+                            int deg, double c, double e, double s, void* d_work);
+
 /* Residual norms r_j = ||H v_j - lam_j v_j||_2 (rayleigh_ritz.py:182-190),
  * fused residual-norm epilogue; h_lam (k) in, h_res (k) out on host.      */
 int bse_residuals(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const void* d_v, int64_t ldv, int64_t k,

@@ -69,6 +69,8 @@ _SIGS = {
     "bse_filter_step": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _dbl]),
     "bse_chebyshev_filter": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
     "bse_make_sum_planes": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
+    "bse_make_rs_planes": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64]),
+    "bse_chebyshev_filter_rs": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
     "bse_residuals": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _dp]),
     "bse_s_orthonormalize": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
     "bse_cholqr": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _ip]),
@@ -116,17 +118,21 @@ _STATUS = {
 
 _lib = None
 _lock = threading.Lock()
-# complex multiplication of the Chebyshev-filter products (bse_set_filter_algorithm): 4 or 3
-_ALGOS = {"4m": 4, "3m": 88, "3m-tma-narrow": 82, "3m-tma-wide": 86, "3m-mbcp": 72, "3m-sync": 65,
+# Chebyshev-filter product kernels (bse_set_filter_algorithm codes)
+_ALGOS = {"4m": 4, "3m": 88, "rs": 90, "rs-wide": 91, "rs-tall": 92, "rs-quad": 93, "rs-narrow": 94,
+          "3m-tma-narrow": 82, "3m-tma-wide": 86, "3m-mbcp": 72, "3m-sync": 65,
           "3m-onthefly": 3}
-# default 3M (Gauss) with precomputed operand-sum planes: 25% fewer DMMA, parity-checked at C1
-# (tests/test_gpu_parity.py); BSE200_FILTER=4m restores the 4M split
-_FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "3m").lower()]
+# BSE200_FILTER=3m / 4m select the Gauss 3M / plain 4M complex splits for every product;
+# default "rs": the real-split filter (csrc/hop_rs.cuh, 4 n^2 k executed flops per step) for
+# single-GPU filters with B != 0; every other product (RR, 2D-grid tiles, B = 0) runs "3m"
+_FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "rs").lower()]
 
 
 def set_filter_algorithm(name: str) -> None:
-    """'3m' (default: Gauss split, 25% fewer FP64 tensor ops in the filter, the operand sums of A and B
-    precomputed once (+32 m^2 bytes), TMA-fed producer-warp kernel), its fixed tiles '3m-tma-narrow' /
+    """'rs' (default: the single-GPU filter on the real-split planes of csrc/hop_rs.cuh, half the FP64
+    tensor ops of 4M, +32 m^2 bytes; fixed tiles 'rs-wide' / 'rs-tall' / 'rs-quad' / 'rs-narrow', all
+    bitwise identical; every other product runs '3m'), '3m' (Gauss split, 25% fewer FP64 tensor ops,
+    the operand sums of A and B precomputed once (+32 m^2 bytes), TMA-fed producer-warp kernel), its fixed tiles '3m-tma-narrow' /
     '3m-tma-wide', the earlier pipelines '3m-mbcp' / '3m-sync' (all bitwise identical),
     '3m-onthefly' (sums formed in registers) or '4m'."""
     global _FILTER_CM
@@ -157,7 +163,12 @@ def filter_precision() -> str:
 
 
 def uses_sum_planes() -> bool:
-    return _FILTER_CM in (65, 72, 82, 86, 88)
+    return _FILTER_CM in (65, 72, 82, 86, 88) or uses_rs_planes()
+
+
+def uses_rs_planes() -> bool:
+    """real-split filter (codes 90-94, csrc/hop_rs.cuh); the other products run the 3M kernel (88)"""
+    return 90 <= _FILTER_CM <= 94
 
 
 def load() -> C.CDLL:

@@ -52,10 +52,22 @@ def filter_inplace(ham: BseHamiltonian, v, cfg: FilterConfig, work=None, ledger:
 
         work = torch.empty(2 * ld_of(v) * k, dtype=torch.complex128, device=v.device)
     ab = ham.device_blocks(v.device)
+    ctx = _lib.Context.get(v.device.index)
+    if _lib.uses_rs_planes():
+        # real-split filter: 4 n^2 k executed flops per step (csrc/hop_rs.cuh); the RR's S H Q keeps the
+        # 3M kernel, so the sum planes are built first and the RS planes only where both fit
+        if _lib.uses_sum_planes():
+            ham.device_sum_planes(v.device, reserve=2 * 16 * ld_of(v) * k)
+        g = ham.device_rs_planes(v.device, reserve=2 * 16 * ld_of(v) * k)
+        if g is not None:
+            ctx.call("bse_chebyshev_filter_rs", _lib.dptr(g), g.stride(1), ham.m, _lib.dptr(v), ld_of(v), k,
+                     cfg.degree, cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))
+            if ledger is not None:
+                ledger.add_flops("filter", cfg.degree * 8.0 * n * n * k)
+            return v
     # the planes must leave room for the RR's T and residual blocks (2 n k) next to the filter's buffers
     sdt = ham.device_sum_planes(v.device, reserve=2 * 16 * ld_of(v) * k) if _lib.uses_sum_planes() else None
     sd = _lib.dptr(sdt) if sdt is not None else None
-    ctx = _lib.Context.get(v.device.index)
     ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(v), ld_of(v), k, cfg.degree,
              cfg.center, cfg.half_width, cfg.scale_ref, _lib.dptr(work))
     if ledger is not None:

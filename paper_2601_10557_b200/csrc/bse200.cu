@@ -22,6 +22,7 @@
 #include "c64.cuh"
 #include "hop.cuh"
 #include "hop_mb.cuh"
+#include "hop_rs.cuh"
 #include "zgemm.cuh"
 
 using bse::zval;
@@ -305,12 +306,16 @@ using Hop3MWide = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 using Hop3MNarrowNP = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 0>;
 using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 
-bool filter_code_needs_planes(int code) { return code == 65 || code == 72 || code == 82 || code == 86 || code == 88; }
+// 90: the real-split filter (hop_rs.cuh) for bse_chebyshev_filter_rs; every other product
+// (RR's S H Q, the distributed tiles) runs code 88 under it
+bool filter_code_needs_planes(int code) {
+  return code == 65 || code == 72 || code == 82 || code == 86 || code == 88 || (code >= 90 && code <= 94);
+}
 bool filter_code_valid(int code) { return code == 3 || code == 4 || filter_code_needs_planes(code); }
 
 // Chebyshev-step products, as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
-  int code = ctx->filter_cm;
+  int code = ctx->filter_cm >= 90 ? 88 : ctx->filter_cm;
   if (filter_code_needs_planes(code) && (!a.sa || !a.sb))  // no P sum planes: sums in registers
     code = code == 88 ? 98 : 3;
   switch (code) {
@@ -335,6 +340,61 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
     case 65: launch_hop<Hop3MSync, bse::HOP_AXPBY, 6>(ctx, a); break;
     case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     default: launch_hop<HopMain, bse::HOP_AXPBY, 4>(ctx, a); break;
+  }
+}
+
+// ---- real-split filter (hop_rs.cuh) ----
+// tiles (codes for bse_set_filter_algorithm; 90 picks 92 from 512 columns, else 94;
+// profiles/r01/tune_rs.txt: 223 / 60 / 24 ms per C3 step at k = 1200 / 300 / 100 vs 346 / 91 / 33 for 3M):
+//   91  128 x 64, 8 consumer warps of 32 x 32, 4 stages (9 warps: capped at 168 registers)
+//   92  128 x 32, 8 consumer warps of 32 x 16, 6 stages
+//   93  64 x 64, 4 consumer warps of 32 x 32, 6 stages (5 warps: up to 255 registers)
+//   94  64 x 32, 8 consumer warps of 16 x 16, 5 stages, 2 CTAs / SM
+using RsWide = bse::RsCfg<128, 64, 16, 4, 4, 4, 1>;
+using RsTall = bse::RsCfg<128, 32, 16, 4, 2, 6, 1>;
+using RsQuad = bse::RsCfg<64, 64, 16, 4, 4, 6, 1>;
+using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
+
+template <class C>
+void launch_rs(bse_ctx* ctx, const bse::RsArgs& a, const double* g, int64_t ldg) {
+  static bool configured = false;
+  if (!configured) {
+    CUDA_OK(cudaFuncSetAttribute(bse::hop_rs_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    configured = true;
+  }
+  bse::RsMaps mp;
+  for (int q = 0; q < 4; ++q)
+    mp.g[q] = map2d_f64(g + (int64_t)q * a.m * ldg, a.m, a.m, ldg * 8, C::LDP, C::BK);
+  mp.x[0] = map2d_f64(a.cur, 2 * (uint64_t)a.m, a.k, a.ld * 16, 2 * C::LDX, C::BN);
+  mp.x[1] = map2d_f64(a.cur + a.m, 2 * (uint64_t)a.m, a.k, a.ld * 16, 2 * C::LDX, C::BN);
+  const int nbm = (a.m + C::BM - 1) / C::BM;
+  dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm);
+  bse::hop_rs_tma_kernel<C><<<grid, C::THREADS + 32, C::SMEM, ctx->stream>>>(a, mp);
+  check_launch(ctx);
+}
+
+void rs_step(bse_ctx* ctx, const double* g, int64_t ldg, int64_t m, const zval* cur, const zval* prev, zval* next,
+             int64_t ld, int64_t k, double c, double alpha, double beta) {
+  bse::RsArgs a{};
+  a.m = (int)m;
+  a.k = (int)k;
+  a.ld = ld;
+  a.cur = cur;
+  a.prev = prev;
+  a.next = next;
+  a.alpha = alpha;
+  a.beta = beta;
+  a.shift = c;
+  switch (ctx->filter_cm) {
+    case 91: launch_rs<RsWide>(ctx, a, g, ldg); break;
+    case 92: launch_rs<RsTall>(ctx, a, g, ldg); break;
+    case 93: launch_rs<RsQuad>(ctx, a, g, ldg); break;
+    case 94: launch_rs<RsNarrow>(ctx, a, g, ldg); break;
+    default:
+      if (k >= 512)
+        launch_rs<RsTall>(ctx, a, g, ldg);
+      else
+        launch_rs<RsNarrow>(ctx, a, g, ldg);
   }
 }
 
@@ -909,7 +969,7 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     if (!filter_code_valid(complex_mults))
-      throw BseError(BSE_EVALIDATION, "filter algorithm must be 3, 4, 65, 72, 82, 86 or 88 (include/bse200.h)");
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 3, 4, 65, 72, 82, 86, 88 or 90-94 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }
@@ -977,6 +1037,48 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64
     }
     if (cur != 0)
       CUDA_OK(cudaMemcpyAsync(bufs[0], bufs[cur], sizeof(zval) * ld * k, cudaMemcpyDeviceToDevice, ctx->stream));
+  });
+}
+
+int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_g, int64_t ldg) {
+  return guarded(ctx, [&] {
+    if (m < 0 || lda < m || ldg < m || (ldg & 1)) throw BseError(BSE_EVALIDATION, "bad shapes (ldg must be even, >= m)");
+    if (m == 0) return;
+    bse::rs_planes_kernel<<<grid1d(m * m, 256, 148 * 32), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ab), lda, m,
+                                                                               static_cast<double*>(d_g), ldg);
+    check_launch(ctx);
+  });
+}
+
+int bse_chebyshev_filter_rs(bse_ctx* ctx, const void* d_g, int64_t ldg, int64_t m, void* d_v, int64_t ld, int64_t k,
+                            int deg, double c, double e, double s, void* d_work) {
+  return guarded(ctx, [&] {
+    if (deg < 2 || deg % 2) throw BseError(BSE_EVALIDATION, "filter degree must be even and >= 2");
+    if (!(e > 0)) throw BseError(BSE_EVALIDATION, "filter half width must be positive");
+    if (m < 0 || k < 0 || ldg < m || (ldg & 1) || ld < 2 * m) throw BseError(BSE_EVALIDATION, "bad shapes");
+    if (ctx->ham_flags & BSE_HAM_B_ZERO) throw BseError(BSE_EVALIDATION, "the real-split filter needs B != 0");
+    if (k == 0 || m == 0) return;
+    const double* g = static_cast<const double*>(d_g);
+    zval* bufs[3] = {static_cast<zval*>(d_v), static_cast<zval*>(d_work), static_cast<zval*>(d_work) + ld * k};
+    const int fb = grid1d(m * k, 256, 148 * 16);
+    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(bufs[0], bufs[0], ld, m, k, 1.0);
+    check_launch(ctx);
+    // the recurrence of bse_chebyshev_filter (chebyshev.py:58-74) in the folded basis
+    const double sigma1 = e / (s - c);
+    double sigma = sigma1;
+    int prev = 0, cur = 1;
+    rs_step(ctx, g, ldg, m, bufs[0], nullptr, bufs[1], ld, k, c, sigma1 / e, 0.0);
+    for (int step = 2; step <= deg; ++step) {
+      const double sigma_new = 1.0 / (2.0 / sigma1 - sigma);
+      const int nxt = 3 - prev - cur;
+      rs_step(ctx, g, ldg, m, bufs[cur], bufs[prev], bufs[nxt], ld, k, c, 2.0 * sigma_new / e, sigma * sigma_new);
+      prev = cur;
+      cur = nxt;
+      sigma = sigma_new;
+    }
+    // unfold into d_v: X1 = (x + y) / 2, X2 = (x - y) / 2
+    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(bufs[cur], bufs[0], ld, m, k, 0.5);
+    check_launch(ctx);
   });
 }
 

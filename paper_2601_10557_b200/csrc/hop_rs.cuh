@@ -1,0 +1,224 @@
+// Real-split ("RS") H operator: the filter product in the basis that diagonalises the
+// pseudo-hermitian structure, 8 m^2 k real MACs per application instead of 12 m^2 k (3M) or
+// 16 m^2 k (4M).
+//
+// With A = Ar + i Ai (hermitian) and B = Br + i Bi (symmetric), a state X = [X1; X2] is kept as
+//   x = X1 + X2,   y = X1 - X2                                   (rs_fold_kernel)
+// and H = [[A, B], [-conj B, -conj A]] (hamiltonian.py:132-151) acts on (x, y) as
+//   x' = i Z x + V y,   y' = U x + i W y
+// with the four REAL m x m planes
+//   Z = Ai + Bi,  V = Ar - Br,  U = Ar + Br,  W = Ai - Bi        (rs_planes_kernel)
+// (expand H X and collect the real and imaginary parts of X1' +- X2': the conjugations pair up so
+// every plane multiplies a whole complex column).  A real plane times a complex column is 2 real
+// products, so one application is 2 halves x 2 planes x 2 = 8 m^2 k DMMA MACs = 4 n^2 k flops,
+// 2/3 of the 3M kernel's 6 n^2 k.  The filter's scalars (c, alpha, beta) are real, so the whole
+// three-term recurrence (chebyshev.py:68-74) runs in the (x, y) basis and the block is unfolded
+// once at the end (X1 = (x + y) / 2, X2 = (x - y) / 2; the factors of 2 are exact).
+//
+// Planes: one m x 4m real column-major array, plane q in columns [q m, (q + 1) m):
+//   q = 0: Z, 1: V (output half x'), 2: U, 3: W (output half y').
+// Output half h contracts plane 2h against x (part 0) and plane 2h + 1 against y (part 1); the
+// pair (h, part) with h == part multiplies by i, done by rotating the B fragments in registers.
+//
+// Feed: the TMA / producer-warp / mbarrier ring of hop3m_tma_kernel (hop_mb.cuh).  The real plane
+// tile lands with pitch BM + 4 doubles (== 4 mod 16: the 16 lanes of each half warp read 16
+// distinct 8-byte slots, conflict-free LDS.64), the complex X tile with pitch BK + 4 (LDS.128).
+#pragma once
+#include <cuda.h>
+
+#include "hop_mb.cuh"
+#include "tc_common.cuh"
+
+namespace bse {
+
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, int MINB_>
+struct RsCfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int WARPS_M = BM / (8 * WM);
+  static constexpr int WARPS_N = BN / (8 * WN);
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;  // consumer threads (+ one producer warp)
+  static constexpr int LDP = BM + 4;                      // doubles
+  static constexpr int LDX = BK + 4;                      // complex
+  static constexpr int P_BYTES = BK * LDP * 8;
+  static constexpr int X_BYTES = BN * LDX * 16;
+  static constexpr int STAGE_BYTES = P_BYTES + X_BYTES;
+  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 128;
+  static_assert(BM % 16 == 0 && BN % 8 == 0 && BK % 4 == 0, "RS tile dims");
+  static_assert(P_BYTES % 128 == 0 && X_BYTES % 128 == 0, "TMA destinations must stay 128-byte aligned");
+  static_assert(LDP <= 256 && 2 * LDX <= 256 && BN <= 256 && BK <= 256, "TMA box dimensions");
+};
+
+struct RsArgs {
+  int m, k;
+  int64_t ld;        // leading dimension (complex) of the state blocks
+  const zval* cur;   // Y_j   (x rows [0, m), y rows [m, 2m))
+  const zval* prev;  // Y_j-1 (may be null when beta == 0)
+  zval* next;        // Y_j+1
+  double alpha, beta, shift;  // next = alpha (H cur - shift cur) - beta prev
+};
+
+struct RsMaps {
+  CUtensorMap g[4];  // planes Z, V, U, W: m x m doubles, leading dim ldg
+  CUtensorMap x[2];  // x and y parts of cur: (2 m doubles) x k, leading dim 2 ld
+};
+
+template <bool ROT, class C>
+__device__ __forceinline__ void rs_stage_mma(double (&acc)[2][C::WM][C::WN][2], const double* Ps, const zval* Xs, int wm,
+                                             int wn, int g, int t) {
+#pragma unroll
+  for (int ks = 0; ks < C::BK / 4; ++ks) {
+    double pf[C::WM];
+    double br[C::WN], bi[C::WN];
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i) pf[i] = Ps[(ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j) {
+      const zval xv = lds128(Xs + (wn * (8 * C::WN) + j * 8 + g) * C::LDX + ks * 4 + t);
+      if constexpr (ROT) {  // i * x
+        br[j] = -xv.im;
+        bi[j] = xv.re;
+      } else {
+        br[j] = xv.re;
+        bi[j] = xv.im;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j) {
+        dmma(acc[0][i][j], pf[i], br[j]);
+        dmma(acc[1][i][j], pf[i], bi[j]);
+      }
+  }
+}
+
+// grid: x = column tiles (fastest: CTAs sharing a plane strip run together), y = 2 * row tiles
+template <class C>
+__global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(const RsArgs a,
+                                                                              const __grid_constant__ RsMaps maps) {
+  constexpr int NWARPS = C::THREADS / 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
+  const int nbm = (a.m + C::BM - 1) / C::BM;
+  const int h = blockIdx.y >= nbm;  // output half: 0 -> x', 1 -> y'
+  const int i0 = (blockIdx.y - h * nbm) * C::BM;
+  const int c0 = blockIdx.x * C::BN;
+  const int nkt_part = (a.m + C::BK - 1) / C::BK;
+  const int nkt = 2 * nkt_part;
+
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init_cta(&full[s], 1);
+      mbar_init_cta(&empty[s], NWARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    tc::prefetch_tmap(&maps.g[2 * h]);
+    tc::prefetch_tmap(&maps.g[2 * h + 1]);
+    tc::prefetch_tmap(&maps.x[0]);
+    tc::prefetch_tmap(&maps.x[1]);
+  }
+  __syncthreads();
+
+  if (warp == NWARPS) {
+    if (lane == 0) {
+      for (int lkt = 0; lkt < nkt; ++lkt) {
+        const int b = lkt % C::STAGES;
+        if (lkt >= C::STAGES) mbar_wait_cta(&empty[b], ((lkt - C::STAGES) / C::STAGES) & 1);
+        const int part = lkt >= nkt_part;
+        const int j0 = (lkt - part * nkt_part) * C::BK;
+        unsigned char* st = base + b * C::STAGE_BYTES;
+        tc::mbar_arrive_expect_tx(&full[b], C::STAGE_BYTES);
+        tc::tma_load_2d(st, &maps.g[2 * h + part], &full[b], i0, j0);
+        tc::tma_load_2d(st + C::P_BYTES, &maps.x[part], &full[b], 2 * j0, c0);
+      }
+    }
+    return;
+  }
+
+  double acc[2][C::WM][C::WN][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i)
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
+
+#pragma unroll 1
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int s = kt % C::STAGES;
+    mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
+    const double* Ps = reinterpret_cast<const double*>(base + s * C::STAGE_BYTES);
+    const zval* Xs = reinterpret_cast<const zval*>(base + s * C::STAGE_BYTES + C::P_BYTES);
+    if ((kt >= nkt_part) == (h == 1))
+      rs_stage_mma<true, C>(acc, Ps, Xs, wm, wn, g, t);
+    else
+      rs_stage_mma<false, C>(acc, Ps, Xs, wm, wn, g, t);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(&empty[s]);
+  }
+
+  // epilogue: next = alpha (acc - shift cur) - beta prev, rows h m + row of the state
+  const int64_t roff = (int64_t)h * a.m;
+#pragma unroll
+  for (int i = 0; i < C::WM; ++i) {
+    const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
+    if (row >= a.m) continue;
+#pragma unroll
+    for (int j = 0; j < C::WN; ++j) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + hh;
+        if (col >= a.k) continue;
+        const int64_t o = (int64_t)col * a.ld + roff + row;
+        double vr = acc[0][i][j][hh], vi = acc[1][i][j][hh];
+        if (a.shift != 0.0) {
+          const zval s = a.cur[o];
+          vr = vr - a.shift * s.re;
+          vi = vi - a.shift * s.im;
+        }
+        zval out{a.alpha * vr, a.alpha * vi};
+        if (a.beta != 0.0) {
+          const zval p = a.prev[o];
+          out.re = out.re - a.beta * p.re;
+          out.im = out.im - a.beta * p.im;
+        }
+        a.next[o] = out;
+      }
+    }
+  }
+}
+
+// planes of [A | B] (m x 2m complex, leading dim lda) -> m x 4m real (leading dim ldg)
+__global__ void rs_planes_kernel(const zval* __restrict__ ab, int64_t lda, int64_t m, double* __restrict__ gp,
+                                 int64_t ldg) {
+  const int64_t total = m * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m, j = idx / m;
+    const zval av = ab[j * lda + i];
+    const zval bv = ab[(m + j) * lda + i];
+    gp[j * ldg + i] = av.im + bv.im;            // Z
+    gp[(m + j) * ldg + i] = av.re - bv.re;      // V
+    gp[(2 * m + j) * ldg + i] = av.re + bv.re;  // U
+    gp[(3 * m + j) * ldg + i] = av.im - bv.im;  // W
+  }
+}
+
+// (X1, X2) -> scale (X1 + X2, X1 - X2): fold with scale 1, unfold with scale 1/2 (src may equal dst)
+__global__ void rs_fold_kernel(const zval* src, zval* dst, int64_t ld, int64_t m, int64_t k, double scale) {
+  const int64_t total = m * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx % m, j = idx / m;
+    const zval a = src[j * ld + i], b = src[j * ld + m + i];
+    dst[j * ld + i] = zval{scale * (a.re + b.re), scale * (a.im + b.im)};
+    dst[j * ld + m + i] = zval{scale * (a.re - b.re), scale * (a.im - b.im)};
+  }
+}
+
+}  // namespace bse

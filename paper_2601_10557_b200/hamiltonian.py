@@ -202,6 +202,28 @@ class BseHamiltonian:
             sd_cache[device] = sd
         return sd
 
+    def device_rs_planes(self, device, reserve: int = 0):
+        """The four real planes [Ai + Bi | Ar - Br | Ar + Br | Ai - Bi] (m x 4m doubles, bse_make_rs_planes)
+        of the real-split filter (csrc/hop_rs.cuh), built once per device; None when B == 0 (the 3M
+        kernel skips the B half there) or when they would not leave `reserve` bytes of HBM."""
+        torch = _torch()
+        device = torch.device(device)
+        cache = self.__dict__.setdefault("_rs", {})
+        g = cache.get(device)
+        if g is False:
+            return None
+        if g is None:
+            ab = self.device_blocks(device)
+            m = self.m
+            ldg = m + (m & 1)
+            if self.b_is_zero or not _lib.planes_fit(ldg * 4 * m * 8, device, reserve):
+                cache[device] = False
+                return None
+            g = torch.empty((4 * m, ldg), dtype=torch.float64, device=device).t()  # column-major m x 4m, ld ldg
+            _lib.Context.get(device.index).call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(g), ldg)
+            cache[device] = g
+        return g
+
     def device_c64_planes(self, device):
         """fp32 hi/lo planes of [A | B] in the K-major layout of the tcgen05 c64 filter
         (bse_c64_prepare; 32 m mp bytes), built once per device."""

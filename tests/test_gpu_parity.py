@@ -287,7 +287,8 @@ def test_c1_parity(bse, c1_instance):
         assert np.abs(ov - 1).max() <= 1e-8
 
 
-@pytest.mark.parametrize("algo", ["3m", "3m-tma-narrow", "3m-tma-wide", "3m-mbcp", "3m-sync", "3m-onthefly", "4m"])
+@pytest.mark.parametrize("algo", ["3m", "3m-tma-narrow", "3m-tma-wide", "3m-mbcp", "3m-sync", "3m-onthefly", "4m",
+                                  "rs", "rs-wide", "rs-tall", "rs-quad", "rs-narrow"])
 def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
@@ -344,6 +345,51 @@ def test_filter_3m_variants_bitwise_identical(bse):
         bse.set_filter_algorithm(default)
     for (algo, kk), v in outs.items():
         assert torch.equal(v, outs[("3m-sync", kk)]), (algo, kk)
+
+
+def test_filter_rs_matches_3m_and_tiles_bitwise(bse):
+    """Real-split filter (csrc/hop_rs.cuh: folded basis, four real planes, 4 n^2 k flops per step)
+    against the 3M filter at ragged shapes: within 1e-12 of the output scale; its tile variants
+    accumulate each output in the same K order, so they agree bit for bit."""
+    import torch
+    from paper_2601_10557_b200.hamiltonian import colmajor_empty, ld_of
+    from paper_2601_10557_b200 import _lib
+
+    dev = torch.device("cuda", 0)
+    ctx = _lib.Context.get(0)
+    gen = torch.Generator(device=dev).manual_seed(9)
+    default = bse.filter_algorithm()
+    try:
+        for m, k in ((203, 530), (203, 100), (37, 7), (1, 1)):
+            ab = colmajor_empty(m, 2 * m, dev)
+            ab.copy_(torch.complex(torch.randn(m, 2 * m, generator=gen, device=dev, dtype=torch.float64),
+                                   torch.randn(m, 2 * m, generator=gen, device=dev, dtype=torch.float64)))
+            sd = colmajor_empty(m, 2 * m, dev)
+            ctx.call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), m, 2 * m, _lib.dptr(sd))
+            ldg = m + (m & 1)
+            gp = torch.empty((4 * m, ldg), dtype=torch.float64, device=dev).t()
+            ctx.call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(gp), ldg)
+            v0 = colmajor_empty(2 * m, k, dev)
+            v0.copy_(torch.complex(torch.randn(2 * m, k, generator=gen, device=dev, dtype=torch.float64),
+                                   torch.randn(2 * m, k, generator=gen, device=dev, dtype=torch.float64)))
+            work = torch.empty(2 * 2 * m * k, dtype=torch.complex128, device=dev)
+            bse.set_filter_algorithm("3m")
+            ref = v0.clone()
+            ctx.call("bse_chebyshev_filter", _lib.dptr(ab), _lib.dptr(sd), ld_of(ab), m, _lib.dptr(ref), 2 * m, k, 4,
+                     0.5, 2.0, -3.0, _lib.dptr(work))
+            outs = {}
+            for algo in ("rs", "rs-wide", "rs-tall", "rs-quad", "rs-narrow"):
+                bse.set_filter_algorithm(algo)
+                v = v0.clone()
+                ctx.call("bse_chebyshev_filter_rs", _lib.dptr(gp), ldg, m, _lib.dptr(v), 2 * m, k, 4, 0.5, 2.0, -3.0,
+                         _lib.dptr(work))
+                outs[algo] = v
+            scale = ref.abs().max().item()
+            assert (outs["rs"] - ref).abs().max().item() <= 1e-12 * scale, (m, k)
+            for algo, v in outs.items():
+                assert torch.equal(v, outs["rs"]), (algo, m, k)
+    finally:
+        bse.set_filter_algorithm(default)
 
 
 def test_fused_residuals_match_explicit(bse, c1_instance):
