@@ -91,9 +91,15 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64
  * critical path (+32 m^2 bytes).  d_sd may be NULL everywhere (sums formed on the fly).      */
 int bse_make_sum_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int64_t cols, void* d_sd);
 
-/* Real-split filter planes (csrc/hop_rs.cuh): d_g (m x 4m doubles, leading dim ldg, even, >= m)
- * <- [Ai + Bi | Ar - Br | Ar + Br | Ai - Bi] of d_ab = [A | B] (32 m^2 bytes, built once).      */
-int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_g, int64_t ldg);
+/* Real-split filter planes (csrc/hop_rs.cuh): d_g (mr x 4kc doubles, leading dim ldg, even, >= mr)
+ * <- [Ai + Bi | Ar - Br | Ar + Br | Ai - Bi] of a tile d_ab = [A_t | B_t] (mr x 2kc complex;
+ * mr = kc = m for the whole operator: 32 m^2 bytes, built once).                              */
+int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t mr, int64_t kc, void* d_g, int64_t ldg);
+/* Register real-split planes d_g (bse_make_rs_planes, mr = kc = m) of the operator d_ab on the
+ * context: while registered, the T = (S) H Q products of bse_rr_hermitian / bse_rr_backup with
+ * this d_ab run on the real-split kernel (fold Q, product, unfold with the S-flip).  d_g = NULL
+ * clears the registration (the Python layer scopes it to one RR call).                          */
+int bse_set_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t m, const void* d_g, int64_t ldg);
 /* bse_chebyshev_filter (chebyshev.py:51-75) on the real-split planes: the block is folded to
  * (X1 + X2, X1 - X2), where H acts through four real m x m planes (4 n^2 k executed flops per
  * step instead of 6 n^2 k for 3M), filtered, and unfolded.  Same arguments and results as
@@ -174,6 +180,15 @@ typedef struct {
   int filter; /* 1: a Chebyshev-filter product (uses the algorithm set by bse_set_filter_algorithm) */
 } bse_hop_tile_args;
 int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* args);
+/* The tile product of a filter step on the tile's real-split planes d_g (bse_make_rs_planes of
+ * [pa | pb]): x1 / x2 are the folded parts (X1 + X2, X1 - X2) of the input rows, y1 / y2 receive
+ * the folded halves of the output; low_sign must be 1 (no S-flip); B != 0.  pa / pb / sa / sb are
+ * not read.  The 2D-grid filter folds its block once (bse_rs_fold), runs deg such products with
+ * the same reductions as bse_hop_tile, and unfolds.                                            */
+int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* args, const void* d_g, int64_t ldg);
+/* (X1, X2) -> scale (X1 + X2, X1 - X2) for a block of 2 rows x k (ld >= 2 rows; X1 rows [0, rows),
+ * X2 rows [rows, 2 rows)); scale 1 folds, 1/2 unfolds; d_dst may equal d_src.                  */
+int bse_rs_fold(bse_ctx* ctx, const void* d_src, void* d_dst, int64_t ld, int64_t rows, int64_t k, double scale);
 /* CholQR factor step (ortho.py:115-119): hermitise the summed Gram d_g (k x k), add shift I,
  * R = chol upper (in d_g), |diag R| -> d_rdiag (nullable), R^{-1} -> d_rinv; *h_info > 0 on failure. */
 int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv, double* d_rdiag, int* h_info);

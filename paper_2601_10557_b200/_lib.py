@@ -69,7 +69,8 @@ _SIGS = {
     "bse_filter_step": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _i64, _dbl, _dbl, _dbl]),
     "bse_chebyshev_filter": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
     "bse_make_sum_planes": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp]),
-    "bse_make_rs_planes": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64]),
+    "bse_make_rs_planes": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64]),
+    "bse_set_rs_planes": (C.c_int, [_vp, _vp, _i64, _vp, _i64]),
     "bse_chebyshev_filter_rs": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, C.c_int, _dbl, _dbl, _dbl, _vp]),
     "bse_residuals": (C.c_int, [_vp, _vp, _i64, _i64, _vp, _i64, _i64, _dp, _dp]),
     "bse_s_orthonormalize": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
@@ -80,6 +81,8 @@ _SIGS = {
     "bse_lanczos_sweep": (C.c_int, [_vp, _vp, _i64, _i64, _vp, C.c_int, _dp, _dp, _ip]),
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
+    "bse_hop_tile_rs": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
+    "bse_rs_fold": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _dbl]),
     "bse_c64_tile_planes": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_c64_tile_step": (C.c_int, [_vp, C.POINTER(C64TileArgs)]),
     "bse_c64_split": (C.c_int, [_vp, _vp, _i64, _i64, _vp]),

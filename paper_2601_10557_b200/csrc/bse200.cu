@@ -39,6 +39,10 @@ struct bse_ctx {
   std::string err;
   int64_t launches = 0;
   void* ws = nullptr;  // general device scratch
+  // real-split planes registered for the RR products of one operator (bse_set_rs_planes)
+  const void* rs_ab = nullptr;
+  const double* rs_g = nullptr;
+  int64_t rs_ldg = 0, rs_m = 0;
   size_t ws_bytes = 0;
   void* hws = nullptr;  // host scratch (cuSOLVER 64-bit API)
   size_t hws_bytes = 0;
@@ -356,7 +360,7 @@ using RsQuad = bse::RsCfg<64, 64, 16, 4, 4, 6, 1>;
 using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
 
 template <class C>
-void launch_rs(bse_ctx* ctx, const bse::RsArgs& a, const double* g, int64_t ldg) {
+void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   static bool configured = false;
   if (!configured) {
     CUDA_OK(cudaFuncSetAttribute(bse::hop_rs_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
@@ -364,38 +368,50 @@ void launch_rs(bse_ctx* ctx, const bse::RsArgs& a, const double* g, int64_t ldg)
   }
   bse::RsMaps mp;
   for (int q = 0; q < 4; ++q)
-    mp.g[q] = map2d_f64(g + (int64_t)q * a.m * ldg, a.m, a.m, ldg * 8, C::LDP, C::BK);
-  mp.x[0] = map2d_f64(a.cur, 2 * (uint64_t)a.m, a.k, a.ld * 16, 2 * C::LDX, C::BN);
-  mp.x[1] = map2d_f64(a.cur + a.m, 2 * (uint64_t)a.m, a.k, a.ld * 16, 2 * C::LDX, C::BN);
-  const int nbm = (a.m + C::BM - 1) / C::BM;
+    mp.g[q] = map2d_f64(g + (int64_t)q * a.kc * ldg, a.mr, a.kc, ldg * 8, C::LDP, C::BK);
+  mp.x[0] = map2d_f64(a.x1, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
+  mp.x[1] = map2d_f64(a.x2, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
+  const int nbm = (a.mr + C::BM - 1) / C::BM;
   dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm);
   bse::hop_rs_tma_kernel<C><<<grid, C::THREADS + 32, C::SMEM, ctx->stream>>>(a, mp);
   check_launch(ctx);
 }
 
-void rs_step(bse_ctx* ctx, const double* g, int64_t ldg, int64_t m, const zval* cur, const zval* prev, zval* next,
-             int64_t ld, int64_t k, double c, double alpha, double beta) {
-  bse::RsArgs a{};
-  a.m = (int)m;
-  a.k = (int)k;
-  a.ld = ld;
-  a.cur = cur;
-  a.prev = prev;
-  a.next = next;
-  a.alpha = alpha;
-  a.beta = beta;
-  a.shift = c;
+// one real-split product (folded input x1 / x2, output halves y1 / y2) on the tile's planes g
+void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   switch (ctx->filter_cm) {
     case 91: launch_rs<RsWide>(ctx, a, g, ldg); break;
     case 92: launch_rs<RsTall>(ctx, a, g, ldg); break;
     case 93: launch_rs<RsQuad>(ctx, a, g, ldg); break;
     case 94: launch_rs<RsNarrow>(ctx, a, g, ldg); break;
     default:
-      if (k >= 512)
+      if (a.k >= 512)
         launch_rs<RsTall>(ctx, a, g, ldg);
       else
         launch_rs<RsNarrow>(ctx, a, g, ldg);
   }
+}
+
+bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, int64_t k);
+
+void rs_step(bse_ctx* ctx, const double* g, int64_t ldg, int64_t m, const zval* cur, const zval* prev, zval* next,
+             int64_t ld, int64_t k, double c, double alpha, double beta) {
+  bse::HopArgs a = hop_args_single(nullptr, m, m, cur, ld, k);
+  a.y1 = next;
+  a.y2 = next + m;
+  a.ldy = ld;
+  a.s1 = cur;
+  a.s2 = cur + m;
+  a.lds = ld;
+  a.shift = c;
+  a.alpha = alpha;
+  a.beta = beta;
+  if (beta != 0.0) {
+    a.p1 = prev;
+    a.p2 = prev + m;
+    a.ldp = ld;
+  }
+  rs_product(ctx, a, g, ldg);
 }
 
 // k == 1 products (Lanczos): split-K GEMV, partials in the context workspace tail
@@ -448,10 +464,29 @@ bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zva
 
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a);
 
-// y = H x / S H x; with the sum planes d_sd the product takes the filter kernel (3M), else 4M
+bool rs_active(const bse_ctx* ctx, const void* d_ab, int64_t m) {
+  return ctx->rs_g && ctx->rs_ab == d_ab && ctx->rs_m == m && !(ctx->ham_flags & BSE_HAM_B_ZERO);
+}
+
+// y = H x / S H x; with the sum planes d_sd the product takes the filter kernel (3M), else 4M;
+// with real-split planes registered for d_ab and a fold buffer (n x k, ld n) the real-split kernel
 void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, zval* y, int64_t ldy,
-             int64_t k, double low_sign, const void* d_sd = nullptr) {
+             int64_t k, double low_sign, const void* d_sd = nullptr, zval* fold = nullptr) {
   if (k == 0 || m == 0) return;
+  if (k > 1 && fold && rs_active(ctx, d_ab, m)) {
+    const int fb = grid1d(m * k, 256, 148 * 16);
+    // fold x into the buffer, the product into y's halves, then unfold y in place (with the S-flip)
+    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(x, fold, ldx, 2 * m, m, k, 1.0, 1.0);
+    check_launch(ctx);
+    bse::HopArgs a = hop_args_single(d_ab, lda, m, fold, 2 * m, k);
+    a.y1 = y;
+    a.y2 = y + m;
+    a.ldy = ldy;
+    rs_product(ctx, a, ctx->rs_g, ctx->rs_ldg);
+    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(y, y, ldy, ldy, m, k, 0.5, 0.5 * low_sign);
+    check_launch(ctx);
+    return;
+  }
   bse::HopArgs a = hop_args_single(d_ab, lda, m, x, ldx, k);
   a.y1 = y;
   a.y2 = y + m;
@@ -1040,13 +1075,24 @@ int bse_chebyshev_filter(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64
   });
 }
 
-int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, void* d_g, int64_t ldg) {
+int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t mr, int64_t kc, void* d_g, int64_t ldg) {
   return guarded(ctx, [&] {
-    if (m < 0 || lda < m || ldg < m || (ldg & 1)) throw BseError(BSE_EVALIDATION, "bad shapes (ldg must be even, >= m)");
-    if (m == 0) return;
-    bse::rs_planes_kernel<<<grid1d(m * m, 256, 148 * 32), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ab), lda, m,
-                                                                               static_cast<double*>(d_g), ldg);
+    if (mr < 0 || kc < 0 || lda < mr || ldg < mr || (ldg & 1))
+      throw BseError(BSE_EVALIDATION, "bad shapes (ldg must be even, >= mr)");
+    if (mr == 0 || kc == 0) return;
+    bse::rs_planes_kernel<<<grid1d(mr * kc, 256, 148 * 32), 256, 0, ctx->stream>>>(
+        static_cast<const zval*>(d_ab), lda, mr, kc, static_cast<double*>(d_g), ldg);
     check_launch(ctx);
+  });
+}
+
+int bse_set_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t m, const void* d_g, int64_t ldg) {
+  return guarded(ctx, [&] {
+    if (d_g && (m <= 0 || ldg < m || (ldg & 1))) throw BseError(BSE_EVALIDATION, "bad shapes (ldg must be even, >= m)");
+    ctx->rs_ab = d_g ? d_ab : nullptr;
+    ctx->rs_g = static_cast<const double*>(d_g);
+    ctx->rs_ldg = d_g ? ldg : 0;
+    ctx->rs_m = d_g ? m : 0;
   });
 }
 
@@ -1061,7 +1107,7 @@ int bse_chebyshev_filter_rs(bse_ctx* ctx, const void* d_g, int64_t ldg, int64_t 
     const double* g = static_cast<const double*>(d_g);
     zval* bufs[3] = {static_cast<zval*>(d_v), static_cast<zval*>(d_work), static_cast<zval*>(d_work) + ld * k};
     const int fb = grid1d(m * k, 256, 148 * 16);
-    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(bufs[0], bufs[0], ld, m, k, 1.0);
+    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(bufs[0], bufs[0], ld, ld, m, k, 1.0, 1.0);
     check_launch(ctx);
     // the recurrence of bse_chebyshev_filter (chebyshev.py:58-74) in the folded basis
     const double sigma1 = e / (s - c);
@@ -1077,7 +1123,7 @@ int bse_chebyshev_filter_rs(bse_ctx* ctx, const void* d_g, int64_t ldg, int64_t 
       sigma = sigma_new;
     }
     // unfold into d_v: X1 = (x + y) / 2, X2 = (x - y) / 2
-    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(bufs[cur], bufs[0], ld, m, k, 0.5);
+    bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(bufs[cur], bufs[0], ld, ld, m, k, 0.5, 0.5);
     check_launch(ctx);
   });
 }
@@ -1185,9 +1231,11 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t l
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
     const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
+    const bool rs = k > 1 && rs_active(ctx, d_ab, m);
     Scratch sc(ctx, (h_res ? 2 : 1) * al(n * k * sizeof(zval)) + 3 * al(kk * sizeof(zval)) + 4 * al(k * 8) + gwsb +
-                        pencil_ws_bytes(k) + 4096);
+                        pencil_ws_bytes(k) + 4096 + (rs ? al(n * k * sizeof(zval)) : 0));
     zval* t = sc.take<zval>(n * k);
+    zval* fold = rs ? sc.take<zval>(n * k) : nullptr;
     zval* u = h_res ? sc.take<zval>(n * k) : nullptr;
     double* d_lam = sc.take<double>(k);
     double* d_rinv = sc.take<double>(k);
@@ -1199,7 +1247,7 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t l
     zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
     StepTimer tm(ctx, "rr_hermitian");
     // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T ; Q2^H Q2
-    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0, d_sd);
+    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0, d_sd, fold);
     tm.mark("T = S H Q", k);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
     zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
@@ -1311,8 +1359,11 @@ int bse_rr_backup(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda,
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
     const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
-    Scratch sc(ctx, al(n * k * sizeof(zval)) + 4 * al(kk * sizeof(zval)) + al(k * 8) + gwsb + backup_ws_bytes(k));
+    const bool rs = k > 1 && rs_active(ctx, d_ab, m);
+    Scratch sc(ctx, al(n * k * sizeof(zval)) + 4 * al(kk * sizeof(zval)) + al(k * 8) + gwsb + backup_ws_bytes(k) +
+                        (rs ? al(n * k * sizeof(zval)) : 0));
     zval* t = sc.take<zval>(n * k);
+    zval* fold = rs ? sc.take<zval>(n * k) : nullptr;
     zval* w = sc.take<zval>(kk);
     zval* g2 = sc.take<zval>(kk);
     zval* g = sc.take<zval>(kk);
@@ -1320,7 +1371,7 @@ int bse_rr_backup(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda,
     double* d_nrm = sc.take<double>(k);
     zval* gws = sc.take<zval>(gwsb / sizeof(zval) + 1);
     // rayleigh_ritz.py:160-168
-    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, 1.0, d_sd);
+    apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, 1.0, d_sd, fold);
     zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
     zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
     // g0 = Q^H (S T) = Q1^H T1 - Q2^H T2
@@ -1420,38 +1471,43 @@ int bse_is_definite(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, int*
   });
 }
 
+bse::HopArgs tile_args(const bse_hop_tile_args* t) {
+  bse::HopArgs a{};
+  a.pa = static_cast<const zval*>(t->pa);
+  a.pb = static_cast<const zval*>(t->pb);
+  a.sa = static_cast<const zval*>(t->sa);
+  a.sb = static_cast<const zval*>(t->sb);
+  a.lda = t->lda;
+  a.mr = (int)t->mr;
+  a.kc = (int)t->kc;
+  a.x1 = static_cast<const zval*>(t->x1);
+  a.x2 = static_cast<const zval*>(t->x2);
+  a.ldx = t->ldx;
+  a.k = (int)t->k;
+  a.y1 = static_cast<zval*>(t->y1);
+  a.y2 = static_cast<zval*>(t->y2);
+  a.ldy = t->ldy;
+  a.s1 = static_cast<const zval*>(t->s1);
+  a.s2 = static_cast<const zval*>(t->s2);
+  a.lds = t->lds;
+  a.shift_lo = (int)t->shift_lo;
+  a.shift_hi = (int)t->shift_hi;
+  a.shift = t->shift;
+  a.shift_col = t->d_shift_col;
+  a.p1 = static_cast<const zval*>(t->p1);
+  a.p2 = static_cast<const zval*>(t->p2);
+  a.ldp = t->ldp;
+  a.alpha = t->alpha;
+  a.beta = t->beta;
+  a.low_sign = t->low_sign;
+  return a;
+}
+
 int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* t) {
   return guarded(ctx, [&] {
     if (!t) throw BseError(BSE_EVALIDATION, "null args");
     if (t->k <= 0 || t->mr <= 0) return;
-    bse::HopArgs a{};
-    a.pa = static_cast<const zval*>(t->pa);
-    a.pb = static_cast<const zval*>(t->pb);
-    a.sa = static_cast<const zval*>(t->sa);
-    a.sb = static_cast<const zval*>(t->sb);
-    a.lda = t->lda;
-    a.mr = (int)t->mr;
-    a.kc = (int)t->kc;
-    a.x1 = static_cast<const zval*>(t->x1);
-    a.x2 = static_cast<const zval*>(t->x2);
-    a.ldx = t->ldx;
-    a.k = (int)t->k;
-    a.y1 = static_cast<zval*>(t->y1);
-    a.y2 = static_cast<zval*>(t->y2);
-    a.ldy = t->ldy;
-    a.s1 = static_cast<const zval*>(t->s1);
-    a.s2 = static_cast<const zval*>(t->s2);
-    a.lds = t->lds;
-    a.shift_lo = (int)t->shift_lo;
-    a.shift_hi = (int)t->shift_hi;
-    a.shift = t->shift;
-    a.shift_col = t->d_shift_col;
-    a.p1 = static_cast<const zval*>(t->p1);
-    a.p2 = static_cast<const zval*>(t->p2);
-    a.ldp = t->ldp;
-    a.alpha = t->alpha;
-    a.beta = t->beta;
-    a.low_sign = t->low_sign;
+    bse::HopArgs a = tile_args(t);
     if (a.beta != 0.0 && (!a.p1 || !a.p2)) throw BseError(BSE_EVALIDATION, "beta != 0 needs p1/p2");
     if ((a.shift != 0.0 || a.shift_col) && a.shift_hi > a.shift_lo && (!a.s1 || !a.s2))
       throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
@@ -1463,6 +1519,32 @@ int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* t) {
       launch_filter_hop(ctx, a);
     else
       launch_hop<HopMain, bse::HOP_AXPBY>(ctx, a);
+  });
+}
+
+int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* t, const void* d_g, int64_t ldg) {
+  return guarded(ctx, [&] {
+    if (!t || !d_g) throw BseError(BSE_EVALIDATION, "null args");
+    if (t->k <= 0 || t->mr <= 0) return;
+    bse::HopArgs a = tile_args(t);
+    if (a.kc <= 0) throw BseError(BSE_EVALIDATION, "empty contraction");
+    if (ldg < a.mr || (ldg & 1)) throw BseError(BSE_EVALIDATION, "ldg must be even and >= mr");
+    if (a.low_sign != 1.0) throw BseError(BSE_EVALIDATION, "the real-split product has no S-flip (low_sign 1)");
+    if (a.beta != 0.0 && (!a.p1 || !a.p2)) throw BseError(BSE_EVALIDATION, "beta != 0 needs p1/p2");
+    if ((a.shift != 0.0 || a.shift_col) && a.shift_hi > a.shift_lo && (!a.s1 || !a.s2))
+      throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
+    if (ctx->ham_flags & BSE_HAM_B_ZERO) throw BseError(BSE_EVALIDATION, "the real-split product needs B != 0");
+    rs_product(ctx, a, static_cast<const double*>(d_g), ldg);
+  });
+}
+
+int bse_rs_fold(bse_ctx* ctx, const void* d_src, void* d_dst, int64_t ld, int64_t rows, int64_t k, double scale) {
+  return guarded(ctx, [&] {
+    if (rows < 0 || k < 0 || ld < 2 * rows) throw BseError(BSE_EVALIDATION, "bad shapes");
+    if (rows == 0 || k == 0) return;
+    bse::rs_fold_kernel<<<grid1d(rows * k, 256, 148 * 16), 256, 0, ctx->stream>>>(
+        static_cast<const zval*>(d_src), static_cast<zval*>(d_dst), ld, ld, rows, k, scale, scale);
+    check_launch(ctx);
   });
 }
 

@@ -48,18 +48,12 @@ struct RsCfg {
   static_assert(LDP <= 256 && 2 * LDX <= 256 && BN <= 256 && BK <= 256, "TMA box dimensions");
 };
 
-struct RsArgs {
-  int m, k;
-  int64_t ld;        // leading dimension (complex) of the state blocks
-  const zval* cur;   // Y_j   (x rows [0, m), y rows [m, 2m))
-  const zval* prev;  // Y_j-1 (may be null when beta == 0)
-  zval* next;        // Y_j+1
-  double alpha, beta, shift;  // next = alpha (H cur - shift cur) - beta prev
-};
-
+// Arguments: HopArgs (hop.cuh) with x1 / x2 = the x / y parts of the folded input (kc rows each),
+// y1 / y2 = the x' / y' halves of the output (mr rows each), s1 / s2 and p1 / p2 likewise; the
+// epilogue is hop_epilogue_axpby's with low_sign == 1 (pa, pb, sa, sb, skip_b unused).
 struct RsMaps {
-  CUtensorMap g[4];  // planes Z, V, U, W: m x m doubles, leading dim ldg
-  CUtensorMap x[2];  // x and y parts of cur: (2 m doubles) x k, leading dim 2 ld
+  CUtensorMap g[4];  // planes Z, V, U, W of the tile: mr x kc doubles each, leading dim ldg
+  CUtensorMap x[2];  // x and y parts of the input: (2 kc doubles) x k, leading dim 2 ldx
 };
 
 template <bool ROT, class C>
@@ -94,7 +88,7 @@ __device__ __forceinline__ void rs_stage_mma(double (&acc)[2][C::WM][C::WN][2], 
 
 // grid: x = column tiles (fastest: CTAs sharing a plane strip run together), y = 2 * row tiles
 template <class C>
-__global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(const RsArgs a,
+__global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(const HopArgs a,
                                                                               const __grid_constant__ RsMaps maps) {
   constexpr int NWARPS = C::THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -105,11 +99,11 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
-  const int nbm = (a.m + C::BM - 1) / C::BM;
+  const int nbm = (a.mr + C::BM - 1) / C::BM;
   const int h = blockIdx.y >= nbm;  // output half: 0 -> x', 1 -> y'
   const int i0 = (blockIdx.y - h * nbm) * C::BM;
   const int c0 = blockIdx.x * C::BN;
-  const int nkt_part = (a.m + C::BK - 1) / C::BK;
+  const int nkt_part = (a.kc + C::BK - 1) / C::BK;
   const int nkt = 2 * nkt_part;
 
   if (threadIdx.x == 0) {
@@ -164,60 +158,65 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
     if (lane == 0) mbar_arrive_cta(&empty[s]);
   }
 
-  // epilogue: next = alpha (acc - shift cur) - beta prev, rows h m + row of the state
-  const int64_t roff = (int64_t)h * a.m;
+  // epilogue: y_h = alpha (acc - shift s_h) - beta p_h on the output half h
+  zval* yh = h ? a.y2 : a.y1;
+  const zval* sh = h ? a.s2 : a.s1;
+  const zval* ph = h ? a.p2 : a.p1;
 #pragma unroll
   for (int i = 0; i < C::WM; ++i) {
     const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
-    if (row >= a.m) continue;
+    if (row >= a.mr) continue;
+    const bool shifted = (a.shift != 0.0 || a.shift_col) && row >= a.shift_lo && row < a.shift_hi;
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + hh;
         if (col >= a.k) continue;
-        const int64_t o = (int64_t)col * a.ld + roff + row;
         double vr = acc[0][i][j][hh], vi = acc[1][i][j][hh];
-        if (a.shift != 0.0) {
-          const zval s = a.cur[o];
-          vr = vr - a.shift * s.re;
-          vi = vi - a.shift * s.im;
+        if (shifted) {
+          const double sc = a.shift_col ? a.shift_col[col] : a.shift;
+          const zval s = sh[(int64_t)col * a.lds + row];
+          vr = vr - sc * s.re;
+          vi = vi - sc * s.im;
         }
         zval out{a.alpha * vr, a.alpha * vi};
         if (a.beta != 0.0) {
-          const zval p = a.prev[o];
+          const zval p = ph[(int64_t)col * a.ldp + row];
           out.re = out.re - a.beta * p.re;
           out.im = out.im - a.beta * p.im;
         }
-        a.next[o] = out;
+        yh[(int64_t)col * a.ldy + row] = out;
       }
     }
   }
 }
 
-// planes of [A | B] (m x 2m complex, leading dim lda) -> m x 4m real (leading dim ldg)
-__global__ void rs_planes_kernel(const zval* __restrict__ ab, int64_t lda, int64_t m, double* __restrict__ gp,
+// planes of a tile [A_t | B_t] (mr x 2kc complex, leading dim lda) -> mr x 4kc real (leading dim ldg)
+__global__ void rs_planes_kernel(const zval* __restrict__ ab, int64_t lda, int64_t mr, int64_t kc, double* __restrict__ gp,
                                  int64_t ldg) {
-  const int64_t total = m * m;
+  const int64_t total = mr * kc;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = idx % m, j = idx / m;
+    const int64_t i = idx % mr, j = idx / mr;
     const zval av = ab[j * lda + i];
-    const zval bv = ab[(m + j) * lda + i];
-    gp[j * ldg + i] = av.im + bv.im;            // Z
-    gp[(m + j) * ldg + i] = av.re - bv.re;      // V
-    gp[(2 * m + j) * ldg + i] = av.re + bv.re;  // U
-    gp[(3 * m + j) * ldg + i] = av.im - bv.im;  // W
+    const zval bv = ab[(kc + j) * lda + i];
+    gp[j * ldg + i] = av.im + bv.im;             // Z
+    gp[(kc + j) * ldg + i] = av.re - bv.re;      // V
+    gp[(2 * kc + j) * ldg + i] = av.re + bv.re;  // U
+    gp[(3 * kc + j) * ldg + i] = av.im - bv.im;  // W
   }
 }
 
-// (X1, X2) -> scale (X1 + X2, X1 - X2): fold with scale 1, unfold with scale 1/2 (src may equal dst)
-__global__ void rs_fold_kernel(const zval* src, zval* dst, int64_t ld, int64_t m, int64_t k, double scale) {
+// (X1, X2) -> (scale (X1 + X2), scale2 (X1 - X2)): fold with 1, 1; unfold with 1/2, 1/2 (S-flipped:
+// 1/2, -1/2); src may equal dst (same leading dimension then)
+__global__ void rs_fold_kernel(const zval* src, zval* dst, int64_t lds, int64_t ldd, int64_t m, int64_t k, double scale,
+                               double scale2) {
   const int64_t total = m * k;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = idx % m, j = idx / m;
-    const zval a = src[j * ld + i], b = src[j * ld + m + i];
-    dst[j * ld + i] = zval{scale * (a.re + b.re), scale * (a.im + b.im)};
-    dst[j * ld + m + i] = zval{scale * (a.re - b.re), scale * (a.im - b.im)};
+    const zval a = src[j * lds + i], b = src[j * lds + m + i];
+    dst[j * ldd + i] = zval{scale * (a.re + b.re), scale * (a.im + b.im)};
+    dst[j * ldd + m + i] = zval{scale2 * (a.re - b.re), scale2 * (a.im - b.im)};
   }
 }
 

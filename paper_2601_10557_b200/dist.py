@@ -188,8 +188,10 @@ class CudaOps:
         return self.torch.empty((k, rows), dtype=self.torch.complex128, device=self.device)
 
     def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
-            p=None, low_sign=1.0, filter=False):
-        """y (storage k x 2 mr) = low_sign^{low} (alpha (tile-product of x - shift s) - beta p)."""
+            p=None, low_sign=1.0, filter=False, rs=False):
+        """y (storage k x 2 mr) = low_sign^{low} (alpha (tile-product of x - shift s) - beta p).
+        rs: x, y, s and p are folded (X1 + X2, X1 - X2) and the product runs on the tile's
+        real-split planes (bse_hop_tile_rs)."""
         k = x.shape[0]
         mr, kc = tile.mr, tile.kc
         xa, ya = x.data_ptr(), y.data_ptr()
@@ -210,7 +212,14 @@ class CudaOps:
             args.p1, args.p2, args.ldp = pa_, pa_ + mr * ZB, p.stride(0)
         args.alpha, args.beta, args.low_sign = alpha, beta, low_sign
         args.filter = 1 if filter else 0
-        self.ctx.call("bse_hop_tile", ctypes.byref(args))
+        if rs:
+            self.ctx.call("bse_hop_tile_rs", ctypes.byref(args), tile.g.data_ptr(), tile.ldg)
+        else:
+            self.ctx.call("bse_hop_tile", ctypes.byref(args))
+
+    def rs_fold(self, v, rows: int, scale: float):
+        """(X1, X2) -> scale (X1 + X2, X1 - X2) in place on a (k x 2 rows) storage block (bse_rs_fold)."""
+        self.ctx.call("bse_rs_fold", v.data_ptr(), v.data_ptr(), v.stride(0), rows, v.shape[0], scale)
 
     # ---- complex64 filter (tcgen05, c64.cuh): plane sets of 8 fp32 planes ----------------------
     @staticmethod
@@ -351,6 +360,8 @@ class Tile:
     sd: object = None
     sa: int = 0
     sb: int = 0
+    g: object = None  # optional real-split planes (csrc/hop_rs.cuh), mr x 4kc doubles, leading dim ldg
+    ldg: int = 0
 
 
 def add_sum_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
@@ -366,6 +377,22 @@ def add_sum_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
     ops.ctx.call("bse_make_sum_planes", tile.buf.data_ptr(), tile.lda, tile.mr, 2 * tile.kc, sd.data_ptr())
     tile.sd, tile.sa = sd, sd.data_ptr()
     tile.sb = tile.sa + tile.mr * tile.kc * ZB
+    return tile
+
+
+def add_rs_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
+    """Attach the tile's real-split planes [Ai + Bi | Ar - Br | Ar + Br | Ai - Bi] (bse_make_rs_planes) for
+    the filter products (CUDA ops only, B != 0), if they leave `reserve` bytes of HBM for the solve."""
+    if not hasattr(ops, "ctx"):
+        return tile
+    ldg = tile.mr + (tile.mr & 1)
+    if not _lib.planes_fit(ldg * 4 * tile.kc * 8, ops.device, reserve):
+        logger.warning("real-split planes of a %d x %d tile do not fit; the filter runs the 3M products",
+                       tile.mr, 2 * tile.kc)
+        return tile
+    g = ops.torch.empty((4 * tile.kc, ldg), dtype=ops.torch.float64, device=ops.device)
+    ops.ctx.call("bse_make_rs_planes", tile.buf.data_ptr(), tile.lda, tile.mr, tile.kc, g.data_ptr(), ldg)
+    tile.g, tile.ldg = g, ldg
     return tile
 
 
@@ -480,6 +507,10 @@ class DistSolver:
         if overlap and not hasattr(self, "_comm_stream"):
             self._comm_stream = torch.cuda.Stream(device=v_col.device)
         reduced = [None] * nch
+        # real-split planes on both tiles: run the recurrence in the folded basis (csrc/hop_rs.cuh)
+        rs = hasattr(self.ops, "ctx") and self.fwd.g is not None and self.trn.g is not None
+        if rs:
+            self.ops.rs_fold(v_col, self.g.nc, 1.0)
         for ci in range(nch):
             a, b = edges[ci], edges[ci + 1]
             src, dst = v_col[a:b], row_buf[a:b]
@@ -494,6 +525,8 @@ class DistSolver:
                     kw = dict(alpha=2.0 * sn / e, shift=c, beta=(s * sn) if owner else 0.0,
                               p=dst if owner else None)
                     s = sn
+                if rs:
+                    kw["rs"] = True
                 fwd = step % 2 == 1
                 if overlap:
                     reduced[ci] = self._step_async(src, dst, fwd, kw, comp, reduced[ci])
@@ -503,6 +536,8 @@ class DistSolver:
         if overlap:
             for ev in reduced:
                 comp.wait_event(ev)
+        if rs:
+            self.ops.rs_fold(v_col, self.g.nc, 0.5)
         return v_col  # even degree: the result is back in the col buffer
 
     def chebyshev_c64(self, v_col, cfg: FilterConfig):
@@ -989,6 +1024,12 @@ class DistributedSolver:
             for t in (self.fwd, self.trn):
                 if t.sd is None:
                     add_sum_planes(self.ops, t, reserve)
+        if _lib.uses_rs_planes() and not self.flags & 1:
+            g = self.inner.g
+            reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
+            for t in (self.fwd, self.trn):
+                if t.g is None:
+                    add_rs_planes(self.ops, t, reserve)
         res = self.inner.solve(cfg)
         res.v = res.v.T  # (n, nev) column-major view
         return res

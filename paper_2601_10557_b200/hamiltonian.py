@@ -220,7 +220,7 @@ class BseHamiltonian:
                 cache[device] = False
                 return None
             g = torch.empty((4 * m, ldg), dtype=torch.float64, device=device).t()  # column-major m x 4m, ld ldg
-            _lib.Context.get(device.index).call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(g), ldg)
+            _lib.Context.get(device.index).call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, m, _lib.dptr(g), ldg)
             cache[device] = g
         return g
 

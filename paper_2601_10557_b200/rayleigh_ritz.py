@@ -66,10 +66,16 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     ctx = _lib.Context.get(q.device.index)
     res = np.zeros(k) if fused_residuals else None
     extra = (_lib.hptr(res) if fused_residuals else None,) if entry == "bse_rr_hermitian" else ()
+    # the real-split planes (csrc/hop_rs.cuh), registered for this call only
+    g = ham.device_rs_planes(q.device, reserve=3 * 16 * n * k) if _lib.uses_rs_planes() else None
     try:
+        if g is not None:
+            ctx.call("bse_set_rs_planes", _lib.dptr(ab), ham.m, _lib.dptr(g), g.stride(1))
         ctx.call(entry, _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(q), ld_of(q), k, _lib.hptr(lam), _lib.dptr(vout),
                  ld_of(vout), ctypes.byref(lmm), *extra)
     finally:
+        if g is not None:
+            ctx.call("bse_set_rs_planes", None, 0, None, 0)
         if ledger is not None:
             # apply_h inside RR charges 8n^2k to "rr" (hamiltonian.py:148-150) before the model of
             # rayleigh_ritz.py:139 / :175 — the reference ledger counts both, so do we

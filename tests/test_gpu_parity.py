@@ -184,6 +184,33 @@ def test_rayleigh_ritz_golden(bse):
     assert np.abs(rb.values - g["bk_values"]).max() <= 1e-10 * np.abs(g["bk_values"]).max()
 
 
+def test_rr_products_on_real_split_planes(bse):
+    """The RR's T = S H Q (hermitian) and T = H Q (backup) on the registered real-split planes
+    (bse_set_rs_planes, csrc/hop_rs.cuh) against the 3M products: Ritz values within 1e-12, Ritz
+    vectors phase-invariantly within 1e-10, the registration scoped to the call."""
+    a, b = golden_ham(64, 21)
+    rng = np.random.default_rng(2)
+    q, _ = np.linalg.qr(rng.standard_normal((128, 24)) + 1j * rng.standard_normal((128, 24)))
+    default = bse.filter_algorithm()
+    out = {}
+    try:
+        for algo in ("3m", "rs"):
+            bse.set_filter_algorithm(algo)
+            ham = bse.BseHamiltonian(a, b)
+            ritz, _ = bse.build_hermitian_rq(ham, q)
+            rb, _ = bse.build_backup_rq(ham, q)
+            out[algo] = (ritz, rb, ham)
+    finally:
+        bse.set_filter_algorithm(default)
+    (r3, b3, _), (rr, br, ham_rs) = out["3m"], out["rs"]
+    assert ham_rs.device_rs_planes(0) is not None
+    scale = np.abs(r3.values).max()
+    assert np.abs(rr.values - r3.values).max() <= 1e-12 * scale
+    assert np.abs(br.values - b3.values).max() <= 1e-12 * scale
+    ov = np.abs(np.einsum("ij,ij->j", np.asarray(rr.vectors).conj(), np.asarray(r3.vectors)))
+    assert np.abs(ov - 1).max() <= 1e-10
+
+
 def test_rr_exact_invariant_subspace(bse):
     # test_rayleigh_ritz.py:48-58: RR on an exact invariant subspace reproduces eigenpairs
     a, b = golden_ham(8, 11)
@@ -368,7 +395,7 @@ def test_filter_rs_matches_3m_and_tiles_bitwise(bse):
             ctx.call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), m, 2 * m, _lib.dptr(sd))
             ldg = m + (m & 1)
             gp = torch.empty((4 * m, ldg), dtype=torch.float64, device=dev).t()
-            ctx.call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(gp), ldg)
+            ctx.call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, m, _lib.dptr(gp), ldg)
             v0 = colmajor_empty(2 * m, k, dev)
             v0.copy_(torch.complex(torch.randn(2 * m, k, generator=gen, device=dev, dtype=torch.float64),
                                    torch.randn(2 * m, k, generator=gen, device=dev, dtype=torch.float64)))

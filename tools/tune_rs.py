@@ -21,7 +21,7 @@ sd = colmajor_empty(m, 2 * m, dev)
 ctx.call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), m, 2 * m, _lib.dptr(sd))
 ldg = m + (m & 1)
 gp = torch.empty((4 * m, ldg), dtype=torch.float64, device=dev).t()
-ctx.call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, _lib.dptr(gp), ldg)
+ctx.call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, m, _lib.dptr(gp), ldg)
 for k in ks:
     v0 = colmajor_empty(n, k, dev); v0.real.normal_(); v0.imag.normal_()
     work = torch.empty(2 * n * k, dtype=torch.complex128, device=dev)
