@@ -186,9 +186,11 @@ int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* args);
  * not read.  The 2D-grid filter folds its block once (bse_rs_fold), runs deg such products with
  * the same reductions as bse_hop_tile, and unfolds.                                            */
 int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* args, const void* d_g, int64_t ldg);
-/* (X1, X2) -> scale (X1 + X2, X1 - X2) for a block of 2 rows x k (ld >= 2 rows; X1 rows [0, rows),
- * X2 rows [rows, 2 rows)); scale 1 folds, 1/2 unfolds; d_dst may equal d_src.                  */
-int bse_rs_fold(bse_ctx* ctx, const void* d_src, void* d_dst, int64_t ld, int64_t rows, int64_t k, double scale);
+/* (X1, X2) -> (scale (X1 + X2), scale2 (X1 - X2)) for a block of 2 rows x k (ld >= 2 rows; X1 rows
+ * [0, rows), X2 rows [rows, 2 rows)); (1, 1) folds, (1/2, 1/2) unfolds, (1/2, -1/2) unfolds with
+ * the S-flip; d_dst may equal d_src.                                                           */
+int bse_rs_fold(bse_ctx* ctx, const void* d_src, void* d_dst, int64_t ld, int64_t rows, int64_t k, double scale,
+                double scale2);
 /* CholQR factor step (ortho.py:115-119): hermitise the summed Gram d_g (k x k), add shift I,
  * R = chol upper (in d_g), |diag R| -> d_rdiag (nullable), R^{-1} -> d_rinv; *h_info > 0 on failure. */
 int bse_chol_rinv(bse_ctx* ctx, void* d_g, int64_t k, double shift, void* d_rinv, double* d_rdiag, int* h_info);

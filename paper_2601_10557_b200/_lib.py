@@ -82,7 +82,7 @@ _SIGS = {
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
     "bse_hop_tile_rs": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
-    "bse_rs_fold": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _dbl]),
+    "bse_rs_fold": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _dbl, _dbl]),
     "bse_c64_tile_planes": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_c64_tile_step": (C.c_int, [_vp, C.POINTER(C64TileArgs)]),
     "bse_c64_split": (C.c_int, [_vp, _vp, _i64, _i64, _vp]),

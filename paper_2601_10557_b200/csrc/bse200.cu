@@ -1538,12 +1538,13 @@ int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* t, const void* d_g, i
   });
 }
 
-int bse_rs_fold(bse_ctx* ctx, const void* d_src, void* d_dst, int64_t ld, int64_t rows, int64_t k, double scale) {
+int bse_rs_fold(bse_ctx* ctx, const void* d_src, void* d_dst, int64_t ld, int64_t rows, int64_t k, double scale,
+                double scale2) {
   return guarded(ctx, [&] {
     if (rows < 0 || k < 0 || ld < 2 * rows) throw BseError(BSE_EVALIDATION, "bad shapes");
     if (rows == 0 || k == 0) return;
     bse::rs_fold_kernel<<<grid1d(rows * k, 256, 148 * 16), 256, 0, ctx->stream>>>(
-        static_cast<const zval*>(d_src), static_cast<zval*>(d_dst), ld, ld, rows, k, scale, scale);
+        static_cast<const zval*>(d_src), static_cast<zval*>(d_dst), ld, ld, rows, k, scale, scale2);
     check_launch(ctx);
   });
 }

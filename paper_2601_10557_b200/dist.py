@@ -217,9 +217,12 @@ class CudaOps:
         else:
             self.ctx.call("bse_hop_tile", ctypes.byref(args))
 
-    def rs_fold(self, v, rows: int, scale: float):
-        """(X1, X2) -> scale (X1 + X2, X1 - X2) in place on a (k x 2 rows) storage block (bse_rs_fold)."""
-        self.ctx.call("bse_rs_fold", v.data_ptr(), v.data_ptr(), v.stride(0), rows, v.shape[0], scale)
+    def rs_fold(self, v, rows: int, scale: float, scale2: float | None = None, out=None):
+        """(X1, X2) -> (scale (X1 + X2), scale2 (X1 - X2)) of a (k x 2 rows) storage block into out
+        (default: in place; same strides), bse_rs_fold."""
+        out = v if out is None else out
+        self.ctx.call("bse_rs_fold", v.data_ptr(), out.data_ptr(), v.stride(0), rows, v.shape[0], scale,
+                      scale if scale2 is None else scale2)
 
     # ---- complex64 filter (tcgen05, c64.cuh): plane sets of 8 fp32 planes ----------------------
     @staticmethod
@@ -694,7 +697,15 @@ class DistSolver:
         n, nr = 2 * self.g.m, self.g.nr
         st = _Steps("rr", self.g.rank)
         t_row = row_buf[:k]
-        self.forward(q_col, t_row, low_sign=-1.0, filter=True)  # T = S H Q (rows R_I), filter kernel
+        if hasattr(self.ops, "ctx") and self.fwd.g is not None:
+            # T = S H Q on the real-split planes: fold Q, tile product + row allreduce, unfold with the S-flip
+            q_f = self.torch.empty_like(q_col)
+            self.ops.rs_fold(q_col, self.g.nc, 1.0, out=q_f)
+            self.forward(q_f, t_row, filter=True, rs=True)
+            self.ops.rs_fold(t_row, nr, 0.5, -0.5)
+            del q_f
+        else:
+            self.forward(q_col, t_row, low_sign=-1.0, filter=True)  # T = S H Q (rows R_I), filter kernel
         st.mark("T = S H Q", k)
         q_full = self.assemble_from_col(q_col)
         st.mark("allgather Q", k)
