@@ -375,8 +375,8 @@ def run_ours(args, world, rank, local):
     peak, peak_src = fp64_peak()
     achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
     algo = _lib.filter_algorithm() if _lib.filter_precision() == "c128" else "c64-3xtf32-tcgen05"
-    if algo.startswith("rs") and (world > 1 or ham.flags & 1):
-        algo = "3m"  # the 2D-grid tiles and B = 0 run the 3M kernel (the real-split planes are single-GPU, B != 0)
+    if algo.startswith("rs") and (ham.flags & 1 or (world > 1 and ds.fwd.g is None)):
+        algo = "3m"  # B = 0 (or tiles without room for the planes) runs the 3M kernel
     exec_ratio = 0.75 if algo.startswith("3m") else 1.0  # 3M: 6 real DMMA per complex block pair instead of 8
     if algo.startswith("rs"):
         exec_ratio = 0.5  # real split: 4 n^2 k DMMA flops per step (csrc/hop_rs.cuh)
