@@ -122,7 +122,7 @@ _STATUS = {
 _lib = None
 _lock = threading.Lock()
 # Chebyshev-filter product kernels (bse_set_filter_algorithm codes)
-_ALGOS = {"4m": 4, "3m": 88, "rs": 90, "rs-wide": 91, "rs-tall": 92, "rs-quad": 93, "rs-narrow": 94,
+_ALGOS = {"4m": 4, "3m": 88, "rs": 90, "rs-wide": 91, "rs-tall": 92, "rs-quad": 93, "rs-narrow": 94, "rs-tall-k32": 95, "rs-tall-deep": 96,
           "3m-tma-narrow": 82, "3m-tma-wide": 86, "3m-mbcp": 72, "3m-sync": 65,
           "3m-onthefly": 3}
 # BSE200_FILTER=3m / 4m select the Gauss 3M / plain 4M complex splits for every product;
@@ -170,8 +170,8 @@ def uses_sum_planes() -> bool:
 
 
 def uses_rs_planes() -> bool:
-    """real-split filter (codes 90-94, csrc/hop_rs.cuh); the other products run the 3M kernel (88)"""
-    return 90 <= _FILTER_CM <= 94
+    """real-split filter (codes 90-96, csrc/hop_rs.cuh); the other products run the 3M kernel (88)"""
+    return 90 <= _FILTER_CM <= 96
 
 
 def load() -> C.CDLL:

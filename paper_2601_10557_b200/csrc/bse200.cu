@@ -313,7 +313,7 @@ using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 // 90: the real-split filter (hop_rs.cuh) for bse_chebyshev_filter_rs; every other product
 // (RR's S H Q, the distributed tiles) runs code 88 under it
 bool filter_code_needs_planes(int code) {
-  return code == 65 || code == 72 || code == 82 || code == 86 || code == 88 || (code >= 90 && code <= 94);
+  return code == 65 || code == 72 || code == 82 || code == 86 || code == 88 || (code >= 90 && code <= 96);
 }
 bool filter_code_valid(int code) { return code == 3 || code == 4 || filter_code_needs_planes(code); }
 
@@ -358,6 +358,10 @@ using RsWide = bse::RsCfg<128, 64, 16, 4, 4, 4, 1>;
 using RsTall = bse::RsCfg<128, 32, 16, 4, 2, 6, 1>;
 using RsQuad = bse::RsCfg<64, 64, 16, 4, 4, 6, 1>;
 using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
+//   95  128 x 32 with BK = 32, 4 stages (half the mbarrier round trips per K)
+//   96  128 x 32 with BK = 16, 8 stages
+using RsTallK32 = bse::RsCfg<128, 32, 32, 4, 2, 4, 1>;
+using RsTallDeep = bse::RsCfg<128, 32, 16, 4, 2, 8, 1>;
 
 template <class C>
 void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
@@ -384,6 +388,8 @@ void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ld
     case 92: launch_rs<RsTall>(ctx, a, g, ldg); break;
     case 93: launch_rs<RsQuad>(ctx, a, g, ldg); break;
     case 94: launch_rs<RsNarrow>(ctx, a, g, ldg); break;
+    case 95: launch_rs<RsTallK32>(ctx, a, g, ldg); break;
+    case 96: launch_rs<RsTallDeep>(ctx, a, g, ldg); break;
     default:
       if (a.k >= 512)
         launch_rs<RsTall>(ctx, a, g, ldg);
@@ -1004,7 +1010,7 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     if (!filter_code_valid(complex_mults))
-      throw BseError(BSE_EVALIDATION, "filter algorithm must be 3, 4, 65, 72, 82, 86, 88 or 90-94 (include/bse200.h)");
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 3, 4, 65, 72, 82, 86, 88 or 90-96 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }

@@ -405,7 +405,7 @@ def test_filter_rs_matches_3m_and_tiles_bitwise(bse):
             ctx.call("bse_chebyshev_filter", _lib.dptr(ab), _lib.dptr(sd), ld_of(ab), m, _lib.dptr(ref), 2 * m, k, 4,
                      0.5, 2.0, -3.0, _lib.dptr(work))
             outs = {}
-            for algo in ("rs", "rs-wide", "rs-tall", "rs-quad", "rs-narrow"):
+            for algo in ("rs", "rs-wide", "rs-tall", "rs-quad", "rs-narrow", "rs-tall-k32", "rs-tall-deep"):
                 bse.set_filter_algorithm(algo)
                 v = v0.clone()
                 ctx.call("bse_chebyshev_filter_rs", _lib.dptr(gp), ldg, m, _lib.dptr(v), 2 * m, k, 4, 0.5, 2.0, -3.0,
