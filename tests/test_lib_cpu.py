@@ -40,6 +40,13 @@ def test_sass_has_dmma_and_no_cpu_path():
     assert "UTCHMMA" in sass  # tcgen05.mma (complex64 filter)
     assert "SYNCS" in sass  # mbarrier pipelines
 
+    # the default filter kernel (real-split planes): DMMA fed by TMA through mbarrier rings
+    bodies = [f for f in sass.split("Function : ") if f.startswith("_ZN3bse17hop_rs_tma_kernel")]
+    assert bodies
+    for body in bodies:
+        for op in ("DMMA.8x8x4", "UTMALDG", "SYNCS"):
+            assert op in body, op
+
 
 def test_rng_bit_exact_vs_reference_fixture():
     from paper_2601_10557_b200 import rng
