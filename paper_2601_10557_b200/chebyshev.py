@@ -54,10 +54,8 @@ def filter_inplace(ham: BseHamiltonian, v, cfg: FilterConfig, work=None, ledger:
     ab = ham.device_blocks(v.device)
     ctx = _lib.Context.get(v.device.index)
     if _lib.uses_rs_planes():
-        # real-split filter: 4 n^2 k executed flops per step (csrc/hop_rs.cuh); the RR's S H Q keeps the
-        # 3M kernel, so the sum planes are built first and the RS planes only where both fit
-        if _lib.uses_sum_planes():
-            ham.device_sum_planes(v.device, reserve=2 * 16 * ld_of(v) * k)
+        # real-split filter: 4 n^2 k executed flops per step (csrc/hop_rs.cuh); the RR products run on
+        # the same planes, so the 3M sum planes are only built when these are unavailable (B = 0, HBM)
         g = ham.device_rs_planes(v.device, reserve=2 * 16 * ld_of(v) * k)
         if g is not None:
             ctx.call("bse_chebyshev_filter_rs", _lib.dptr(g), g.stride(1), ham.m, _lib.dptr(v), ld_of(v), k,

@@ -1028,19 +1028,18 @@ class DistributedSolver:
     def solve(self, cfg: SolverConfig) -> SolveResult:
         if hasattr(self.ops, "ctx"):
             self.ops.ctx.set_ham_flags(self.flags)
-        if _lib.uses_sum_planes():
-            g = self.inner.g
-            # vectors of the solve: col / row blocks, locked block, the RR's T and products (~6 blocks)
-            reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
-            for t in (self.fwd, self.trn):
-                if t.sd is None:
-                    add_sum_planes(self.ops, t, reserve)
+        g = self.inner.g
+        # vectors of the solve: col / row blocks, locked block, the RR's T and products (~6 blocks)
+        reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
         if _lib.uses_rs_planes() and not self.flags & 1:
-            g = self.inner.g
-            reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
+            # real-split planes for the filter and the RR's T = S H Q (csrc/hop_rs.cuh)
             for t in (self.fwd, self.trn):
                 if t.g is None:
                     add_rs_planes(self.ops, t, reserve)
+        if _lib.uses_sum_planes() and (self.fwd.g is None or self.trn.g is None):
+            for t in (self.fwd, self.trn):
+                if t.sd is None:
+                    add_sum_planes(self.ops, t, reserve)
         res = self.inner.solve(cfg)
         res.v = res.v.T  # (n, nev) column-major view
         return res

@@ -60,14 +60,14 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     vout = colmajor_empty(n, k, q.device)
     lmm = ctypes.c_double(float("nan"))
     ab = ham.device_blocks(q.device)
-    # the T = (S) H Q product runs on the filter's kernel (3M) when the sum planes are in use
-    sdt = ham.device_sum_planes(q.device, reserve=2 * 16 * n * k) if _lib.uses_sum_planes() else None
+    # the T = (S) H Q product runs on the real-split planes (csrc/hop_rs.cuh, registered for this call
+    # only) when they are in use, else on the filter's 3M kernel when the sum planes are
+    g = ham.device_rs_planes(q.device, reserve=3 * 16 * n * k) if _lib.uses_rs_planes() else None
+    sdt = ham.device_sum_planes(q.device, reserve=2 * 16 * n * k) if _lib.uses_sum_planes() and g is None else None
     sd = _lib.dptr(sdt) if sdt is not None else None
     ctx = _lib.Context.get(q.device.index)
     res = np.zeros(k) if fused_residuals else None
     extra = (_lib.hptr(res) if fused_residuals else None,) if entry == "bse_rr_hermitian" else ()
-    # the real-split planes (csrc/hop_rs.cuh), registered for this call only
-    g = ham.device_rs_planes(q.device, reserve=3 * 16 * n * k) if _lib.uses_rs_planes() else None
     try:
         if g is not None:
             ctx.call("bse_set_rs_planes", _lib.dptr(ab), ham.m, _lib.dptr(g), g.stride(1))
