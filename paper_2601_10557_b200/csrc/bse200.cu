@@ -450,7 +450,7 @@ bse::HopArgs hop_args_single(const void* d_ab, int64_t lda, int64_t m, const zva
   bse::HopArgs a{};
   const zval* ab = static_cast<const zval*>(d_ab);
   a.pa = ab;
-  a.pb = ab + m * lda;
+  a.pb = ab ? ab + m * lda : nullptr;  // null for the real-split products (planes passed separately)
   a.lda = lda;
   a.mr = (int)m;
   a.kc = (int)m;
