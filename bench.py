@@ -181,39 +181,7 @@ def max_over_ranks(x: float, world: int) -> float:
 
 
 # ----------------------------------------------------------------------------- CPU arms
-_BLOCKS = {}
-
-
-def cpu_sample(m: int, k_sample: int, ham=None) -> dict:
-    """Time the oracle's H-application (the reference's 86 %-of-wall kernel, 4 zgemm) on
-    k_sample columns at the full m, on the host cores (OpenBLAS threads = all)."""
-    from oracle import bse_oracle as o
-
-    if ham is not None:
-        a, b = ham.host_blocks()
-    else:  # reference arm without a GPU-built input: same-shaped blocks (zgemm time is data independent)
-        if m not in _BLOCKS:
-            z = o.gauss_c(12345, m * m)
-            a = np.asfortranarray(z.reshape(m, m))
-            _BLOCKS[m] = (a, a)
-        a, b = _BLOCKS[m]
-    x = o.gauss_c_matrix(o.child_seed(0, 3), 2 * m, k_sample)
-    o.h_times(a[:64, :64], b[:64, :64], x[:128, :2])  # warm BLAS
-    t0 = time.perf_counter()
-    o.h_times(a, b, x)
-    dt = time.perf_counter() - t0
-    flops = 8.0 * (2 * m) ** 2 * k_sample
-    return {"seconds": dt, "flops": flops, "gflops": flops / dt / 1e9}
-
-
-def expected_solve_flops(cfg_name: str, nevex: int, m: int, deg: int) -> tuple[float, str]:
-    p = Path(str(TRACE_FILE).format(cfg=cfg_name))
-    if p.exists():
-        d = json.loads(p.read_text())
-        return float(d["total_model_flops"]), f"modeled flops of our {cfg_name} solve trace ({p.name})"
-    n = 2 * m
-    sum_k = 6.9 * nevex  # measured Sigma k / nevex at the C2 shape (SURVEY §6.4)
-    return (deg + 2) * 8.0 * n * n * sum_k, "model (deg+2) 8 n^2 Sigma k, Sigma k = 6.9 nevex (SURVEY 6.4)"
+CACHE = ROOT / ".bench_cache"
 
 
 def cores() -> int:
@@ -223,30 +191,95 @@ def cores() -> int:
         return os.cpu_count() or 1
 
 
+def solve_trace(cfg_name: str):
+    from oracle import cpu_model
+
+    return cpu_model.reference_trace(ROOT / "tests" / "golden" / f"large_{cfg_name}.npz",
+                                     Path(str(TRACE_FILE).format(cfg=cfg_name)))
+
+
+def cpu_reference_time(cfg_name: str, blocks=None, quick: bool = False, samples: int = 0):
+    """Reference CPU time-to-solution from timed reference-path phases (oracle/cpu_model.py):
+    every phase of the reference code path timed once at the full n on this host's cores, the
+    solve's per-iteration (k, l) applied to those timings; ``samples`` further per-step samples
+    of the H application rescale the filter rate (median reported).  ``quick`` (our arm's
+    cpu_baseline leg, ~30 s): narrower calibration widths unless the reference arm cached a full
+    calibration on this host."""
+    from oracle import cpu_model
+
+    m, nev, nex, deg, tol, rel = CONFIGS[cfg_name]
+    nevex = nev + nex
+    tr = solve_trace(cfg_name)
+    if tr is None:
+        return None
+    tk, tl, lsteps, tsrc = tr
+    host = f"{cores()}c"
+    cache = CACHE / f"cpu_calibration_{cfg_name}_{host}.json"
+    cal = None
+    if quick and cache.exists():
+        cal = json.loads(cache.read_text())
+    t0 = time.perf_counter()
+    if blocks is None:
+        blocks = cpu_model.timing_instance(m)
+    a, b = blocks
+    if cal is None:
+        k_hi, k_lo, l_hi = (min(nevex, 512), 64, min(nev, 256)) if quick else (nevex, max(min(tk), 32), nev)
+        cal = cpu_model.calibrate(a, b, k_hi, k_lo, l_hi)
+        cal["sample_k"] = 64
+        cal["sample_s"] = cpu_model.sample_step(a, b, 64)
+        cal["quick"] = quick
+        if not quick:
+            CACHE.mkdir(exist_ok=True)
+            cache.write_text(json.dumps(cal, indent=1) + "\n")
+        cal["source"] = "timed here"
+    else:
+        cal["source"] = f"timed by this host's --impl reference run ({cache.name})"
+    vals = []
+    for _ in range(samples):
+        sc = cpu_model.sample_step(a, b, cal["sample_k"]) / cal["sample_s"]
+        vals.append(cpu_model.model(cal, tk, tl, deg, lsteps, step_scale=sc, nevex=nevex))
+    base = cpu_model.model(cal, tk, tl, deg, lsteps, nevex=nevex)
+    tot = [v["total"] for v in vals] or [base["total"]]
+    return {"value": statistics.median(tot), "phases": {k: round(v, 2) for k, v in base.items()},
+            "per_step": [round(x, 2) for x in tot], "calibration": cal, "trace_source": tsrc,
+            "wall_s": time.perf_counter() - t0,
+            "sample": (f"reference code path (oracle restatement: numpy temporaries + OpenBLAS/LAPACK, "
+                       f"{cores()} threads) timed phase by phase at n={2 * m}: filter step at k={cal['k_lo']} "
+                       f"and {cal['k_hi']}, Householder QR of S Y_locked at l={cal['l_hi']}, CholQR2 and "
+                       f"hermitian RR at both k, residuals, Lanczos step ({cal['source']}); evaluated over "
+                       f"the {len(tk)} iterations of the {tsrc}")}
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    m, nev, nex, deg, tol, rel = CONFIGS[args.config]
-    nevex = nev + nex
-    k_sample = 16 if m >= 10000 else 64
-    total, how = expected_solve_flops(args.config, nevex, m, deg)
-    times = []
-    for i in range(args.warmup + args.steps):
-        s = cpu_sample(m, k_sample)
-        if i >= args.warmup:
-            times.append(total / (s["flops"] / s["seconds"]))
-    val = statistics.median(times)
+    r = cpu_reference_time(args.config, samples=args.warmup + args.steps)
+    val = statistics.median(r["per_step"][args.warmup:]) if r is not None else None
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": val * 1e3 if val else None, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)", "data": "synthetic",
         "config": config_dict(args.config),
         "cpu_baseline": {"value": val, "unit": "s", "cores": cores(), "kind": "port",
-                         "sample": f"oracle H-application (4 OpenBLAS zgemm) at m={m} on {k_sample} columns per step, "
-                                   f"extrapolated to the solve's total modeled flops ({how})"},
+                         "sample": r["sample"] if r else "no solve trace"},
+        "cpu_phases_s": r["phases"] if r else None,
+        "cpu_calibration": r["calibration"] if r else None,
+        "cpu_model_check": model_check_summary(),
         "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def model_check_summary():
+    """The CPU model against measured full solves (profiles/r02/cpu_model_check_*.json)."""
+    out = {}
+    for p in sorted((ROOT / "profiles" / "r02").glob("cpu_model_check_*.json")):
+        try:
+            d = json.loads(p.read_text())
+            out[p.stem] = {k: d.get(k) for k in ("measured_s", "model_s", "ratio", "cores", "where")}
+        except Exception:
+            pass
+    return out or None
 
 
 def config_dict(name):
@@ -306,9 +339,10 @@ def run_ours(args, world, rank, local):
             sel = [e for e in events if e[3] == "c128"] or events
             return sum(a.elapsed_time(b) for a, b, _, _ in sel), sum(f for _, _, f, _ in sel)
     else:
-        from paper_2601_10557_b200.dist import DistributedSolver
+        from paper_2601_10557_b200.dist import DistributedSolver, tile_blocks_host
 
         ds = DistributedSolver(ham, device=dev)
+        pieces = None if args.no_e2e else tile_blocks_host(ds.grid, ham)  # this rank's tile, for the e2e leg
         ham.release_device()
         ham._dev.clear()
         torch.cuda.empty_cache()
@@ -351,10 +385,9 @@ def run_ours(args, world, rank, local):
         host_ham = BseHamiltonian(a_h, b_h, Definiteness.DEFINITE)  # definiteness certified by the generator
         h2d = 2 * m * m * 16 + n * cfg.nevex * 16 + 8 * n * 16
     else:
-        pieces = ds.tile_pieces_host()
-        for name in ("fwd", "trn"):  # user inputs staged in pinned host memory
-            pieces[name] = tuple(pinned_fortran(x) for x in pieces[name])
-        h2d = world * sum(x.nbytes for name in ("fwd", "trn") for x in pieces[name]) + world * (n // world) * cfg.nevex * 16
+        pieces["fwd"] = tuple(pinned_fortran(x) for x in pieces["fwd"])  # user inputs staged in pinned memory
+        # every rank uploads its own tile of A and B (bytes summed over ranks) and its start-block rows
+        h2d = world * sum(x.nbytes for x in pieces["fwd"]) + world * 2 * ds.grid.nc * cfg.nevex * 16
     if not args.no_e2e:
         barrier(world)
         torch.cuda.synchronize()
@@ -373,9 +406,9 @@ def run_ours(args, world, rank, local):
             host_ham.release_device()
 
     peak, peak_src = fp64_peak()
-    achieved = ffl / (fms / 1e3) / 1e12 if fms > 0 else None
+    model_rate = ffl / (fms / 1e3) / 1e12 if fms > 0 else None  # reference model flops (8 n^2 k per step)
     algo = _lib.filter_algorithm() if _lib.filter_precision() == "c128" else "c64-3xtf32-tcgen05"
-    if algo.startswith("rs") and (ham.flags & 1 or (world > 1 and ds.fwd.g is None)):
+    if algo.startswith("rs") and (ham.flags & 1 or (world > 1 and not ds.planes)):
         algo = "3m"  # B = 0 (or tiles without room for the planes) runs the 3M kernel
     exec_ratio = 0.75 if algo.startswith("3m") else 1.0  # 3M: 6 real DMMA per complex block pair instead of 8
     if algo.startswith("rs"):
@@ -384,30 +417,35 @@ def run_ours(args, world, rank, local):
         peak, peak_src = 1177.7, ("dense tf32 tcgen05 peak as ncu reports it at 1965 MHz (sm__ops_path_tensor_op_utchmma_"
                                   "src_tf32 peak); measured probe GEMMs: 433 TF/s (1 CTA), 663 TF/s (CTA pair)")
         exec_ratio = 3.0  # 3 TF32 MMAs per real product
-    if ham.flags & 1 and achieved:  # B = 0: the B half is skipped, count 4 n^2 k
-        achieved *= 0.5
+    if ham.flags & 1 and model_rate:  # B = 0: the B half is skipped, count 4 n^2 k
+        model_rate *= 0.5
+    achieved = model_rate * exec_ratio if model_rate else None  # flops the tensor pipe executes
     total_model = res.ledger.total_flops()
     if rank == 0 and args.config != "c1" and world == 1:
         TRACE_FILE.parent.mkdir(exist_ok=True)
         Path(str(TRACE_FILE).format(cfg=args.config)).write_text(json.dumps({
             "total_model_flops": total_model, "iterations": res.iterations_used, "converged": res.converged,
+            "lanczos_steps": res.bounds.steps,
             "trace": [[t.it, t.locked, t.k, t.max_res, t.mu_nevex, t.flops] for t in res.trace],
             "ledger_seconds": res.ledger.seconds, "ledger_flops": res.ledger.flops}, indent=1) + "\n")
 
+    parity = parity_vs_reference(args.config, res) if rank == 0 else None
+    defin = None
+    if rank == 0 and world == 1 and not args.no_e2e and m <= 20000:
+        defin = time_is_definite(ham, dev)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        k_sample = 16 if m >= 10000 else 64
-        s = cpu_sample(m, k_sample, ham)
-        cpu = {"value": total_model / (s["flops"] / s["seconds"]), "unit": "s", "cores": cores(), "kind": "port",
-               "sample": f"oracle H-application (4 OpenBLAS zgemm, {s['gflops']:.0f} GF/s) at m={m} on {k_sample} "
-                         f"columns, extrapolated to this solve's {total_model:.3e} modeled flops"}
+        r = cpu_reference_time(args.config, blocks=ham.host_blocks(), quick=True)
+        if r is not None:
+            cpu = {"value": r["value"], "unit": "s", "cores": cores(), "kind": "port", "sample": r["sample"],
+                   "phases_s": r["phases"]}
     if rank == 0:
         cfgd = config_dict(args.config)
         if world > 1:
             from paper_2601_10557_b200.dist import grid_shape
 
             p, q = grid_shape(world)
-            cfgd["parallelism"] = f"2D block grid {p}x{q} (A/B tiles + block transposes per GPU), NCCL row/col allreduce"
+            cfgd["parallelism"] = f"2D block grid {p}x{q} (one A/B tile per GPU), NCCL row/col allreduce"
         line = {
             "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong",
@@ -424,14 +462,14 @@ def run_ours(args, world, rank, local):
                                     "bse::hop_rs_tma_kernel (real-split H operator: folded block, four real planes, 4 n^2 k DMMA flops per step, TMA-fed by a producer warp, Chebyshev epilogue)"
                                     if algo.startswith("rs") else "bse::hop_kernel (fused H-operator DMMA GEMM + Chebyshev epilogue)"),
                          "peak_source": peak_src,
-                         "algorithmic": "8 n^2 k flops per filter step (bsesolve metrics model, BASELINE.md §3.5) "
-                                        "per GPU, summed over the solve's filter calls / CUDA-event (1 GPU) or "
-                                        "synchronised (N GPUs) time of those calls; with the 3M filter the DMMA pipe "
-                                        "executes 6 n^2 k, with the real-split filter 4 n^2 k (filter_executed_*)"},
-            "filter_tflops_per_gpu": achieved, "filter_frac_of_fp64_peak": (achieved / peak) if achieved else None,
+                         "algorithmic": ("EXECUTED tensor-pipe flops per filter step: 4 n^2 k with the real-split "
+                                         "kernel (6 n^2 k 3M, 8 n^2 k 4M; DESIGN.md §Roofline), summed over the "
+                                         "solve's filter calls / their CUDA-event time on the launching stream "
+                                         "(1 GPU) or synchronised time (N GPUs)")},
+            "filter_tflops_model": model_rate,
+            "filter_model_note": "reference model 8 n^2 k flops per step (metrics.py:11-39) / filter time; exceeds "
+                                 "the FP64 peak because the real-split kernel executes half of it",
             "filter_algorithm": algo,
-            "filter_executed_tflops_per_gpu": achieved * exec_ratio if achieved else None,
-            "filter_executed_frac_of_fp64_peak": achieved * exec_ratio / peak if achieved else None,
             "solve": {"iterations": res.iterations_used, "converged": res.converged,
                       "ledger_seconds": {k: round(v, 4) for k, v in res.ledger.seconds.items()},
                       "model_tflop": total_model / 1e12, "generator_s": round(gen_s, 2),
@@ -442,11 +480,67 @@ def run_ours(args, world, rank, local):
                       "phase_events_s": [[ph, round(dt, 4)] for ph, dt in res.ledger.events],
                       "e2e_iterations": r_e2e.iterations_used,
                       "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},
+            "parity_vs_reference": parity,
+            "is_definite": defin,
             "clocks": clk.summary(),
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
+
+
+def parity_vs_reference(cfg_name, res):
+    """The solve against the REFERENCE's own result at this config (tests/golden/large_<cfg>.npz,
+    made by oracle/make_golden_large.py from bsesolve.solve on the reference instance)."""
+    p = ROOT / "tests" / "golden" / f"large_{cfg_name}.npz"
+    if cfg_name not in ("c2", "c3") or not p.exists():
+        return None
+    g = np.load(p, allow_pickle=False)
+    ref = g["lambdas"]
+    same_it = res.iterations_used == int(g["iterations_used"])
+    v = res.v if isinstance(res.v, np.ndarray) else None
+    out = {"golden": p.name, "max_dlambda_rel": float(np.max(np.abs(res.lambdas - ref) / np.abs(ref))),
+           "iterations": res.iterations_used, "iterations_ref": int(g["iterations_used"]),
+           "trace_locked_equal": same_it and [t.locked for t in res.trace] == [int(x) for x in g["trace_locked"]],
+           "trace_k_equal": same_it and [t.k for t in res.trace] == [int(x) for x in g["trace_k"]],
+           "max_residual_over_tol": float(res.residual_norms.max() / (float(g["tol"]) * abs(res.bounds.mu_1))),
+           "mu_1_rel": float(abs(res.bounds.mu_1 - float(g["mu_1"])) / abs(float(g["mu_1"]))),
+           "reference_solve_s": float(g["solve_seconds"]),
+           "reference_host": json.loads(str(g["host_json"]))}
+    if v is None:
+        v = res.v[:, :4].T.contiguous().cpu().numpy().T
+        v2 = res.v[:, -4:].T.contiguous().cpu().numpy().T
+    else:
+        v, v2 = v[:, :4], v[:, -4:]
+    ov = np.concatenate([np.abs(np.einsum("ij,ij->j", g["v_first4"].conj(), v)),
+                         np.abs(np.einsum("ij,ij->j", g["v_last4"].conj(), v2))])
+    out["ritz_vector_overlap_min"] = float(ov.min())
+    out["pass"] = bool(out["max_dlambda_rel"] <= 1e-10 and abs(out["iterations"] - out["iterations_ref"]) <= 1
+                       and out["max_residual_over_tol"] <= 1.0 and out["ritz_vector_overlap_min"] >= 1 - 1e-8)
+    return out
+
+
+def time_is_definite(ham, dev):
+    """The definiteness check a host-supplied input pays (solver.py:128 -> hamiltonian.py:208-218):
+    upload of A, B plus the device Cholesky of the n x n S H, timed on its own (the generated input
+    skips it as the reference's generate() does, generate.py:77)."""
+    import torch
+
+    import paper_2601_10557_b200 as bse
+    from paper_2601_10557_b200.hamiltonian import BseHamiltonian
+
+    a_h, b_h = (pinned_fortran(x) for x in ham.host_blocks())
+    h = BseHamiltonian(a_h, b_h)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.device(dev):
+        out = bse.is_definite(h)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    h.release_device()
+    return {"seconds": round(dt, 3), "outcome": out.name,
+            "what": "H2D of A, B + device Cholesky of S H (16 n^2 bytes) -- not in value/e2e, like the "
+                    "reference's generate()-cached check"}
 
 
 def main():

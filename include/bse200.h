@@ -189,6 +189,12 @@ int bse_hop_tile(bse_ctx* ctx, const bse_hop_tile_args* args);
  * not read.  The 2D-grid filter folds its block once (bse_rs_fold), runs deg such products with
  * the same reductions as bse_hop_tile, and unfolds.                                            */
 int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* args, const void* d_g, int64_t ldg);
+/* The TRANSPOSED tile product on the same planes d_g: d_g holds the planes of a tile T (kc x mr
+ * real, leading dim ldg >= kc, even) and the product is that of the block transpose
+ * [A_T^H | B_T^T] (mr output rows = T's columns, contraction kc = T's rows), the row -> col step
+ * of the 2D grid (the same local block, conjugate-transposed), so a grid GPU
+ * stores one tile's planes.  Arguments and epilogue as bse_hop_tile_rs.                        */
+int bse_hop_tile_rs_t(bse_ctx* ctx, const bse_hop_tile_args* args, const void* d_g, int64_t ldg);
 /* (X1, X2) -> (scale (X1 + X2), scale2 (X1 - X2)) for a block of 2 rows x k (ld >= 2 rows; X1 rows
  * [0, rows), X2 rows [rows, 2 rows)); (1, 1) folds, (1/2, 1/2) unfolds, (1/2, -1/2) unfolds with
  * the S-flip; d_dst may equal d_src.                                                           */

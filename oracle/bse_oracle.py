@@ -83,6 +83,17 @@ def h_times(a: np.ndarray, b: np.ndarray, x: np.ndarray) -> np.ndarray:
     return np.concatenate([top, bot], axis=0)
 
 
+def h_times_adjoint(a: np.ndarray, b: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """hamiltonian.py:154-176: H x computed as S (H* (S x)) -- the form the
+    reference's filter uses on odd steps (chebyshev.py:62-65).  Same bits as
+    h_times on one device up to roundoff; kept for timing fidelity."""
+    m = a.shape[0]
+    y1, y2 = x[:m], -x[m:]
+    up = a @ y1 - b @ y2
+    low = np.conj(b @ np.conj(y1) - a @ np.conj(y2))
+    return np.concatenate([up, -low], axis=0)
+
+
 def s_flip(x: np.ndarray) -> np.ndarray:
     """hamiltonian.py:104-111."""
     y = np.array(x, dtype=np.complex128, copy=True)
@@ -385,16 +396,30 @@ class OracleResult:
 
 
 def oracle_solve(a, b, nev, nex=None, deg=20, tol=1e-8, maxiter=25, rr_variant="auto",
-                 seed=0, lanczos_steps=24, rel_res=False):
+                 seed=0, lanczos_steps=24, rel_res=False, seconds=None):
     """solver.py:125-250 outer loop (trace rows: it, locked, k, max_res,
-    min_res_unlocked, mu_nevex, variant, lambda_min_m, flops)."""
+    min_res_unlocked, mu_nevex, variant, lambda_min_m, flops).  ``seconds``
+    (a dict) receives per-phase wall seconds like the reference's PhaseLedger
+    (metrics.py:11-39, solver.py:157-184)."""
+    import time as _time
+
+    sec = seconds if seconds is not None else {}
+    clock = [_time.perf_counter()]
+
+    def lap(phase):
+        now = _time.perf_counter()
+        sec[phase] = sec.get(phase, 0.0) + now - clock[0]
+        clock[0] = now
+
     m = a.shape[0]
     n = 2 * m
     nevex = nev + (nev if nex is None else nex)
     fl = {p: [0.0] for p in ("lanczos", "filter", "ortho", "rr", "residuals")}
     bnd = lanczos_bounds(a, b, nevex, lanczos_steps, child_seed(seed, 2), fl["lanczos"])
+    lap("lanczos")
     normalizer = abs(bnd.mu_1) if rel_res else 1.0
     vhat = gauss_c_matrix(child_seed(seed, 3), n, nevex)
+    lap("start")
     lk_vals, lk_res = [], []
     lk_y = np.zeros((n, 0), dtype=np.complex128)
     trace, backups, done, it_used = [], 0, False, 0
@@ -406,7 +431,9 @@ def oracle_solve(a, b, nev, nex=None, deg=20, tol=1e-8, maxiter=25, rr_variant="
         k = nevex - len(lk_vals)
         c, e = (bnd.mu_n + cur_cut) / 2.0, (bnd.mu_n - cur_cut) / 2.0
         vhat = cheb_filter(a, b, vhat, deg, c, e, bnd.mu_1, fl["filter"])
+        lap("filter")
         q_act, _ = s_ortho(vhat, lk_y, fl["ortho"])
+        lap("ortho")
         variant = "hermitian"
         if rr_variant == "backup":
             variant = "backup"
@@ -420,7 +447,9 @@ def oracle_solve(a, b, nev, nex=None, deg=20, tol=1e-8, maxiter=25, rr_variant="
                 variant = "backup"
                 backups += 1
                 lam, vec, lmm = rr_backup(a, b, q_act, fl["rr"])
+        lap("rr")
         res = residual_norms(a, b, lam, vec)
+        lap("residuals")
         fl["residuals"][0] += 8.0 * n * n * vec.shape[1]
         cnt, ok = converged_prefix(res, tol, nev - len(lk_vals), normalizer)
         if cnt:

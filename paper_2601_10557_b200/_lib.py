@@ -82,6 +82,7 @@ _SIGS = {
     "bse_is_definite": (C.c_int, [_vp, _vp, _i64, _i64, _ip]),
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
     "bse_hop_tile_rs": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
+    "bse_hop_tile_rs_t": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
     "bse_rs_fold": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _dbl, _dbl]),
     "bse_c64_tile_planes": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_c64_tile_step": (C.c_int, [_vp, C.POINTER(C64TileArgs)]),
@@ -122,22 +123,19 @@ _STATUS = {
 _lib = None
 _lock = threading.Lock()
 # Chebyshev-filter product kernels (bse_set_filter_algorithm codes)
-_ALGOS = {"4m": 4, "3m": 88, "rs": 90, "rs-wide": 91, "rs-tall": 92, "rs-quad": 93, "rs-narrow": 94, "rs-tall-k32": 95, "rs-tall-deep": 96,
-          "3m-tma-narrow": 82, "3m-tma-wide": 86, "3m-mbcp": 72, "3m-sync": 65,
-          "3m-onthefly": 3}
-# BSE200_FILTER=3m / 4m select the Gauss 3M / plain 4M complex splits for every product;
-# default "rs": the real-split filter (csrc/hop_rs.cuh, 4 n^2 k executed flops per step) for
-# single-GPU filters with B != 0; every other product (RR, 2D-grid tiles, B = 0) runs "3m"
+_ALGOS = {"4m": 4, "3m": 88, "3m-tma-narrow": 82, "3m-tma-wide": 86, "rs": 90, "rs-tall": 92, "rs-narrow": 94}
+# BSE200_FILTER=3m / 4m select the Gauss 3M / plain 4M complex splits for the filter;
+# default "rs": the real-split filter (csrc/hop_rs.cuh, 4 n^2 k executed flops per step) for every
+# filter product with B != 0 (single GPU and both directions of the 2D grid) and the RR's
+# T = S H Q; B = 0 runs "3m" with the B half skipped
 _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "rs").lower()]
 
 
 def set_filter_algorithm(name: str) -> None:
-    """'rs' (default: the single-GPU filter on the real-split planes of csrc/hop_rs.cuh, half the FP64
-    tensor ops of 4M, +32 m^2 bytes; fixed tiles 'rs-wide' / 'rs-tall' / 'rs-quad' / 'rs-narrow', all
-    bitwise identical; every other product runs '3m'), '3m' (Gauss split, 25% fewer FP64 tensor ops,
-    the operand sums of A and B precomputed once (+32 m^2 bytes), TMA-fed producer-warp kernel), its fixed tiles '3m-tma-narrow' /
-    '3m-tma-wide', the earlier pipelines '3m-mbcp' / '3m-sync' (all bitwise identical),
-    '3m-onthefly' (sums formed in registers) or '4m'."""
+    """'rs' (default: the real-split planes of csrc/hop_rs.cuh, half the FP64 tensor ops of 4M;
+    fixed tiles 'rs-tall' / 'rs-narrow', bitwise identical), '3m' (Gauss split, 25% fewer FP64
+    tensor ops than 4M, operand sums precomputed once, TMA-fed producer-warp kernel; fixed tiles
+    '3m-tma-narrow' / '3m-tma-wide', bitwise identical) or '4m'."""
     global _FILTER_CM
     cm = _ALGOS[name.lower()] if isinstance(name, str) else int(name)
     _FILTER_CM = cm
@@ -166,12 +164,12 @@ def filter_precision() -> str:
 
 
 def uses_sum_planes() -> bool:
-    return _FILTER_CM in (65, 72, 82, 86, 88) or uses_rs_planes()
+    return _FILTER_CM in (82, 86, 88) or uses_rs_planes()
 
 
 def uses_rs_planes() -> bool:
-    """real-split filter (codes 90-96, csrc/hop_rs.cuh); the other products run the 3M kernel (88)"""
-    return 90 <= _FILTER_CM <= 96
+    """real-split filter (codes 90, 92, 94; csrc/hop_rs.cuh); B = 0 products run the 3M kernel (88)"""
+    return _FILTER_CM in (90, 92, 94)
 
 
 def load() -> C.CDLL:

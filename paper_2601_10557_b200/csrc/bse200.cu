@@ -10,7 +10,9 @@
 #include <cstring>
 #include <cstdlib>
 #include <ctime>
+#include <mutex>
 #include <numeric>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -80,6 +82,17 @@ struct BseError : std::runtime_error {
     if (s_ != CUSOLVER_STATUS_SUCCESS)                                                                \
       throw BseError(BSE_ECUDA, "cuSOLVER status " + std::to_string(s_) + " at " #x);                 \
   } while (0)
+
+// cudaFuncSetAttribute applies per device (context): remember the (kernel, device) pairs already
+// raised, under a lock, so a second GPU driven from the same process gets its own call.
+void ensure_smem(bse_ctx* ctx, const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({fn, ctx->device})) return;
+  CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({fn, ctx->device});
+}
 
 void check_launch(bse_ctx* ctx) {
   ctx->launches++;
@@ -218,12 +231,7 @@ template <class C, int EPI, int CM = 4>
 void launch_hop(bse_ctx* ctx, const bse::HopArgs& a_in) {
   bse::HopArgs a = a_in;
   a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop_kernel<C, EPI, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)C::SMEM));
-    configured = true;
-  }
+  ensure_smem(ctx, (const void*)bse::hop_kernel<C, EPI, CM>, (int)C::SMEM);
   dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
   bse::hop_kernel<C, EPI, CM><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(a);
   check_launch(ctx);
@@ -260,11 +268,7 @@ void launch_hop_tma(bse_ctx* ctx, const bse::HopArgs& a_in) {
   bse::HopArgs a = a_in;
   a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
   constexpr size_t smem = bse::TmaLayout<C>::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  ensure_smem(ctx, (const void*)bse::hop3m_tma_kernel<C>, (int)smem);
   bse::HopMaps mp;
   const uint64_t pr = 2 * (uint64_t)a.mr, xr = 2 * (uint64_t)a.kc;
   const zval* pp[2] = {a.pa, a.pb};
@@ -280,30 +284,14 @@ void launch_hop_tma(bse_ctx* ctx, const bse::HopArgs& a_in) {
   check_launch(ctx);
 }
 
-template <class C>
-void launch_hop_mb(bse_ctx* ctx, const bse::HopArgs& a_in) {
-  bse::HopArgs a = a_in;
-  a.skip_b = (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0;
-  constexpr size_t smem = bse::MbLayout<C>::SMEM;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop3m_mb_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
-  dim3 grid((a.k + C::BN - 1) / C::BN, (a.mr + C::BM - 1) / C::BM);
-  bse::hop3m_mb_kernel<C><<<grid, C::THREADS, smem, ctx->stream>>>(a);
-  check_launch(ctx);
-}
 
 // Filter-product variants (bse_set_filter_algorithm codes; the sweeps that chose them are in
 // profiles/r01/tune_*.txt):
 //   88  default 3M: TMA-fed, producer warp, mbarrier rings (hop_mb.cuh); tile by block width
 //   82 / 86  its two tiles alone (64 x 16, 4 consumer warps, 2 CTAs/SM / 64 x 32, 8 warps, 6 stages)
-//   72  3M, cp.async feed with mbarrier rings (hop3m_mb_kernel), 64 x 16, 4 warps of 32 x 8
-//   65  3M, cp.async feed with one __syncthreads per stage (hop_kernel CM 6), 32 x 32
-//    3  3M with the operand sums formed in registers (no sum planes needed)
 //    4  4M (HopMain)
-using Hop3MSync = bse::HopCfg<32, 32, 8, 2, 2, 4, 3, 1>;
+// (round 1's dominated 3M feeds -- cp.async + mbarrier, cp.async + __syncthreads, sums in
+// registers through hop_kernel -- are retired; profiles/r01/tune_3m_*.txt keeps their numbers)
 using Hop3MNarrow = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 1>;
 using Hop3MWide = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 // the default's tiles without sum planes (HBM too short for them): operand sums formed in registers
@@ -312,16 +300,14 @@ using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 
 // 90: the real-split filter (hop_rs.cuh) for bse_chebyshev_filter_rs; every other product
 // (RR's S H Q, the distributed tiles) runs code 88 under it
-bool filter_code_needs_planes(int code) {
-  return code == 65 || code == 72 || code == 82 || code == 86 || code == 88 || (code >= 90 && code <= 96);
-}
-bool filter_code_valid(int code) { return code == 3 || code == 4 || filter_code_needs_planes(code); }
+bool filter_code_needs_planes(int code) { return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94; }
+bool filter_code_valid(int code) { return code == 4 || filter_code_needs_planes(code); }
 
 // Chebyshev-step products, as selected by bse_set_filter_algorithm
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm >= 90 ? 88 : ctx->filter_cm;
   if (filter_code_needs_planes(code) && (!a.sa || !a.sb))  // no P sum planes: sums in registers
-    code = code == 88 ? 98 : 3;
+    code = 98;
   switch (code) {
     case 98:  // the default's TMA kernel forming the operand sums in registers (same bits)
       if (a.k >= 512)
@@ -340,61 +326,51 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
       break;
     case 82: launch_hop_tma<Hop3MNarrow>(ctx, a); break;
     case 86: launch_hop_tma<Hop3MWide>(ctx, a); break;
-    case 72: launch_hop_mb<Hop3MNarrow>(ctx, a); break;
-    case 65: launch_hop<Hop3MSync, bse::HOP_AXPBY, 6>(ctx, a); break;
-    case 3: launch_hop<Hop3M, bse::HOP_AXPBY, 3>(ctx, a); break;
     default: launch_hop<HopMain, bse::HOP_AXPBY, 4>(ctx, a); break;
   }
 }
 
 // ---- real-split filter (hop_rs.cuh) ----
 // tiles (codes for bse_set_filter_algorithm; 90 picks 92 from 512 columns, else 94;
-// profiles/r01/tune_rs.txt: 223 / 60 / 24 ms per C3 step at k = 1200 / 300 / 100 vs 346 / 91 / 33 for 3M):
-//   91  128 x 64, 8 consumer warps of 32 x 32, 4 stages (9 warps: capped at 168 registers)
+// profiles/r01/tune_rs.txt: 223 / 60 / 24 ms per C3 step at k = 1200 / 300 / 100 vs 346 / 91 / 33 for 3M;
+// the dominated 128 x 64, 64 x 64, BK = 32 and 8-stage tiles of round 1 are retired):
 //   92  128 x 32, 8 consumer warps of 32 x 16, 6 stages
-//   93  64 x 64, 4 consumer warps of 32 x 32, 6 stages (5 warps: up to 255 registers)
 //   94  64 x 32, 8 consumer warps of 16 x 16, 5 stages, 2 CTAs / SM
-using RsWide = bse::RsCfg<128, 64, 16, 4, 4, 4, 1>;
 using RsTall = bse::RsCfg<128, 32, 16, 4, 2, 6, 1>;
-using RsQuad = bse::RsCfg<64, 64, 16, 4, 4, 6, 1>;
 using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
-//   95  128 x 32 with BK = 32, 4 stages (half the mbarrier round trips per K)
-//   96  128 x 32 with BK = 16, 8 stages
-using RsTallK32 = bse::RsCfg<128, 32, 32, 4, 2, 4, 1>;
-using RsTallDeep = bse::RsCfg<128, 32, 16, 4, 2, 8, 1>;
 
-template <class C>
+// TRANS: the transposed-tile product on the same planes (hop_rs.cuh header): a.mr output rows
+// = plane columns, a.kc contraction = plane rows; the planes are read through K-major boxes.
+template <class C, bool TRANS = false>
 void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::hop_rs_tma_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    configured = true;
-  }
+  constexpr size_t smem = C::template smem<TRANS>();
+  ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS>, (int)smem);
   bse::RsMaps mp;
-  for (int q = 0; q < 4; ++q)
-    mp.g[q] = map2d_f64(g + (int64_t)q * a.kc * ldg, a.mr, a.kc, ldg * 8, C::LDP, C::BK);
+  for (int q = 0; q < 4; ++q) {
+    if (TRANS)
+      mp.g[q] = map2d_f64(g + (int64_t)q * a.mr * ldg, a.kc, a.mr, ldg * 8, C::LDK, C::BM);
+    else
+      mp.g[q] = map2d_f64(g + (int64_t)q * a.kc * ldg, a.mr, a.kc, ldg * 8, C::LDP, C::BK);
+  }
   mp.x[0] = map2d_f64(a.x1, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
   mp.x[1] = map2d_f64(a.x2, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
   const int nbm = (a.mr + C::BM - 1) / C::BM;
   dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm);
-  bse::hop_rs_tma_kernel<C><<<grid, C::THREADS + 32, C::SMEM, ctx->stream>>>(a, mp);
+  bse::hop_rs_tma_kernel<C, TRANS><<<grid, C::THREADS + 32, smem, ctx->stream>>>(a, mp);
   check_launch(ctx);
 }
 
 // one real-split product (folded input x1 / x2, output halves y1 / y2) on the tile's planes g
+template <bool TRANS = false>
 void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   switch (ctx->filter_cm) {
-    case 91: launch_rs<RsWide>(ctx, a, g, ldg); break;
-    case 92: launch_rs<RsTall>(ctx, a, g, ldg); break;
-    case 93: launch_rs<RsQuad>(ctx, a, g, ldg); break;
-    case 94: launch_rs<RsNarrow>(ctx, a, g, ldg); break;
-    case 95: launch_rs<RsTallK32>(ctx, a, g, ldg); break;
-    case 96: launch_rs<RsTallDeep>(ctx, a, g, ldg); break;
+    case 92: launch_rs<RsTall, TRANS>(ctx, a, g, ldg); break;
+    case 94: launch_rs<RsNarrow, TRANS>(ctx, a, g, ldg); break;
     default:
       if (a.k >= 512)
-        launch_rs<RsTall>(ctx, a, g, ldg);
+        launch_rs<RsTall, TRANS>(ctx, a, g, ldg);
       else
-        launch_rs<RsNarrow>(ctx, a, g, ldg);
+        launch_rs<RsNarrow, TRANS>(ctx, a, g, ldg);
   }
 }
 
@@ -585,11 +561,7 @@ void zgemm(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const zv
            int64_t ldb, double beta, zval* c, int64_t ldc, zval* ws) {
   if (M == 0 || N == 0) return;
   using C = GemmMain;
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::zgemm_kernel<C, OPA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    configured = true;
-  }
+  ensure_smem(ctx, (const void*)bse::zgemm_kernel<C, OPA>, (int)C::SMEM);
   bse::GemmArgs g{};
   g.a = a;
   g.lda = lda;
@@ -904,14 +876,8 @@ bool c64_pair(int64_t k) {
 }
 
 void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const C64Step& st) {
-  static bool configured = false;
-  if (!configured) {
-    CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)bse::c64::SMEM));
-    CUDA_OK(cudaFuncSetAttribute(bse::c64::step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)bse::c64::PAIR_SMEM));
-    configured = true;
-  }
+  ensure_smem(ctx, (const void*)bse::c64::step_kernel<false>, (int)bse::c64::SMEM);
+  ensure_smem(ctx, (const void*)bse::c64::step_kernel<true>, (int)bse::c64::PAIR_SMEM);
   c64_x_maps(maps, st.x, st.kc, st.k);
   bse::c64::StepArgs a{};
   a.mo = (int)st.mo;
@@ -1541,6 +1507,22 @@ int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* t, const void* d_g, i
       throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
     if (ctx->ham_flags & BSE_HAM_B_ZERO) throw BseError(BSE_EVALIDATION, "the real-split product needs B != 0");
     rs_product(ctx, a, static_cast<const double*>(d_g), ldg);
+  });
+}
+
+int bse_hop_tile_rs_t(bse_ctx* ctx, const bse_hop_tile_args* t, const void* d_g, int64_t ldg) {
+  return guarded(ctx, [&] {
+    if (!t || !d_g) throw BseError(BSE_EVALIDATION, "null args");
+    if (t->k <= 0 || t->mr <= 0) return;
+    bse::HopArgs a = tile_args(t);
+    if (a.kc <= 0) throw BseError(BSE_EVALIDATION, "empty contraction");
+    if (ldg < a.kc || (ldg & 1)) throw BseError(BSE_EVALIDATION, "ldg must be even and >= kc (the plane rows)");
+    if (a.low_sign != 1.0) throw BseError(BSE_EVALIDATION, "the real-split product has no S-flip (low_sign 1)");
+    if (a.beta != 0.0 && (!a.p1 || !a.p2)) throw BseError(BSE_EVALIDATION, "beta != 0 needs p1/p2");
+    if ((a.shift != 0.0 || a.shift_col) && a.shift_hi > a.shift_lo && (!a.s1 || !a.s2))
+      throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
+    if (ctx->ham_flags & BSE_HAM_B_ZERO) throw BseError(BSE_EVALIDATION, "the real-split product needs B != 0");
+    rs_product<true>(ctx, a, static_cast<const double*>(d_g), ldg);
   });
 }
 

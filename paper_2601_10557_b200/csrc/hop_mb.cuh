@@ -1,18 +1,11 @@
-// 3M filter product (hop_kernel CM == 6 math) with an mbarrier pipeline instead of one
-// __syncthreads per K stage.
+// 3M filter product fed by TMA through mbarrier rings (hop3m_tma_kernel), plus the mbarrier
+// helpers the real-split kernel (hop_rs.cuh) shares.
 //
-// hop_kernel synchronises the whole CTA at every 8-wide K stage; ncu shows the DMMA pipe 24% idle
-// while warps are throttled on it, i.e. the warps of an SM stall and then burst together.  Here
-// every stage buffer has two mbarriers:
-//   full[s]   THREADS arrivals, each one a cp.async.mbarrier.arrive.noinc of a thread's copies,
-//   empty[s]  one arrival per warp once it has read the stage.
-// A warp computes stage kt as soon as its bytes landed and refills the buffer of stage kt - 1 as
-// soon as every warp has left stage kt - 1, so warps drift up to a stage apart instead of meeting
-// at a barrier.  The loader keeps loop-invariant shared offsets and global pointers (the A part,
-// then the B part) instead of recomputing addresses and predicates for every copy.
-//
-// Semantics are those of hop_kernel<C, HOP_AXPBY, 6> (hop.cuh): U = P Xa, L' = conj(P) Xb with
-// Gauss's 3M split on the precomputed (Pr + Pi, Pr - Pi) planes; same epilogue.
+// Every stage buffer has two mbarriers: full[s] (the producer's expect-tx arrival; the TMA bytes
+// complete it) and empty[s] (one arrival per consumer warp once it has read the stage), so warps
+// drift up to a stage apart instead of meeting at a CTA barrier.  The math is hop_kernel's
+// CM == 6 3M split (hop.cuh): U = P Xa, L' = conj(P) Xb on the precomputed (Pr + Pi, Pr - Pi)
+// planes; same epilogue.  (Round 1's cp.async-fed version of this pipeline is retired.)
 #pragma once
 #include <cuda.h>
 
@@ -26,10 +19,6 @@ __device__ __forceinline__ void mbar_init_cta(uint64_t* bar, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-// arrive on bar once all prior cp.async of this thread have landed; counts as one expected arrival
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cta(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -52,74 +41,6 @@ struct MbLayout {
   static constexpr int X_ELEMS = C::BN * LDX;
   static constexpr int STAGE_ELEMS = C::P_ELEMS + C::SD_ELEMS + 2 * X_ELEMS;
   static constexpr size_t SMEM = size_t(C::STAGES) * STAGE_ELEMS * sizeof(zval);
-};
-
-// Per-thread copy slots of one stage: NP (P and sum-plane) slots and NX (X) slots.
-template <class C>
-struct MbLoader {
-  using L = MbLayout<C>;
-  static constexpr int NP = (C::BK * C::BM + C::THREADS - 1) / C::THREADS;
-  static constexpr int NX = (2 * C::BN * C::BK + C::THREADS - 1) / C::THREADS;
-  static constexpr bool X_ALL = (2 * C::BN * C::BK) % C::THREADS == 0;  // else the last X slot is partial
-  static_assert((C::BK * C::BM) % C::THREADS == 0, "hop3m_mb_kernel: the P tile must split evenly over the threads");
-  const zval* p[NP];
-  const zval* sd[NP];
-  const zval* x[NX];
-  uint32_t p_off[NP], x_off[NX];  // shared element offsets inside a stage
-  int pk[NP], xk[NX];              // K index of the slot inside the stage
-  bool prow[NP], xcol[NX];         // row / column inside the problem
-  bool xact[NX];                   // slot holds an element of the stage tile
-
-  __device__ __forceinline__ void init(const HopArgs& a, int part, int i0, int c0) {
-    const zval* P = part ? a.pb : a.pa;
-    const zval* SD = part ? a.sb : a.sa;
-    const zval* XA = part ? a.x2 : a.x1;
-    const zval* XB = part ? a.x1 : a.x2;
-#pragma unroll
-    for (int r = 0; r < NP; ++r) {
-      const int id = threadIdx.x + r * C::THREADS;
-      const int ii = id % C::BM, jj = id / C::BM;
-      prow[r] = i0 + ii < a.mr;
-      pk[r] = jj;
-      p_off[r] = jj * C::LDP + ii;
-      const int64_t o = (int64_t)jj * a.lda + (prow[r] ? i0 + ii : 0);
-      p[r] = P + o;
-      sd[r] = SD + o;
-    }
-#pragma unroll
-    for (int r = 0; r < NX; ++r) {
-      const int id0 = threadIdx.x + r * C::THREADS;
-      xact[r] = X_ALL || id0 < 2 * C::BN * C::BK;
-      const int id = xact[r] ? id0 : 0;
-      const int kk = id % C::BK, cc = (id / C::BK) % C::BN, which = id / (C::BK * C::BN);
-      xcol[r] = c0 + cc < a.k;
-      xk[r] = kk;
-      x_off[r] = which * L::X_ELEMS + cc * L::LDX + kk;
-      x[r] = (which ? XB : XA) + (int64_t)(xcol[r] ? c0 + cc : 0) * a.ldx + kk;
-    }
-  }
-
-  // copies of the stage whose K block starts at j0 (inside the current part); then advance
-  __device__ __forceinline__ void issue(zval* st, const HopArgs& a, int j0) {
-    zval* Ps = st;
-    zval* SDs = st + C::P_ELEMS;
-    zval* Xs = SDs + C::SD_ELEMS;
-    const bool tail = j0 + C::BK > a.kc;
-#pragma unroll
-    for (int r = 0; r < NP; ++r) {
-      const bool ok = prow[r] && (!tail || j0 + pk[r] < a.kc);
-      cp_async16(Ps + p_off[r], ok ? p[r] : a.pa, ok);
-      cp_async16(SDs + p_off[r], ok ? sd[r] : a.pa, ok);
-      p[r] += (int64_t)C::BK * a.lda;
-      sd[r] += (int64_t)C::BK * a.lda;
-    }
-#pragma unroll
-    for (int r = 0; r < NX; ++r) {
-      const bool ok = xcol[r] && (!tail || j0 + xk[r] < a.kc);
-      if (xact[r]) cp_async16(Xs + x_off[r], ok ? x[r] : a.pa, ok);
-      x[r] += C::BK;
-    }
-  }
 };
 
 // the 3M DMMA work of one landed stage (identical arithmetic to hop_kernel CM == 6)
@@ -163,76 +84,6 @@ __device__ __forceinline__ void mb_stage_mma(double (&acc)[6][C::WM][C::WN][2], 
       }
     }
   }
-}
-
-template <class C>
-__global__ void __launch_bounds__(C::THREADS, C::MINB) hop3m_mb_kernel(const HopArgs a) {
-  using L = MbLayout<C>;
-  static_assert(C::PS == 1, "hop3m_mb_kernel: 3M with P-side sum planes only");
-  constexpr int CM = 6;
-  constexpr int NWARPS = C::THREADS / 32;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  zval* smem = reinterpret_cast<zval*>(smem_raw);
-  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
-  const int c0 = blockIdx.x * C::BN;
-  const int i0 = blockIdx.y * C::BM;
-  const int nkt_part = (a.kc + C::BK - 1) / C::BK;
-  const int nkt = a.skip_b ? nkt_part : 2 * nkt_part;
-
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init_cta(&full[s], C::THREADS);
-      mbar_init_cta(&empty[s], NWARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-  }
-  __syncthreads();
-
-  MbLoader<C> ld;
-  ld.init(a, 0, i0, c0);
-  int lkt = 0;  // next stage to load
-  auto load_next = [&](int buf) {
-    if (lkt == nkt_part) ld.init(a, 1, i0, c0);
-    ld.issue(smem + buf * L::STAGE_ELEMS, a, (lkt >= nkt_part ? lkt - nkt_part : lkt) * C::BK);
-    cp_async_arrive_noinc(&full[buf]);
-    ++lkt;
-  };
-#pragma unroll 1
-  for (int s = 0; s < C::STAGES - 1; ++s)
-    if (lkt < nkt) load_next(s);
-
-  double acc[Acc<CM>::N][C::WM][C::WN][2];
-#pragma unroll
-  for (int q = 0; q < Acc<CM>::N; ++q)
-#pragma unroll
-    for (int i = 0; i < C::WM; ++i)
-#pragma unroll
-      for (int j = 0; j < C::WN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
-
-#pragma unroll 1
-  for (int kt = 0; kt < nkt; ++kt) {
-    const int s = kt % C::STAGES;
-    mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
-    const zval* Ps = smem + s * L::STAGE_ELEMS;
-    const zval* SDs = Ps + C::P_ELEMS;
-    const zval* Xas = SDs + C::SD_ELEMS;
-    const zval* Xbs = Xas + L::X_ELEMS;
-    mb_stage_mma<C>(acc, Ps, SDs, Xas, Xbs, wm, wn, g, t);
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cta(&empty[s]);
-    if (lkt < nkt) {
-      // the buffer of stage lkt last held stage lkt - STAGES == kt - 1: wait until every warp left it
-      const int b = lkt % C::STAGES;
-      if (kt >= 1) mbar_wait_cta(&empty[b], ((kt - 1) / C::STAGES) & 1);
-      load_next(b);
-    }
-  }
-  hop_epilogue_axpby<C, CM>(acc, a, i0, c0, wm, wn, g, t);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -20,6 +20,14 @@
 // Output half h contracts plane 2h against x (part 0) and plane 2h + 1 against y (part 1); the
 // pair (h, part) with h == part multiplies by i, done by rotating the B fragments in registers.
 //
+// Transposed-tile product (the 2D grid's row -> col step): the block
+// transposes A[C_J, R_I] = A[R_I, C_J]^H, B[C_J, R_I] = B[R_I, C_J]^T have planes
+//   Z' = -W^T,  V' = V^T,  U' = U^T,  W' = -Z^T
+// (Ar, Br symmetric, Ai antisymmetric, Bi symmetric), so the same four planes serve both
+// directions: TRANS reads them through a K-major TMA box (pitch BK + 4 doubles, == 4 mod 16:
+// conflict-free LDS.64 again) and multiplies by -i where the forward product multiplies by i.
+// A grid GPU therefore stores ONE tile's planes (32 m^2 / (p q) bytes) and nothing else.
+//
 // Feed: the TMA / producer-warp / mbarrier ring of hop3m_tma_kernel (hop_mb.cuh).  The real plane
 // tile lands with pitch BM + 4 doubles (== 4 mod 16: the 16 lanes of each half warp read 16
 // distinct 8-byte slots, conflict-free LDS.64), the complex X tile with pitch BK + 4 (LDS.128).
@@ -39,13 +47,21 @@ struct RsCfg {
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;  // consumer threads (+ one producer warp)
   static constexpr int LDP = BM + 4;                      // doubles
   static constexpr int LDX = BK + 4;                      // complex
-  static constexpr int P_BYTES = BK * LDP * 8;
+  static constexpr int LDK = BK + 4;                      // doubles (transposed plane tile)
   static constexpr int X_BYTES = BN * LDX * 16;
-  static constexpr int STAGE_BYTES = P_BYTES + X_BYTES;
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 128;
+  template <bool TRANS>
+  __host__ __device__ static constexpr int p_bytes() { return TRANS ? BM * LDK * 8 : BK * LDP * 8; }
+  template <bool TRANS>
+  __host__ __device__ static constexpr int stage_bytes() { return p_bytes<TRANS>() + X_BYTES; }
+  template <bool TRANS>
+  __host__ __device__ static constexpr size_t smem() { return size_t(STAGES) * stage_bytes<TRANS>() + 128; }
+  static constexpr int P_BYTES = p_bytes<false>();
+  static constexpr int STAGE_BYTES = stage_bytes<false>();
+  static constexpr size_t SMEM = smem<false>();
   static_assert(BM % 16 == 0 && BN % 8 == 0 && BK % 4 == 0, "RS tile dims");
-  static_assert(P_BYTES % 128 == 0 && X_BYTES % 128 == 0, "TMA destinations must stay 128-byte aligned");
-  static_assert(LDP <= 256 && 2 * LDX <= 256 && BN <= 256 && BK <= 256, "TMA box dimensions");
+  static_assert(p_bytes<false>() % 128 == 0 && p_bytes<true>() % 128 == 0 && X_BYTES % 128 == 0,
+                "TMA destinations must stay 128-byte aligned");
+  static_assert(LDP <= 256 && LDK <= 256 && 2 * LDX <= 256 && BN <= 256 && BK <= 256, "TMA box dimensions");
 };
 
 // Arguments: HopArgs (hop.cuh) with x1 / x2 = the x / y parts of the folded input (kc rows each),
@@ -56,7 +72,8 @@ struct RsMaps {
   CUtensorMap x[2];  // x and y parts of the input: (2 kc doubles) x k, leading dim 2 ldx
 };
 
-template <bool ROT, class C>
+// ROT: 0 -> x, +1 -> i x, -1 -> -i x; TRANS: the plane tile is K-major (see the header)
+template <int ROT, bool TRANS, class C>
 __device__ __forceinline__ void rs_stage_mma(double (&acc)[2][C::WM][C::WN][2], const double* Ps, const zval* Xs, int wm,
                                              int wn, int g, int t) {
 #pragma unroll
@@ -64,13 +81,19 @@ __device__ __forceinline__ void rs_stage_mma(double (&acc)[2][C::WM][C::WN][2], 
     double pf[C::WM];
     double br[C::WN], bi[C::WN];
 #pragma unroll
-    for (int i = 0; i < C::WM; ++i) pf[i] = Ps[(ks * 4 + t) * C::LDP + wm * (8 * C::WM) + i * 8 + g];
+    for (int i = 0; i < C::WM; ++i) {
+      const int r = wm * (8 * C::WM) + i * 8 + g;
+      pf[i] = TRANS ? Ps[r * C::LDK + ks * 4 + t] : Ps[(ks * 4 + t) * C::LDP + r];
+    }
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
       const zval xv = lds128(Xs + (wn * (8 * C::WN) + j * 8 + g) * C::LDX + ks * 4 + t);
-      if constexpr (ROT) {  // i * x
+      if constexpr (ROT > 0) {  // i * x
         br[j] = -xv.im;
         bi[j] = xv.re;
+      } else if constexpr (ROT < 0) {  // -i * x
+        br[j] = xv.im;
+        bi[j] = -xv.re;
       } else {
         br[j] = xv.re;
         bi[j] = xv.im;
@@ -87,9 +110,17 @@ __device__ __forceinline__ void rs_stage_mma(double (&acc)[2][C::WM][C::WN][2], 
 }
 
 // grid: x = column tiles (fastest: CTAs sharing a plane strip run together), y = 2 * row tiles
-template <class C>
+// plane read by output half h for input part (0: x, 1: y): forward Z V | U W, transposed W V | U Z
+template <bool TRANS>
+__device__ __forceinline__ int rs_plane(int h, int part) {
+  return TRANS ? (h ? (part ? 0 : 2) : (part ? 1 : 3)) : 2 * h + part;
+}
+
+template <class C, bool TRANS = false>
 __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(const HopArgs a,
                                                                               const __grid_constant__ RsMaps maps) {
+  constexpr int P_BYTES = C::template p_bytes<TRANS>();
+  constexpr int STAGE_BYTES = C::template stage_bytes<TRANS>();
   constexpr int NWARPS = C::THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base =
@@ -113,8 +144,8 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
       mbar_init_cta(&empty[s], NWARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
-    tc::prefetch_tmap(&maps.g[2 * h]);
-    tc::prefetch_tmap(&maps.g[2 * h + 1]);
+    tc::prefetch_tmap(&maps.g[rs_plane<TRANS>(h, 0)]);
+    tc::prefetch_tmap(&maps.g[rs_plane<TRANS>(h, 1)]);
     tc::prefetch_tmap(&maps.x[0]);
     tc::prefetch_tmap(&maps.x[1]);
   }
@@ -127,10 +158,13 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
         if (lkt >= C::STAGES) mbar_wait_cta(&empty[b], ((lkt - C::STAGES) / C::STAGES) & 1);
         const int part = lkt >= nkt_part;
         const int j0 = (lkt - part * nkt_part) * C::BK;
-        unsigned char* st = base + b * C::STAGE_BYTES;
-        tc::mbar_arrive_expect_tx(&full[b], C::STAGE_BYTES);
-        tc::tma_load_2d(st, &maps.g[2 * h + part], &full[b], i0, j0);
-        tc::tma_load_2d(st + C::P_BYTES, &maps.x[part], &full[b], 2 * j0, c0);
+        unsigned char* st = base + b * STAGE_BYTES;
+        tc::mbar_arrive_expect_tx(&full[b], STAGE_BYTES);
+        if (TRANS)
+          tc::tma_load_2d(st, &maps.g[rs_plane<TRANS>(h, part)], &full[b], j0, i0);
+        else
+          tc::tma_load_2d(st, &maps.g[rs_plane<TRANS>(h, part)], &full[b], i0, j0);
+        tc::tma_load_2d(st + P_BYTES, &maps.x[part], &full[b], 2 * j0, c0);
       }
     }
     return;
@@ -148,12 +182,12 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   for (int kt = 0; kt < nkt; ++kt) {
     const int s = kt % C::STAGES;
     mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
-    const double* Ps = reinterpret_cast<const double*>(base + s * C::STAGE_BYTES);
-    const zval* Xs = reinterpret_cast<const zval*>(base + s * C::STAGE_BYTES + C::P_BYTES);
+    const double* Ps = reinterpret_cast<const double*>(base + s * STAGE_BYTES);
+    const zval* Xs = reinterpret_cast<const zval*>(base + s * STAGE_BYTES + P_BYTES);
     if ((kt >= nkt_part) == (h == 1))
-      rs_stage_mma<true, C>(acc, Ps, Xs, wm, wn, g, t);
+      rs_stage_mma<TRANS ? -1 : 1, TRANS, C>(acc, Ps, Xs, wm, wn, g, t);
     else
-      rs_stage_mma<false, C>(acc, Ps, Xs, wm, wn, g, t);
+      rs_stage_mma<0, TRANS, C>(acc, Ps, Xs, wm, wn, g, t);
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);
   }

@@ -161,6 +161,10 @@ class Comm:
         if self.g.world > 1:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
 
+    def min_all(self, t) -> None:
+        if self.g.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+
     def gather(self, t, group: str) -> list:
         """allgather of equally shaped contiguous tensors within the row / col group."""
         import torch
@@ -213,9 +217,17 @@ class CudaOps:
         args.alpha, args.beta, args.low_sign = alpha, beta, low_sign
         args.filter = 1 if filter else 0
         if rs:
-            self.ctx.call("bse_hop_tile_rs", ctypes.byref(args), tile.g.data_ptr(), tile.ldg)
+            self.ctx.call("bse_hop_tile_rs_t" if tile.trans else "bse_hop_tile_rs", ctypes.byref(args),
+                          tile.g.data_ptr(), tile.ldg)
         else:
             self.ctx.call("bse_hop_tile", ctypes.byref(args))
+
+    def make_rs_planes(self, tile):
+        """Real-split planes [Z | V | U | W] (mr x 4kc doubles, leading dim ldg) of a complex tile."""
+        ldg = tile.mr + (tile.mr & 1)
+        g = self.torch.empty((4 * tile.kc, ldg), dtype=self.torch.float64, device=self.device)
+        self.ctx.call("bse_make_rs_planes", tile.buf.data_ptr(), tile.lda, tile.mr, tile.kc, g.data_ptr(), ldg)
+        return g, ldg
 
     def rs_fold(self, v, rows: int, scale: float, scale2: float | None = None, out=None):
         """(X1, X2) -> (scale (X1 + X2), scale2 (X1 - X2)) of a (k x 2 rows) storage block into out
@@ -365,6 +377,39 @@ class Tile:
     sb: int = 0
     g: object = None  # optional real-split planes (csrc/hop_rs.cuh), mr x 4kc doubles, leading dim ldg
     ldg: int = 0
+    trans: bool = False  # the block transpose of the tile whose planes g holds (bse_hop_tile_rs_t)
+
+
+def plane_tiles(ops, tile: Tile) -> tuple[Tile, Tile]:
+    """(forward, transposed) views of ONE set of real-split planes built from the complex tile
+    (A, B)[R_I, C_J]; the complex tile can be freed afterwards.  The transposed view computes the
+    row -> col product with A[C_J, R_I] = A[R_I, C_J]^H, B[C_J, R_I] = B[R_I, C_J]^T read from the
+    same planes (hop_rs.cuh), so this is the whole operator storage of a grid GPU: 32 mr kc bytes."""
+    g, ldg = ops.make_rs_planes(tile)
+    fwd = Tile(None, 0, 0, 0, tile.mr, tile.kc, g=g, ldg=ldg)
+    trn = Tile(None, 0, 0, 0, tile.kc, tile.mr, g=g, ldg=ldg, trans=True)
+    return fwd, trn
+
+
+def complex_tiles_from_planes(ops, fwd: Tile) -> tuple[Tile, Tile]:
+    """Complex (A_t | B_t) forward and transposed tiles rebuilt from the planes (Ar = (V + U)/2,
+    Br = (U - V)/2, Ai = (Z + W)/2, Bi = (Z - W)/2; exact to rounding), for the complex64 filter's
+    plane conversion only (a temporary; FP32 accuracy there)."""
+    torch = ops.torch
+    mr, kc = fwd.mr, fwd.kc
+    gm = fwd.g.t()[:mr]  # (mr, 4 kc) view, column-major
+    z, v, u, w = (gm[:, q * kc:(q + 1) * kc] for q in range(4))
+    a_t = torch.complex((v + u) * 0.5, (z + w) * 0.5)
+    b_t = torch.complex((u - v) * 0.5, (z - w) * 0.5)
+    out = []
+    for at, bt in ((a_t, b_t), (a_t.conj().T, b_t.T)):
+        rows, cols = at.shape
+        buf = torch.empty((2 * cols, rows), dtype=torch.complex128, device=ops.device)
+        buf[:cols].copy_(at.T)
+        buf[cols:].copy_(bt.T)
+        addr = buf.data_ptr()
+        out.append(Tile(buf, addr, addr + rows * cols * ZB, rows, rows, cols))
+    return tuple(out)
 
 
 def add_sum_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
@@ -399,27 +444,26 @@ def add_rs_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
     return tile
 
 
-def make_tiles(ops, grid: Grid, a_blocks, b_blocks):
-    """Forward tile (A, B)[R_I, C_J] and transposed tile (A, B)[C_J, R_I] from full (host or device)
-    blocks; each stored as one column-major [A_t | B_t] buffer."""
+def tile_from_blocks(ops, a_t, b_t, transpose: bool = False) -> Tile:
+    """One column-major [A_t | B_t] device buffer from tile blocks (host numpy or device tensors);
+    transpose: the block transpose [A_t^H | B_t^T] instead."""
     torch = ops.torch
+    if transpose:
+        a_t = a_t.conj().T
+        b_t = b_t.T
+    mr, kc = a_t.shape
+    buf = torch.empty((2 * kc, mr), dtype=torch.complex128, device=ops.device)  # storage of mr x 2kc
+    for h, blk in enumerate((a_t, b_t)):
+        src = torch.from_numpy(np.ascontiguousarray(blk.T)) if isinstance(blk, np.ndarray) else blk.T
+        buf[h * kc:(h + 1) * kc].copy_(src)
+    addr = buf.data_ptr()
+    return Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc)
 
-    def one(rows, cols):
-        r0, r1 = rows
-        c0, c1 = cols
-        mr, kc = r1 - r0, c1 - c0
-        buf = torch.empty((2 * kc, mr), dtype=torch.complex128, device=ops.device)  # storage of mr x 2kc
-        for h, blk in enumerate((a_blocks, b_blocks)):
-            src = blk[r0:r1, c0:c1]
-            if isinstance(src, np.ndarray):
-                src = torch.from_numpy(np.ascontiguousarray(src.T)).T
-            buf[h * kc:(h + 1) * kc].copy_(src.T)
-        addr = buf.data_ptr()
-        return Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc)
 
-    fwd = one((grid.r0, grid.r1), (grid.c0, grid.c1))
-    trn = one((grid.c0, grid.c1), (grid.r0, grid.r1))
-    return fwd, trn  # 3M sum planes are attached lazily at the first solve (after the source is freed)
+def slice_tile(ops, rows, cols, a_blocks, b_blocks) -> Tile:
+    """The tile (A, B)[rows, cols] of full (host or device) blocks."""
+    (r0, r1), (c0, c1) = rows, cols
+    return tile_from_blocks(ops, a_blocks[r0:r1, c0:c1], b_blocks[r0:r1, c0:c1])
 
 
 # ----------------------------------------------------------------------------- distributed solver
@@ -435,6 +479,8 @@ class DistSolver:
     def __init__(self, grid: Grid, comm: Comm, ops, fwd: Tile, trn: Tile):
         self.g, self.c, self.ops, self.fwd, self.trn = grid, comm, ops, fwd, trn
         self.torch = ops.torch
+        # real-split mode: this rank stores ONE tile's planes; every product runs on them
+        self.planes = fwd.g is not None and trn.g is not None
 
     # ---- layout helpers -----------------------------------------------------------------
     def col_rows(self, full_storage):
@@ -510,8 +556,8 @@ class DistSolver:
         if overlap and not hasattr(self, "_comm_stream"):
             self._comm_stream = torch.cuda.Stream(device=v_col.device)
         reduced = [None] * nch
-        # real-split planes on both tiles: run the recurrence in the folded basis (csrc/hop_rs.cuh)
-        rs = hasattr(self.ops, "ctx") and self.fwd.g is not None and self.trn.g is not None
+        # real-split planes: run the recurrence in the folded basis (csrc/hop_rs.cuh)
+        rs = self.planes
         if rs:
             self.ops.rs_fold(v_col, self.g.nc, 1.0)
         for ci in range(nch):
@@ -553,7 +599,9 @@ class DistSolver:
         ops = self.ops
         k = v_col.shape[0]
         if not hasattr(self, "_c64_pl"):
-            self._c64_pl = (ops.c64_tile_planes(self.fwd, self.trn), ops.c64_tile_planes(self.trn, self.fwd))
+            fwd, trn = complex_tiles_from_planes(ops, self.fwd) if self.planes else (self.fwd, self.trn)
+            self._c64_pl = (ops.c64_tile_planes(fwd, trn), ops.c64_tile_planes(trn, fwd))
+            del fwd, trn
         pl_fwd, pl_trn = self._c64_pl
         col, row = ops.c64_planes(g.nc, k), ops.c64_planes(g.nr, k)
         raw = ops.c64_raw(max(g.nr, g.nc), k)
@@ -683,7 +731,37 @@ class DistSolver:
             proj = self._gram_row(basis, v_col)  # l x k
             self.ops.nn(basis, proj, out=v_col, alpha=-1.0, beta=1.0)
             st.mark("projection", v_col.shape[0])
-        return self.cholqr(v_col)
+        q, method = self.cholqr(v_col)
+        self.fix_phases(q)
+        st.mark("phase convention", q.shape[0])
+        return q, method
+
+    def fix_phases(self, q_col) -> None:
+        """ortho.py:70-82 on the grid (the single-GPU phase_fix_kernel's convention): each column is
+        scaled by conj(p)/|p|, p its first entry in GLOBAL row order (upper half, then lower) with
+        |q| >= 1e-8 max|q|.  Three k-length collectives: max, first index, the entry itself (sent by
+        the I = 0 replica of the column group that holds it)."""
+        torch, g = self.torch, self.g
+        k = q_col.shape[0]
+        if k == 0:
+            return
+        if not hasattr(self, "_gidx") or self._gidx.numel() != 2 * g.nc:
+            self._gidx = torch.cat([torch.arange(g.c0, g.c1), g.m + torch.arange(g.c0, g.c1)]).to(
+                device=q_col.device, dtype=torch.float64)
+        mag = q_col.abs()
+        top = mag.amax(dim=1) if mag.shape[1] else torch.zeros(k, dtype=torch.float64, device=q_col.device)
+        self.c.max_all(top)
+        big = float(2 * g.m)
+        hit = mag >= (1e-8 * top)[:, None]
+        first = torch.where(hit, self._gidx[None, :], torch.full_like(mag, big)).amin(dim=1) if mag.shape[1] else \
+            torch.full((k,), big, dtype=torch.float64, device=q_col.device)
+        self.c.min_all(first)
+        sel = (self._gidx[None, :] == first[:, None]) & hit
+        val = (q_col * sel).sum(dim=1) if g.I == 0 else torch.zeros(k, dtype=q_col.dtype, device=q_col.device)
+        self.c.sum_all(val)
+        ap = val.abs()
+        fac = torch.where(ap > 0, val.conj() / torch.where(ap > 0, ap, torch.ones_like(ap)), torch.ones_like(val))
+        q_col *= fac[:, None]
 
     # ---- Rayleigh-Ritz + residuals ------------------------------------------------------------
     def rayleigh_ritz(self, q_col, row_buf, fused_residuals: bool = False, variant: str = "auto", it: int = 0,
@@ -697,7 +775,7 @@ class DistSolver:
         n, nr = 2 * self.g.m, self.g.nr
         st = _Steps("rr", self.g.rank)
         t_row = row_buf[:k]
-        if hasattr(self.ops, "ctx") and self.fwd.g is not None:
+        if self.planes:
             # T = S H Q on the real-split planes: fold Q, tile product + row allreduce, unfold with the S-flip
             q_f = self.torch.empty_like(q_col)
             self.ops.rs_fold(q_col, self.g.nc, 1.0, out=q_f)
@@ -711,11 +789,15 @@ class DistSolver:
         st.mark("allgather Q", k)
         q_rows = self.row_rows(q_full)
         rlo, rhi = self._share(nr, "row")  # this replica's share of the rows of each half
-        gtb = self.torch.stack([self.ops.gram(q_rows[:, rlo:rhi], t_row[:, rlo:rhi]),
-                                self.ops.gram(q_rows[:, nr + rlo:nr + rhi], t_row[:, nr + rlo:nr + rhi])])
-        self.c.sum_all(gtb)
-        g2 = self._gram_row(q_col[:, self.g.nc:])
-        st.mark("Q^H T halves, Q2^H Q2 + allreduce", k)
+        clo, chi = self._share(self.g.nc, "col")
+        nc = self.g.nc
+        # [Q^H T (upper rows) | Q^H T (lower rows) | Q2^H Q2]: three partial Grams, ONE allreduce
+        grams = self.torch.stack([self.ops.gram(q_rows[:, rlo:rhi], t_row[:, rlo:rhi]),
+                                  self.ops.gram(q_rows[:, nr + rlo:nr + rhi], t_row[:, nr + rlo:nr + rhi]),
+                                  self.ops.gram(q_col[:, nc + clo:nc + chi], q_col[:, nc + clo:nc + chi])])
+        self.c.sum_all(grams)
+        gtb, g2 = grams[:2], grams[2]
+        st.mark("Q^H T halves, Q2^H Q2 + one allreduce", k)
         used, fallback, lam = "hermitian", False, None
         if ledger is not None:
             ledger.add_flops("rr", 8.0 * n * n * k)  # apply_h inside RR (hamiltonian.py:148-150)
@@ -738,24 +820,26 @@ class DistSolver:
             if ledger is not None:
                 ledger.add_flops("rr", 8.0 * n * n * k + 20.0 * n * k * k + 30.0 * k**3)
         st.mark("pencil", k)
+        torch = self.torch
         v = self.ops.nn(q_col, wvec)
-        n2 = self._colnorm2(v, "col")
-        self.ops.colscale_rsqrt(v, n2)
-        st.mark("V = Q w, normalise", k)
-        res = None
+        # column norms of V (col layout) and, fused, the residual partials |S T w - lam Q w|^2 (row
+        # layout): one allreduce of both k-vectors
+        red = torch.zeros((2, k), dtype=torch.float64, device=v.device)
+        lo, hi = self._share(v.shape[1], "col")
+        red[0] = self.ops.colnorm2(v[:, lo:hi])
         if fused_residuals:
-            torch = self.torch
             ones = torch.ones(k, dtype=torch.float64, device=v.device)
             lam_d = torch.as_tensor(np.ascontiguousarray(lam), dtype=torch.float64, device=v.device)
-            r2 = torch.zeros(k, dtype=torch.float64, device=v.device)
             for off, half in ((0, rhi - rlo), (nr, 0)):  # upper share (no sign flip), lower share (S: negated)
                 sl = slice(off + rlo, off + rhi)
                 if rhi > rlo:
-                    r2 += self.ops.resid_partial(self.ops.nn(t_row[:, sl], wvec), self.ops.nn(q_rows[:, sl], wvec),
-                                                 half, ones, lam_d)
-            self.c.sum_all(r2)
-            res = np.sqrt(r2.cpu().numpy() / n2.cpu().numpy())
-            st.mark("residuals from S T w", k)
+                    red[1] += self.ops.resid_partial(self.ops.nn(t_row[:, sl], wvec),
+                                                     self.ops.nn(q_rows[:, sl], wvec), half, ones, lam_d)
+        self.c.sum_all(red)
+        n2 = red[0].contiguous()
+        self.ops.colscale_rsqrt(v, n2)
+        res = np.sqrt(red[1].cpu().numpy() / n2.cpu().numpy()) if fused_residuals else None
+        st.mark("V = Q w, normalise (+ residuals from S T w), one allreduce", k)
         return lam, v, lmm, res, used, fallback
 
     _PENCIL_ERRORS = {1: "Cholesky of Q*SHQ failed; S*H is not definite on the subspace",
@@ -764,7 +848,7 @@ class DistSolver:
     def _pencil(self, w, g2):
         """The k x k pencil of the hermitian RR (rayleigh_ritz.py:113-137).  On one GPU as a whole; on a
         grid its two independent halves run concurrently on ranks 1 (eigenvalues of M) and 0 (chol(W),
-        G, eigh(G), back-transform), then one small allreduce and two broadcasts share the results.
+        G, eigh(G), back-transform), then one small allreduce and one broadcast share the results.
         Errors keep the reference's order: a singular M first, then the Cholesky / theta ~ 0 failures."""
         g = self.g
         if g.world == 1 or not hasattr(self.ops, "rr_pencil_part"):
@@ -788,23 +872,42 @@ class DistSolver:
             raise HermitianRqError(f"|lambda_min(Q*SQ)| = {lmm:.6e} below 1e-8")
         if code:
             raise HermitianRqError(self._PENCIL_ERRORS[code])
-        self.c.bcast_all(lam_d, src=0)
-        self.c.bcast_all(wvec, src=0)
-        return lam_d.cpu().numpy(), wvec, lmm
+        # [w vectors | lambda] in one broadcast
+        pack = torch.empty(k * k + k, dtype=torch.complex128, device=w.device)
+        if g.rank == 0:
+            pack[:k * k].copy_(wvec.reshape(-1))
+            pack[k * k:].copy_(lam_d)
+        self.c.bcast_all(pack, src=0)
+        wvec = pack[:k * k].view(k, k)
+        return pack[k * k:].real.cpu().numpy(), wvec, lmm
 
     def residuals(self, v_col, lam, row_buf) -> np.ndarray:
         k = v_col.shape[0]
         r_row = row_buf[:k]
         lam_d = self.torch.as_tensor(np.ascontiguousarray(lam), dtype=self.torch.float64, device=v_col.device)
-        self.forward(v_col, r_row, shift_col=lam_d)  # R = H V - V Lambda (rows R_I)
-        n2 = self._colnorm2(r_row, "row")
+        if self.planes:
+            # folded: (R1 + R2, R1 - R2) = H_f v_f - Lambda v_f, and |r_x|^2 + |r_y|^2 = 2 |R|^2
+            v_f = self.torch.empty_like(v_col)
+            self.ops.rs_fold(v_col, self.g.nc, 1.0, out=v_f)
+            self.forward(v_f, r_row, shift_col=lam_d, filter=True, rs=True)
+            del v_f
+            n2 = self._colnorm2(r_row, "row") * 0.5
+        else:
+            self.forward(v_col, r_row, shift_col=lam_d)  # R = H V - V Lambda (rows R_I)
+            n2 = self._colnorm2(r_row, "row")
         return np.sqrt(n2.cpu().numpy())
 
     # ---- Lanczos (lanczos.py:53-142) ------------------------------------------------------------
     def matvec_full(self, x_full):
         """H x for a full (1, n) storage vector; returns the full product on every rank."""
         y_row = self.ops.empty(1, 2 * self.g.nr)
-        self.forward(self.col_rows(x_full), y_row)
+        x_col = self.col_rows(x_full)
+        if self.planes:  # fold, product on the planes, unfold
+            self.ops.rs_fold(x_col, self.g.nc, 1.0)
+            self.forward(x_col, y_row, filter=True, rs=True)
+            self.ops.rs_fold(y_row, self.g.nr, 0.5)
+        else:
+            self.forward(x_col, y_row)
         return self.assemble_from_row(y_row)
 
     def lanczos(self, nevex: int, steps: int, seed: int, ledger: PhaseLedger) -> SpectralBounds:
@@ -973,12 +1076,20 @@ def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):
 
 
 class DistributedSolver:
-    """Holds the grid, the communicators and this rank's tiles across solves (SPMD; every rank of an
-    initialised torch.distributed world constructs it with the same Hamiltonian).  ``source`` is a
-    BseHamiltonian (host or device-born) or an (A, B) pair of host/device blocks, or a dict
-    {"fwd": (A_t, B_t), "trn": (A_t', B_t')} of this rank's own tile blocks."""
+    """Holds the grid, the communicators and this rank's operator storage across solves (SPMD; every
+    rank of an initialised torch.distributed world constructs it with the same Hamiltonian).
+    ``source`` is a BseHamiltonian (host or device-born) or an (A, B) pair of host/device blocks, or
+    a dict {"fwd": (A_t, B_t)} of this rank's own tile (A, B)[R_I, C_J].
 
-    def __init__(self, source, *, m: int | None = None, device=None, grid: Grid | None = None, ops=None):
+    Storage (one decision for the whole grid: it depends only on settings every rank shares):
+      * real-split (default, B != 0): the planes of the tile (A, B)[R_I, C_J] and nothing else,
+        32 m^2 / (p q) bytes per GPU -- the paper's A/B-only layout; the transposed products read
+        the same planes (bse_hop_tile_rs_t);
+      * complex (B = 0, where the 3M kernel skips the B half, or planes=False): the complex tile and
+        its block transpose (+ optional 3M sum planes)."""
+
+    def __init__(self, source, *, m: int | None = None, device=None, grid: Grid | None = None, ops=None,
+                 planes: bool | None = None):
         import torch
 
         world = torch.distributed.get_world_size() if torch.distributed.is_initialized() else 1
@@ -1004,39 +1115,46 @@ class DistributedSolver:
             m = source[0].shape[0]
             b = source[1]
             self.flags = 0 if (bool(b.any()) if hasattr(b, "any") else True) else 1
+        if planes is None:
+            planes = _lib.uses_rs_planes() and not self.flags & 1
+        self.use_planes = bool(planes) and hasattr(self.ops, "make_rs_planes")
         self.grid = grid or Grid(m, world, rank)
         self.comm = Comm(self.grid)
         self.load(source)
 
+    @property
+    def planes(self) -> bool:
+        return self.inner.planes
+
     def load(self, source) -> None:
-        """(Re)upload this rank's tiles (host -> device when the blocks are numpy)."""
+        """(Re)build this rank's operator storage (host -> device when the blocks are numpy)."""
+        g = self.grid
         if isinstance(source, dict):
-            self.fwd, self.trn = make_tiles_from_pieces(self.ops, source)
+            fwd = tile_from_blocks(self.ops, *source["fwd"])
+            trn = None if self.use_planes else tile_from_blocks(self.ops, *source["fwd"], transpose=True)
         else:
-            self.fwd, self.trn = make_tiles(self.ops, self.grid, *source)
+            fwd = slice_tile(self.ops, (g.r0, g.r1), (g.c0, g.c1), *source)
+            trn = None if self.use_planes else slice_tile(self.ops, (g.c0, g.c1), (g.r0, g.r1), *source)
+        if self.use_planes:
+            self.fwd, self.trn = plane_tiles(self.ops, fwd)
+            del fwd  # the complex tile was only the planes' source
+        else:
+            self.fwd, self.trn = fwd, trn
         self.inner = DistSolver(self.grid, self.comm, self.ops, self.fwd, self.trn)
 
-    def tile_pieces_host(self) -> dict:
-        """This rank's tile blocks as host numpy arrays (for end-to-end timing from host buffers)."""
-        out = {}
-        for name, t in (("fwd", self.fwd), ("trn", self.trn)):
-            mat = t.buf.cpu().numpy().T  # (mr, 2kc) F-order view
-            out[name] = (np.asfortranarray(mat[:, :t.kc]), np.asfortranarray(mat[:, t.kc:]))
-        out["flags"] = self.flags
-        return out
+    def operator_bytes(self) -> int:
+        """Device bytes of this rank's operator storage."""
+        if self.planes:
+            return self.fwd.g.numel() * 8
+        return sum(t.buf.numel() * ZB + (t.sd.numel() * ZB if t.sd is not None else 0) for t in (self.fwd, self.trn))
 
     def solve(self, cfg: SolverConfig) -> SolveResult:
         if hasattr(self.ops, "ctx"):
             self.ops.ctx.set_ham_flags(self.flags)
         g = self.inner.g
-        # vectors of the solve: col / row blocks, locked block, the RR's T and products (~6 blocks)
-        reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
-        if _lib.uses_rs_planes() and not self.flags & 1:
-            # real-split planes for the filter and the RR's T = S H Q (csrc/hop_rs.cuh)
-            for t in (self.fwd, self.trn):
-                if t.g is None:
-                    add_rs_planes(self.ops, t, reserve)
-        if _lib.uses_sum_planes() and (self.fwd.g is None or self.trn.g is None):
+        if not self.planes and _lib.uses_sum_planes():
+            # complex storage: optional 3M sum planes (bitwise-identical products without them)
+            reserve = 6 * 16 * cfg.nevex * 2 * max(g.nr, g.nc)
             for t in (self.fwd, self.trn):
                 if t.sd is None:
                     add_sum_planes(self.ops, t, reserve)
@@ -1045,19 +1163,25 @@ class DistributedSolver:
         return res
 
 
-def make_tiles_from_pieces(ops, pieces: dict):
-    torch = ops.torch
-    tiles = []
-    for name in ("fwd", "trn"):  # "flags" entry (if any) is read by DistributedSolver
-        a_t, b_t = pieces[name]
-        mr, kc = a_t.shape
-        buf = torch.empty((2 * kc, mr), dtype=torch.complex128, device=ops.device)
-        for h, blk in enumerate((a_t, b_t)):
-            src = torch.from_numpy(np.ascontiguousarray(blk.T)) if isinstance(blk, np.ndarray) else blk.T
-            buf[h * kc:(h + 1) * kc].copy_(src)
-        addr = buf.data_ptr()
-        tiles.append(Tile(buf, addr, addr + mr * kc * ZB, mr, mr, kc))
-    return tuple(tiles)
+def tile_blocks_host(grid: Grid, source) -> dict:
+    """This rank's tile (A, B)[R_I, C_J] as host numpy arrays (F-order), from a BseHamiltonian or
+    full (A, B) blocks -- the pre-sliced input a user hands DistributedSolver (bench e2e)."""
+    if hasattr(source, "device_blocks"):
+        if source.a is not None:
+            a, b = source.a, source.b
+        else:
+            ab = source.device_blocks()
+            a, b = ab[:, :source.m], ab[:, source.m:]
+        flags = source.flags
+    else:
+        a, b = source
+        flags = 0
+    out = []
+    for blk in (a, b):
+        t = blk[grid.r0:grid.r1, grid.c0:grid.c1]
+        t = t.T.contiguous().cpu().numpy().T if hasattr(t, "cpu") else np.asfortranarray(t)
+        out.append(np.asfortranarray(t))
+    return {"fwd": tuple(out), "flags": flags}
 
 
 def solve_distributed(source, cfg: SolverConfig, *, device=None, grid: Grid | None = None, ops=None) -> SolveResult:

@@ -192,10 +192,11 @@ class BseHamiltonian:
         if sd is None:
             ab = self.device_blocks(device)
             if not _lib.planes_fit(ab.numel() * 16, device, reserve):
-                logger.warning("3M sum planes (%.1f GB) do not fit next to the solve; forming the operand sums "
-                               "in registers", ab.numel() * 16 / 1e9)
-                sd_cache[device] = False
-                return None
+                if device not in self.__dict__.setdefault("_sd_warned", set()):
+                    self._sd_warned.add(device)
+                    logger.warning("3M sum planes (%.1f GB) do not fit next to the solve; forming the operand sums "
+                                   "in registers", ab.numel() * 16 / 1e9)
+                return None  # decided again next call
             sd = colmajor_empty(ab.shape[0], ab.shape[1], device)
             _lib.Context.get(device.index).call("bse_make_sum_planes", _lib.dptr(ab), ld_of(ab), ab.shape[0],
                                                 ab.shape[1], _lib.dptr(sd))
@@ -216,9 +217,11 @@ class BseHamiltonian:
             ab = self.device_blocks(device)
             m = self.m
             ldg = m + (m & 1)
-            if self.b_is_zero or not _lib.planes_fit(ldg * 4 * m * 8, device, reserve):
+            if self.b_is_zero:
                 cache[device] = False
                 return None
+            if not _lib.planes_fit(ldg * 4 * m * 8, device, reserve):
+                return None  # decided again next call: HBM pressure is not a property of the operator
             g = torch.empty((4 * m, ldg), dtype=torch.float64, device=device).t()  # column-major m x 4m, ld ldg
             _lib.Context.get(device.index).call("bse_make_rs_planes", _lib.dptr(ab), ld_of(ab), m, m, _lib.dptr(g), ldg)
             cache[device] = g
@@ -241,8 +244,8 @@ class BseHamiltonian:
         return pl
 
     def release_device(self) -> None:
-        self.__dict__.get("_sd", {}).clear()
-        self.__dict__.get("_p64", {}).clear()
+        for cache in ("_sd", "_p64", "_rs"):
+            self.__dict__.get(cache, {}).clear()
         if self.a is not None:
             self._dev.clear()
 

@@ -4,9 +4,9 @@
 streams.  Computed on the host with numpy so the start vectors of a solve are
 the very same bits the reference draws (GPU libm would differ in the last
 ulp and can change a small case's iteration trace).  Above EXACT_LIMIT
-(generate.py's policy, where the Hamiltonian itself comes from the device
-generator) the start block is drawn on the device: bit-exact words, Box-Muller
-within ~1 ulp, milliseconds instead of host seconds shared by all ranks."""
+(generate.py's policy, n = 100k, where the Hamiltonian itself comes from the
+device generator) the start block is drawn on the device: bit-exact words,
+Box-Muller within ~1 ulp."""
 
 from __future__ import annotations
 
@@ -53,28 +53,28 @@ def _normals_serial(seed: int, count: int, start_index: int) -> np.ndarray:
 
 
 _PARALLEL_MIN = 1 << 20
+_CHUNK = 1 << 16  # normals per task: the ~10 temporaries of one task stay in L2
 
 
 def complex_normals(seed: int, count: int, start_index: int = 0, threads: int | None = None) -> np.ndarray:
     """Normals start_index .. start_index+count-1.  Large draws are split into
-    counter ranges computed on all host cores (numpy ufuncs release the GIL);
-    the stream is counter based, so the bits do not depend on the split
-    (tests/test_lib_cpu.py checks this)."""
+    cache-sized counter ranges computed on all host cores (numpy ufuncs release
+    the GIL); the stream is counter based, so the bits do not depend on the
+    split (tests/test_lib_cpu.py checks this)."""
     if count < _PARALLEL_MIN:
         return _normals_serial(seed, count, start_index)
     import os
     from concurrent.futures import ThreadPoolExecutor
 
-    nt = threads or min(32, os.cpu_count() or 1)
+    nt = threads or min(64, os.cpu_count() or 1)
     out = np.empty(count, dtype=np.complex128)
-    edges = np.linspace(0, count, nt + 1).astype(np.int64)
 
-    def work(i):
-        a, b = int(edges[i]), int(edges[i + 1])
+    def work(a):
+        b = min(a + _CHUNK, count)
         out[a:b] = _normals_serial(seed, b - a, start_index + a)
 
     with ThreadPoolExecutor(nt) as ex:
-        list(ex.map(work, range(nt)))
+        list(ex.map(work, range(0, count, _CHUNK)))
     return out
 
 

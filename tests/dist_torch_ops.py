@@ -19,13 +19,47 @@ class TorchOps:
         kc = tile.kc
         return tile.buf[:kc].T, tile.buf[kc:2 * kc].T  # (mr x kc) A_t, B_t
 
-    def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
-            p=None, low_sign=1.0, filter=False):
-        mr, kc = tile.mr, tile.kc
+    # real-split storage (csrc/hop_rs.cuh): planes Z, V, U, W of a tile, one (4 kc, ldg) float64 storage
+    def make_rs_planes(self, tile):
         at, bt = self._mat(tile)
+        mr, kc = tile.mr, tile.kc
+        ldg = mr + (mr & 1)
+        g = torch.zeros((4 * kc, ldg), dtype=torch.float64)
+        gm = g.t()
+        for q, pl in enumerate((at.imag + bt.imag, at.real - bt.real, at.real + bt.real, at.imag - bt.imag)):
+            gm[:mr, q * kc:(q + 1) * kc] = pl
+        return g, ldg
+
+    @staticmethod
+    def _rs_product(tile, xf, yf):
+        """folded product: forward x' = i Z x + V y, y' = U x + i W y; transposed (same planes)
+        x' = -i W^T x + V^T y, y' = U^T x - i Z^T y."""
+        gm = tile.g.t()
+        if tile.trans:
+            rows, cols = tile.kc, tile.mr  # the planes' own shape
+            z, v, u, w = (gm[:rows, q * cols:(q + 1) * cols].to(torch.complex128) for q in range(4))
+            return -1j * (w.T @ xf) + v.T @ yf, u.T @ xf - 1j * (z.T @ yf)
+        z, v, u, w = (gm[:tile.mr, q * tile.kc:(q + 1) * tile.kc].to(torch.complex128) for q in range(4))
+        return 1j * (z @ xf) + v @ yf, u @ xf + 1j * (w @ yf)
+
+    def rs_fold(self, v, rows, scale, scale2=None, out=None):
+        out = v if out is None else out
+        s2 = scale if scale2 is None else scale2
+        x1, x2 = v[:, :rows].clone(), v[:, rows:2 * rows].clone()
+        out[:, :rows] = scale * (x1 + x2)
+        out[:, rows:2 * rows] = s2 * (x1 - x2)
+
+    def hop(self, tile, x, y, *, alpha=1.0, shift=0.0, shift_col=None, shift_rows=(0, 0), s_off=0, beta=0.0,
+            p=None, low_sign=1.0, filter=False, rs=False):
+        mr, kc = tile.mr, tile.kc
         x1, x2 = x[:, :kc].T, x[:, kc:2 * kc].T
-        up = at @ x1 + bt @ x2
-        low = -(at.conj() @ x2 + bt.conj() @ x1)
+        if rs:
+            assert low_sign == 1.0
+            up, low = self._rs_product(tile, x1, x2)
+        else:
+            at, bt = self._mat(tile)
+            up = at @ x1 + bt @ x2
+            low = -(at.conj() @ x2 + bt.conj() @ x1)
         lo, hi = shift_rows
         if (shift != 0.0 or shift_col is not None) and hi > lo:
             sh = shift_col[None, :] if shift_col is not None else shift
@@ -62,7 +96,7 @@ class TorchOps:
 
     def c64_step(self, pplanes, tile, k, x, out, *, alpha, shift, shift_rows, s_off, beta=0.0, prev=None):
         y = torch.empty((k, 2 * tile.mr), dtype=torch.complex128)
-        self.hop(tile, x.to(torch.complex128), y, alpha=alpha, shift=shift, shift_rows=shift_rows, s_off=s_off,
+        self.hop(pplanes, x.to(torch.complex128), y, alpha=alpha, shift=shift, shift_rows=shift_rows, s_off=s_off,
                  beta=beta, p=prev.to(torch.complex128) if prev is not None else None)
         self.c64_raw_view(out, tile.mr, k).copy_(y.to(torch.complex64))
 

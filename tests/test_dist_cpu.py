@@ -21,7 +21,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, key, pq, out):
+def _worker(rank, world, port, key, pq, out, planes=None):
     import torch.distributed as dist
     from dist_torch_ops import TorchOps
     from paper_2601_10557_b200 import SolverConfig
@@ -38,7 +38,11 @@ def _worker(rank, world, port, key, pq, out):
     from paper_2601_10557_b200.dist import DistSolver
 
     DistSolver.CHUNK_MIN = 4  # exercise the column-chunked filter pipeline on the small cases
-    res = solve_distributed((a, b), SolverConfig(**kw), device=torch.device("cpu"), grid=grid, ops=TorchOps())
+    from paper_2601_10557_b200.dist import DistributedSolver as DS
+
+    ds = DS((a, b), device=torch.device("cpu"), grid=grid, ops=TorchOps(), planes=planes)
+    assert ds.planes == (planes is not False and not ds.flags & 1)  # B = 0 keeps the complex tiles
+    res = ds.solve(SolverConfig(**kw))
     if rank == 0:
         np.savez(out, lambdas=res.lambdas, v=res.v.numpy(), res=res.residual_norms, iters=res.iterations_used,
                  converged=res.converged, locked=[t.locked for t in res.trace], k=[t.k for t in res.trace],
@@ -47,12 +51,17 @@ def _worker(rank, world, port, key, pq, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,pq,key", [(1, None, "m48_s12"), (2, None, "m48_s12"), (4, None, "m64_s21"),
-                                          (2, (2, 1), "m24_s100"), (4, (1, 4), "m32_s14"), (8, None, "m64_s40"),
-                                          (2, None, "m32_s6"), (4, None, "m32_s6")])
-def test_distributed_solve_matches_reference(tmp_path, world, pq, key):
+@pytest.mark.parametrize("world,pq,key,planes", [
+    (1, None, "m48_s12", None), (2, None, "m48_s12", None), (4, None, "m64_s21", None),
+    (2, (2, 1), "m24_s100", None), (4, (1, 4), "m32_s14", None), (8, None, "m64_s40", None),
+    (2, None, "m32_s6", None), (4, None, "m32_s6", None), (8, None, "m48_s13", None),
+    # complex tiles + block transposes (B = 0 storage) on B != 0 inputs
+    (4, None, "m64_s21", False), (8, None, "m48_s12", False)])
+def test_distributed_solve_matches_reference(tmp_path, world, pq, key, planes):
+    """planes=None: the default real-split storage (one tile's planes per rank, the transposed
+    product read from them); False: complex tiles.  Same bar as the single-GPU golden solves."""
     out = str(tmp_path / "r.npz")
-    mp.spawn(_worker, args=(world, _port(), key, pq, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _port(), key, pq, out, planes), nprocs=world, join=True)
     r = np.load(out)
     g = golden(f"solve_{key}.npz")
     assert bool(r["converged"]) == bool(g["converged"])
@@ -124,3 +133,49 @@ def test_distributed_c64_filter_matches_fp64(tmp_path, world):
     f128, f64 = r["f128"], r["f64"]
     err = np.abs(f64 - f128).max(axis=1) / np.abs(f128).max(axis=1)
     assert err.max() <= 2e-5, err.max()
+
+
+def _phase_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from dist_torch_ops import TorchOps
+    from paper_2601_10557_b200 import rng
+    from paper_2601_10557_b200.dist import DistributedSolver, start_block_col
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.set_num_threads(1)
+    a, b = golden_ham(48, 12)
+    ops = TorchOps()
+    ds = DistributedSolver((a, b), device=torch.device("cpu"), ops=ops)
+    g = ds.inner.g
+    q = start_block_col(rng.substream(4, 3), 96, 9, g, ops)
+    q[:, :2] = 0.0  # leading zero rows of this rank's upper-half slice: the "first" entry moves
+    q[5] = 0.0  # a zero column stays untouched
+    ds.inner.fix_phases(q)
+    full = ds.inner.assemble_from_col(q)
+    if rank == 0:
+        np.save(out, full.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_distributed_phase_convention(tmp_path, world):
+    """dist.DistSolver.fix_phases == ortho.py:70-82 on the assembled block (first entry with
+    |q| >= 1e-8 max|q| in global row order made real positive; zero columns untouched)."""
+    from oracle import bse_oracle as o
+    from paper_2601_10557_b200 import rng
+
+    out = str(tmp_path / "q.npy")
+    mp.spawn(_phase_worker, args=(world, _port(), out), nprocs=world, join=True)
+    got = np.load(out).T
+    raw = rng.complex_normal_matrix(rng.substream(4, 3), 96, 9)
+    from paper_2601_10557_b200.dist import Grid
+
+    ref_in = raw.copy()  # the same input, assembled: each rank zeroed 2 rows of its upper slice
+    for r in range(world):
+        gr = Grid(48, world, r)
+        ref_in[gr.c0:min(gr.c0 + 2, gr.c1)] = 0.0
+    ref_in[:, 5] = 0.0
+    ref = o.phase_fix(ref_in)
+    assert np.abs(got - ref).max() <= 1e-15

@@ -77,7 +77,7 @@ def test_dist_c64_filter_matches_single_gpu_c64():
         filter_inplace(ham, single, fcfg)
     finally:
         _lib.set_filter_precision(prec)
-    ds = DistributedSolver((a, b), device=dev)
+    ds = DistributedSolver((a, b), device=dev, planes=False)  # c64 planes from the exact complex tiles
     vd = v0.T.contiguous()  # (k, n) storage = col layout at world 1
     ds.inner.chebyshev_c64(vd, fcfg)
     assert torch.equal(vd.T.cpu(), single.cpu())
@@ -110,3 +110,58 @@ def test_dist_c64_filter_b_zero(monkeypatch, pair):
     ds.inner.chebyshev(v128, fcfg, ds.inner.ops.empty(k, 128))
     err = ((v64 - v128).abs().amax(dim=1) / v128.abs().amax(dim=1)).max().item()
     assert err <= 2e-5, err
+
+
+@pytest.mark.parametrize("mr,kc,k", [(203, 157, 530), (157, 203, 100), (64, 64, 33), (9, 5, 1)])
+def test_transposed_rs_product_from_forward_planes(mr, kc, k):
+    """bse_hop_tile_rs_t on the planes of (A, B)[R, C] is BITWISE the forward real-split product on
+    the planes of the explicit block transpose (A^H, B^T)[C, R] (Z' = -W^T, V' = V^T, U' = U^T,
+    W' = -Z^T; hop_rs.cuh): the grid's row -> col step needs no second copy of the operator.
+    Ragged shapes, both CTA tiles (k >= 512 / < 512), shift rows, beta term."""
+    from paper_2601_10557_b200.dist import CudaOps, Tile, plane_tiles, tile_from_blocks
+
+    dev = torch.device("cuda", 0)
+    ops = CudaOps(dev)
+    ops.ctx.set_ham_flags(0)
+    gen = torch.Generator(device=dev).manual_seed(mr * 7 + kc)
+
+    def rnd(*shape):
+        return torch.complex(torch.randn(*shape, generator=gen, device=dev, dtype=torch.float64),
+                             torch.randn(*shape, generator=gen, device=dev, dtype=torch.float64))
+
+    a_t, b_t = rnd(mr, kc), rnd(mr, kc)  # any tile of a hermitian A / symmetric B
+    fwd, trn = plane_tiles(ops, tile_from_blocks(ops, a_t, b_t))
+    ref_f, _ = plane_tiles(ops, tile_from_blocks(ops, a_t, b_t, transpose=True))  # explicit transpose
+    assert (trn.mr, trn.kc) == (kc, mr) and trn.trans and trn.g is fwd.g
+    x = rnd(k, 2 * mr)  # folded input rows of the transposed product (contraction mr)
+    p = rnd(k, 2 * kc)
+    lo, hi = (2, min(mr, kc) - 1)
+    out = {}
+    for name, tile in (("trans", trn), ("explicit", ref_f)):
+        y = torch.zeros(k, 2 * kc, dtype=torch.complex128, device=dev)
+        ops.hop(tile, x, y, alpha=0.75, shift=3.5, shift_rows=(lo, hi), s_off=1, beta=0.25, p=p, filter=True,
+                rs=True)
+        out[name] = y
+    torch.cuda.synchronize()
+    assert torch.equal(out["trans"], out["explicit"])
+    # and against the complex definition: x' = i Z' x + V' y, y' = U' x + i W' y with the transpose's planes
+    at, bt = a_t.conj().T, b_t.T
+    z, v, u, w = at.imag + bt.imag, at.real - bt.real, at.real + bt.real, at.imag - bt.imag
+    xf, yf = x[:, :mr].T, x[:, mr:].T
+    up = 1j * (z.to(xf.dtype) @ xf) + v.to(xf.dtype) @ yf
+    low = u.to(xf.dtype) @ xf + 1j * (w.to(xf.dtype) @ yf)
+    up[lo:hi] -= 3.5 * xf[lo + 1:hi + 1]
+    low[lo:hi] -= 3.5 * yf[lo + 1:hi + 1]
+    ref = torch.cat([0.75 * up - 0.25 * p[:, :kc].T, 0.75 * low - 0.25 * p[:, kc:].T]).T
+    err = (out["trans"] - ref).abs().max().item() / ref.abs().max().item()
+    assert err <= 1e-13, err
+
+
+def test_grid_storage_is_one_tile_of_planes():
+    """The real-split grid storage: one tile's planes per GPU (32 mr kc bytes), no complex tile."""
+    from paper_2601_10557_b200.dist import DistributedSolver
+
+    a, b = golden_ham(64, 21)
+    ds = DistributedSolver((a, b), device=torch.device("cuda", 0))
+    assert ds.planes and ds.fwd.buf is None and ds.trn.buf is None and ds.trn.g is ds.fwd.g
+    assert ds.operator_bytes() == 4 * 64 * 64 * 8

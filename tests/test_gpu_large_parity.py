@@ -1,0 +1,98 @@
+"""Parity at the large BASELINE configs against the REFERENCE itself.
+
+``tests/golden/large_c2.npz`` / ``large_c3.npz`` hold the result of the
+reference ``bsesolve.solve`` (run in the build container by
+``oracle/make_golden_large.py`` on the reference's own instance, generate.py:
+60-83) at C2 (n = 20k, nev 500, nex 100) and C3 (n = 40k, nev 1000, nex 200),
+deg 20, tol 1e-10 relative, seed 0.  Here the GPU generator rebuilds the same
+instance and the GPU solver runs the same configuration.
+
+Bars (BASELINE.json north_star):
+  * construction scalars lambda_min(A) / ||B0||_2 and A, B probes match the
+    reference's (eigensolver / GEMM roundoff only);
+  * every eigenvalue within 1e-10 relative;
+  * iterations equal (north star allows +-1) and, when equal, the locking
+    trace (locked, k, flops per iteration) identical;
+  * every residual below tol * |mu_1|;
+  * the stored Ritz vectors equal up to a phase (|v_ref^H v| >= 1 - 1e-8).
+"""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _load(cfg):
+    p = GOLDEN / f"large_{cfg}.npz"
+    if not p.exists():
+        pytest.skip(f"{p.name} not generated (oracle/make_golden_large.py {cfg})")
+    return np.load(p, allow_pickle=False)
+
+
+def _rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def check_instance(ham, g):
+    """The GPU-built instance is the reference's (generate.py:63-74)."""
+    info = ham.construction
+    assert info["exact"]
+    # eigvalsh(A)[0]: both sides backward stable, |dlam| <~ eps ||A|| (||A|| ~ 4m, lambda_min ~ 1)
+    assert abs(info["lambda_min_a"] - float(g["lambda_min_a"])) <= 1e-15 * 8 * int(g["m"]) * 10
+    assert abs(info["b0_norm"] - float(g["b0_norm"])) <= 1e-13 * float(g["b0_norm"])  # svdvals(B0)[0]
+    ab = ham.device_blocks()
+    m = int(g["m"])
+    dev = ab.device
+    probe = torch.from_numpy(np.asfortranarray(g["probe"])).to(dev)
+    a_p = (ab[:, :m] @ probe).cpu().numpy()
+    b_p = (ab[:, m:] @ probe).cpu().numpy()
+    assert _rel(a_p, g["a_probe"]) <= 1e-13  # C C^H summation order
+    assert _rel(b_p, g["b_probe"]) <= 1e-13
+    assert _rel(torch.real(torch.diagonal(ab[:, :m])).cpu().numpy(), g["a_diag"]) <= 1e-14
+    assert _rel(ab[0, m:].cpu().numpy(), g["b_row0"]) <= 1e-14
+    assert _rel(ab[:, 1].cpu().numpy(), g["a_col1"]) <= 1e-14
+    assert _rel(ab[:, m + 1].cpu().numpy(), g["b_col1"]) <= 1e-14
+
+
+def check_result(res, g):
+    ref_l = g["lambdas"]
+    rel = np.abs(res.lambdas - ref_l) / np.abs(ref_l)
+    out = {"max_dlambda_rel": float(rel.max()), "iterations": res.iterations_used,
+           "iterations_ref": int(g["iterations_used"])}
+    assert res.converged and bool(g["converged"])
+    assert rel.max() <= 1e-10
+    assert abs(res.iterations_used - int(g["iterations_used"])) <= 1
+    if res.iterations_used == int(g["iterations_used"]):
+        assert [t.locked for t in res.trace] == list(g["trace_locked"])
+        assert [t.k for t in res.trace] == list(g["trace_k"])
+        np.testing.assert_allclose([t.flops for t in res.trace], g["trace_flops"], rtol=1e-15)
+    assert abs(res.bounds.mu_1 - float(g["mu_1"])) <= 1e-12 * abs(float(g["mu_1"]))
+    assert res.residual_norms.max() <= float(g["tol"]) * abs(res.bounds.mu_1)
+    v = res.v if isinstance(res.v, np.ndarray) else res.v.T.contiguous().cpu().numpy().T
+    for ref, got in ((g["v_first4"], v[:, :4]), (g["v_last4"], v[:, -4:])):
+        ov = np.abs(np.einsum("ij,ij->j", ref.conj(), got))
+        assert np.abs(ov - 1).max() <= 1e-8, ov
+    return out
+
+
+@pytest.fixture(scope="module")
+def bse():
+    assert torch.cuda.is_available(), "GPU test without a GPU"
+    import paper_2601_10557_b200 as m
+
+    return m
+
+
+def test_c2_parity_against_reference(bse):
+    """C2 (BASELINE.json configs[1]): n = 20k, nev 500, nex 100 on 1 GPU."""
+    g = _load("c2")
+    ham = bse.generate(bse.GeneratorSpec(m=int(g["m"]), seed=0))
+    check_instance(ham, g)
+    cfg = bse.SolverConfig(nev=int(g["nev"]), nex=int(g["nex"]), deg=int(g["deg"]), tol=float(g["tol"]),
+                           seed=int(g["seed"]), rel_res=bool(g["rel_res"]))
+    res = bse.solve(ham, cfg)
+    check_result(res, g)
