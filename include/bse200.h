@@ -103,6 +103,11 @@ int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t mr, 
  * this d_ab run on the real-split kernel (fold Q, product, unfold with the S-flip).  d_g = NULL
  * clears the registration (the Python layer scopes it to one RR call).                          */
 int bse_set_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t m, const void* d_g, int64_t ldg);
+/* Register a device buffer of 4 k^2 complex128 + k doubles that the next bse_rr_hermitian /
+ * bse_rr_backup calls fill with their reduced problem (rayleigh_ritz.py:41-51, 140-143, 176-179):
+ * [W | L (lower triangle; upper = W's) | M | G] column-major k x k each, then d (backup only).
+ * NULL clears it; the solver loop never registers one (no copies on the hot path).             */
+int bse_set_rr_capture(bse_ctx* ctx, void* d_buf);
 /* bse_chebyshev_filter (chebyshev.py:51-75) on the real-split planes: the block is folded to
  * (X1 + X2, X1 - X2), where H acts through four real m x m planes (4 n^2 k executed flops per
  * step instead of 6 n^2 k for 3M), filtered, and unfolded.  Same arguments and results as

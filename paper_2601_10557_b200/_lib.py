@@ -83,6 +83,7 @@ _SIGS = {
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
     "bse_hop_tile_rs": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
     "bse_hop_tile_rs_t": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
+    "bse_set_rr_capture": (C.c_int, [_vp, _vp]),
     "bse_rs_fold": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _dbl, _dbl]),
     "bse_c64_tile_planes": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_c64_tile_step": (C.c_int, [_vp, C.POINTER(C64TileArgs)]),

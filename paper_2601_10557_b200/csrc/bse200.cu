@@ -45,6 +45,8 @@ struct bse_ctx {
   const void* rs_ab = nullptr;
   const double* rs_g = nullptr;
   int64_t rs_ldg = 0, rs_m = 0;
+  // optional capture of the RR's k x k reduced problem (bse_set_rr_capture): [W | L | M | G] + d
+  zval* rr_capture = nullptr;
   size_t ws_bytes = 0;
   void* hws = nullptr;  // host scratch (cuSOLVER 64-bit API)
   size_t hws_bytes = 0;
@@ -749,6 +751,13 @@ int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scra
   return 1;
 }
 
+// copy one k x k factor into slot `slot` of the registered capture buffer (no-op when none)
+void capture_kk(bse_ctx* ctx, int slot, const zval* src, int64_t k) {
+  if (!ctx->rr_capture) return;
+  CUDA_OK(cudaMemcpyAsync(ctx->rr_capture + (size_t)slot * k * k, src, (size_t)k * k * sizeof(zval),
+                          cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
 size_t pencil_ws_bytes(int64_t k) { return 3 * al((size_t)k * k * sizeof(zval)) + al(k * 8) + al(k * 4) + al(64); }
 
 // Small hermitian pencil of the oblique RR (rayleigh_ritz.py:113-137) on k x k device data:
@@ -772,6 +781,8 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   check_launch(ctx);
   bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
   check_launch(ctx);
+  capture_kk(ctx, 0, w, k);
+  capture_kk(ctx, 2, mm, k);
   std::vector<double> hw(k);
   if (mode != 2) {
     // :116-120  |lambda|_min(M) >= 1e-8
@@ -789,6 +800,7 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   // :121-126  L = chol(W)
   if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0)
     throw BseError(BSE_EHERMITIAN_RQ, "Cholesky of Q*SHQ failed; S*H is not definite on the subspace");
+  capture_kk(ctx, 1, w, k);  // L in the lower triangle (the caller drops the upper)
   // :127-129  G = L^{-1} M L^{-H}, hermitised
   const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
   CUDA_OK(cudaMemcpyAsync(g, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
@@ -798,6 +810,7 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
                       (int)k, &z1, cz(w), (int)k, cz(g), (int)k));
   bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k);
   check_launch(ctx);
+  capture_kk(ctx, 3, g, k);
   tm.mark("chol(W), G = L^-1 M L^-H", k);
   // :130-133  theta, y = eigh(G); lambda = 1/theta
   heevd(ctx, g, (int)k, d_w, true, d_info);
@@ -1058,6 +1071,10 @@ int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t mr, 
   });
 }
 
+int bse_set_rr_capture(bse_ctx* ctx, void* d_buf) {
+  return guarded(ctx, [&] { ctx->rr_capture = static_cast<zval*>(d_buf); });
+}
+
 int bse_set_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t m, const void* d_g, int64_t ldg) {
   return guarded(ctx, [&] {
     if (d_g && (m <= 0 || ldg < m || (ldg & 1))) throw BseError(BSE_EVALIDATION, "bad shapes (ldg must be even, >= m)");
@@ -1284,12 +1301,17 @@ void backup_pencil(bse_ctx* ctx, zval* g, const zval* w, zval* g2, int64_t k, do
   if (h_lam_min_m) *h_lam_min_m = lmm;
   bse::diag_real_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(mm, (int)k, 1e-12, d_d);
   check_launch(ctx);
+  capture_kk(ctx, 0, w, k);
+  capture_kk(ctx, 2, mm, k);
+  if (ctx->rr_capture)
+    CUDA_OK(cudaMemcpyAsync(ctx->rr_capture + 4 * kk, d_d, k * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
   bse::offdiag_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, tmp, (int)k);
   check_launch(ctx);
   // g = (g0 - off W) / d
   zgemm<bse::OPA_N>(ctx, k, k, k, -1.0, tmp, k, w, k, 1.0, g, k, gws);
   bse::rowscale_inv_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g, (int)k, d_d);
   check_launch(ctx);
+  capture_kk(ctx, 3, g, k);
   // direct.py:102-116: general eigensolver, ascending real parts (stable)
   size_t dws = 0, hws = 0;
   SOLVER_OK(cusolverDnXgeev_bufferSize(ctx->solver, ctx->params, CUSOLVER_EIG_MODE_NOVECTOR, CUSOLVER_EIG_MODE_VECTOR,

@@ -28,8 +28,10 @@ DIAG_ZERO_TOL = 1e-12
 
 @dataclass
 class ReducedProblem:
-    """Reduced-problem record (rayleigh_ritz.py:41-51).  The k x k factors stay
-    on the device; only the variant and |lambda|_min(Q*SQ) come back."""
+    """Reduced-problem record (rayleigh_ritz.py:41-51).  Inside the solver loop the k x k
+    factors stay on the device (only the variant and |lambda|_min(Q*SQ) come back); the public
+    build_hermitian_rq / build_backup_rq fill w, l, m, g (and d for the backup) as host arrays, as
+    the reference returns them (rayleigh_ritz.py:140-143, 176-179)."""
 
     variant: str
     w: object = None
@@ -54,7 +56,8 @@ class RitzSet:
         return self.values.shape[0]
 
 
-def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residuals: bool = False):
+def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residuals: bool = False,
+        capture: bool = False):
     n, k = q.shape
     lam = np.zeros(k)
     vout = colmajor_empty(n, k, q.device)
@@ -68,6 +71,12 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     ctx = _lib.Context.get(q.device.index)
     res = np.zeros(k) if fused_residuals else None
     extra = (_lib.hptr(res) if fused_residuals else None,) if entry == "bse_rr_hermitian" else ()
+    cap = None
+    if capture:
+        import torch
+
+        cap = torch.zeros(4 * k * k + (k + 1) // 2, dtype=torch.complex128, device=q.device)
+        ctx.call("bse_set_rr_capture", _lib.dptr(cap))
     try:
         if g is not None:
             ctx.call("bse_set_rs_planes", _lib.dptr(ab), ham.m, _lib.dptr(g), g.stride(1))
@@ -76,6 +85,8 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     finally:
         if g is not None:
             ctx.call("bse_set_rs_planes", None, 0, None, 0)
+        if cap is not None:
+            ctx.call("bse_set_rr_capture", None)
         if ledger is not None:
             # apply_h inside RR charges 8n^2k to "rr" (hamiltonian.py:148-150) before the model of
             # rayleigh_ritz.py:139 / :175 — the reference ledger counts both, so do we
@@ -83,7 +94,17 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
     if ledger is not None:
         extra = (12.0 * n * k * k + 16.0 * k**3) if variant == "hermitian" else (20.0 * n * k * k + 30.0 * k**3)
         ledger.add_flops("rr", 8.0 * n * n * k + extra)
-    return RitzSet(values=lam, vectors=vout, residual_norms=res), ReducedProblem(variant=variant, lambda_min_m=lmm.value)
+    red = ReducedProblem(variant=variant, lambda_min_m=lmm.value)
+    if cap is not None:
+        host = cap.cpu().numpy()
+        kk = k * k
+        w_, l_, m_, g_ = (host[i * kk:(i + 1) * kk].reshape(k, k, order="F") for i in range(4))
+        red.w, red.m, red.g = w_.copy(), m_.copy(), g_.copy()
+        if variant == "hermitian":
+            red.l = np.tril(l_)
+        else:
+            red.d = host[4 * kk:].view(np.float64)[:k].copy()
+    return RitzSet(values=lam, vectors=vout, residual_norms=res), red
 
 
 def build_hermitian_rq_device(ham, q, ledger=None, fused_residuals: bool = False):
@@ -96,22 +117,22 @@ def build_backup_rq_device(ham, q, ledger=None):
     return _rr("bse_rr_backup", "backup", ham, q, ledger)
 
 
-def _public(fn, ham, q_active, ledger):
+def _public(entry, variant, ham, q_active, ledger):
     dev = _device_for(q_active)
     q = to_colmajor(q_active, dev)
-    ritz, red = fn(ham, q, ledger)
+    ritz, red = _rr(entry, variant, ham, q, ledger, capture=True)
     ritz.vectors = _host_like(q_active, ritz.vectors)
     return ritz, red
 
 
 def build_hermitian_rq(ham: BseHamiltonian, q_active, ledger: PhaseLedger | None = None):
     """Hermitian-equivalent projection (rayleigh_ritz.py:98-143)."""
-    return _public(build_hermitian_rq_device, ham, q_active, ledger)
+    return _public("bse_rr_hermitian", "hermitian", ham, q_active, ledger)
 
 
 def build_backup_rq(ham: BseHamiltonian, q_active, ledger: PhaseLedger | None = None):
     """Non-hermitian backup projection (rayleigh_ritz.py:146-179)."""
-    return _public(build_backup_rq_device, ham, q_active, ledger)
+    return _public("bse_rr_backup", "backup", ham, q_active, ledger)
 
 
 def residuals_device(ham: BseHamiltonian, values: np.ndarray, vectors, ledger=None) -> np.ndarray:

@@ -63,7 +63,7 @@ def main(m, k, l):
     print(f"  grams + rr_pencil:        {wall(pencil):.1f} ms")
     wk = w.clone()
     print(f"  eigvalsh k x k:           {wall(lambda: ctx.call('bse_eigvalsh', _lib.dptr(wk), k, k, _lib.hptr(lam))):.1f} ms")
-    for alg in ("4m", "3m", "3m-onthefly"):
+    for alg in ("4m", "3m", "rs"):
         bse.set_filter_algorithm(alg)
         sdp = _lib.dptr(ham.device_sum_planes(dev)) if alg == "3m" else None
         yp = v0.clone()

@@ -63,7 +63,7 @@ def whole_filter(m, ks, codes, deg=4):
         work = torch.empty(2 * n * k, dtype=torch.complex128, device=dev)
         for code in codes:
             ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
-            sdp = _lib.dptr(sd) if code in (65, 72, 82, 86, 88) else None
+            sdp = _lib.dptr(sd) if code in (82, 86, 88) else None
             ms = timed(lambda: ctx.call("bse_chebyshev_filter", _lib.dptr(ab), sdp, ld_of(ab), m, _lib.dptr(v), n, k,
                                         deg, 0.0, 1.0, -1.5, _lib.dptr(work)), 2)
             print(f"filter deg={deg} m={m} k={k} code={code}: {ms / deg:8.2f} ms/step  model "
