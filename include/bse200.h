@@ -127,6 +127,16 @@ int bse_residuals(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const 
  * *h_method = 0 cholqr2, 1 shifted fallback.  BSE_ERANK on rank deficiency. */
 int bse_s_orthonormalize(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t ldv, const void* d_ylocked,
                          int64_t l, int64_t ldy, int* h_method);
+/* Incremental basis of span(S Y_locked): S-flip the c newly locked columns d_ynew into
+ * basis[:, l_old:l_old+c], project them twice against basis[:, :l_old] and CholQR them (the
+ * reference re-QRs the whole flipped locked block every iteration, ortho.py:149-150; same span). */
+int bse_extend_sbasis(bse_ctx* ctx, void* d_basis, int64_t n, int64_t ldb, int64_t l_old, const void* d_ynew,
+                      int64_t ldy, int64_t c);
+/* ortho.py:132-158 with the locked space given by that orthonormal basis (n x l, leading dim
+ * ldb): projection, CholQR2 with the shifted fallback, phase convention; h_method as
+ * bse_s_orthonormalize.                                                                       */
+int bse_s_orthonormalize_basis(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t ldv, const void* d_basis,
+                               int64_t l, int64_t ldb, int* h_method);
 int bse_cholqr(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq, int* h_method);
 /* column phase convention alone (fix_column_phases, ortho.py:70-82) */
 int bse_fix_phases(bse_ctx* ctx, void* d_q, int64_t n, int64_t k, int64_t ldq);

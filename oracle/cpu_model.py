@@ -49,19 +49,32 @@ def _block(seed, n, k):
     return o.gauss_c_matrix(seed, n, k)
 
 
+REPS = 3  # every phase is timed REPS times and the median kept
+
+
+def _best(fn, reps=REPS):
+    ts = []
+    for _ in range(reps):
+        t0 = _now()
+        fn()
+        ts.append(_now() - t0)
+    return float(np.median(ts))
+
+
 def _filter_steps(a, b, k, c, e, s):
-    """Two recurrence steps (one plain, one adjoint product), chebyshev.py:70-74."""
+    """Recurrence steps with the plain and the adjoint product (chebyshev.py:62-74); seconds per
+    step (median of REPS pairs)."""
     n = 2 * a.shape[0]
-    y_old = _block(11, n, k)
-    y = _block(12, n, k)
+    st = {"y_old": _block(11, n, k), "y": _block(12, n, k), "sig": e / (s - c)}
     sig1 = e / (s - c)
-    sig = sig1
-    t0 = _now()
-    for prod in (o.h_times, o.h_times_adjoint):
-        sn = 1.0 / (2.0 / sig1 - sig)
-        y_new = (2.0 * sn / e) * (prod(a, b, y) - c * y) - (sig * sn) * y_old
-        y_old, y, sig = y, y_new, sn
-    return (_now() - t0) / 2.0
+
+    def pair():
+        for prod in (o.h_times, o.h_times_adjoint):
+            sn = 1.0 / (2.0 / sig1 - st["sig"])
+            y_new = (2.0 * sn / e) * (prod(a, b, st["y"]) - c * st["y"]) - (st["sig"] * sn) * st["y_old"]
+            st["y_old"], st["y"], st["sig"] = st["y"], y_new / np.abs(y_new).max(), sn
+
+    return _best(pair) / 2.0
 
 
 def _orthonormal(n, k, seed):
@@ -77,7 +90,7 @@ def calibrate(a, b, k_hi: int, k_lo: int, l_hi: int, *, bounds=(-1.0, 0.5, 1.0))
     c, e = (mu_n + cut) / 2.0, (mu_n - cut) / 2.0
     t = {"n": n, "k_hi": k_hi, "k_lo": k_lo, "l_hi": l_hi, "cores": _cores(),
          "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
-    o.h_times(a[:64, :64], b[:64, :64], _block(1, 128, 2))  # BLAS thread pool up
+    o.h_times(a, b, _block(1, n, min(k_lo, 64)))  # BLAS threads and buffers up at the full size
     t0 = _now()
     for k in (k_lo, k_hi):
         t[f"step_{k}"] = _filter_steps(a, b, k, c, e, mu_1)
@@ -87,34 +100,24 @@ def calibrate(a, b, k_hi: int, k_lo: int, l_hi: int, *, bounds=(-1.0, 0.5, 1.0))
     # ortho pieces (ortho.py:132-158)
     v_lo = _block(22, n, k_lo)
     locked = _orthonormal(n, l_hi, 23)
-    t1 = _now()
-    basis, _ = np.linalg.qr(o.s_flip(locked))
-    t["qr_l"] = _now() - t1
-    t1 = _now()
-    _ = v_hi - basis @ (basis.conj().T @ v_hi)
-    t["proj_l_khi"] = _now() - t1
+    res = {}
+    t["qr_l"] = _best(lambda: res.__setitem__("basis", np.linalg.qr(o.s_flip(locked))[0]))
+    basis = res["basis"]
+    t["proj_l_khi"] = _best(lambda: v_hi - basis @ (basis.conj().T @ v_hi))
     for k, v in ((k_lo, v_lo), (k_hi, v_hi)):
-        t1 = _now()
-        o.cholqr2(v)
-        t[f"chol_{k}"] = _now() - t1
-    del basis, locked
+        t[f"chol_{k}"] = _best(lambda: o.cholqr2(v))
+    del basis, locked, res
     # Rayleigh-Ritz (rayleigh_ritz.py:98-143) and residuals (:182-190)
     for k, v in ((k_lo, v_lo), (k_hi, v_hi)):
         q, _ = o.cholqr2(v)
-        t1 = _now()
-        lam, vec, _ = o.rr_hermitian(a, b, q)
-        t[f"rr_{k}"] = _now() - t1
+        out = {}
+        t[f"rr_{k}"] = _best(lambda: out.__setitem__("rr", o.rr_hermitian(a, b, q)))
         if k == k_lo:
-            t1 = _now()
-            o.residual_norms(a, b, lam, vec)
-            t[f"res_{k}"] = _now() - t1
+            lam, vec, _ = out["rr"]
+            t[f"res_{k}"] = _best(lambda: o.residual_norms(a, b, lam, vec))
     # Lanczos: one step = one k = 1 H application + S-dots (lanczos.py:53-88)
     x = _block(31, n, 1)[:, 0]
-    t1 = _now()
-    for _ in range(2):
-        g = o.h_times(a, b, x)
-        float(np.real(np.vdot(o.s_flip(g), x)))
-    t["lanczos_step"] = (_now() - t1) / 2.0
+    t["lanczos_step"] = _best(lambda: float(np.real(np.vdot(o.s_flip(o.h_times(a, b, x)), x))), 3)
     t["calibration_s"] = _now() - t0
     return t
 
@@ -165,13 +168,12 @@ def model(cal: dict, trace_k, trace_locked, deg: int, lanczos_steps: int, step_s
 
 
 def sample_step(a, b, k: int) -> float:
-    """A bounded per-bench-step sample: one plain H application with the recurrence arithmetic."""
+    """A bounded per-bench-step sample: one plain H application with the recurrence arithmetic
+    (median of REPS)."""
     n = 2 * a.shape[0]
     y = _block(41, n, k)
     y_old = _block(42, n, k)
-    t0 = _now()
-    _ = 0.5 * (o.h_times(a, b, y) - 0.25 * y) - 0.125 * y_old
-    return _now() - t0
+    return _best(lambda: 0.5 * (o.h_times(a, b, y) - 0.25 * y) - 0.125 * y_old)
 
 
 def _cores() -> int:

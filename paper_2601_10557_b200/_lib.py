@@ -84,6 +84,8 @@ _SIGS = {
     "bse_hop_tile_rs": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
     "bse_hop_tile_rs_t": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
     "bse_set_rr_capture": (C.c_int, [_vp, _vp]),
+    "bse_extend_sbasis": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64]),
+    "bse_s_orthonormalize_basis": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),
     "bse_rs_fold": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _dbl, _dbl]),
     "bse_c64_tile_planes": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "bse_c64_tile_step": (C.c_int, [_vp, C.POINTER(C64TileArgs)]),

@@ -122,6 +122,21 @@ __global__ void sflip_copy_kernel(const zval* __restrict__ x, int64_t ldx, zval*
 }
 
 // g <- (g + g^H) / 2 for a k x k matrix (ld = k); one thread per (i, j) with i <= j
+// hermitian matrix from its upper triangle (GEMM_UPPER Grams): lower = conj(upper), real diagonal
+__global__ void herm_upper_kernel(zval* g, int k) {
+  const int64_t total = (int64_t)k * k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = int(idx % k), j = int(idx / k);
+    if (i > j) continue;
+    const zval a = g[(int64_t)j * k + i];
+    if (i == j) {
+      g[(int64_t)j * k + i] = zval{a.re, 0.0};
+    } else {
+      g[(int64_t)i * k + j] = zval{a.re, -a.im};
+    }
+  }
+}
+
 __global__ void hermitize_kernel(zval* g, int k) {
   const int64_t total = (int64_t)k * k;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {

@@ -560,7 +560,7 @@ size_t gemm_ws_bytes(int64_t M, int64_t N, int64_t K) {
 
 template <int OPA>
 void zgemm(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const zval* a, int64_t lda, const zval* b,
-           int64_t ldb, double beta, zval* c, int64_t ldc, zval* ws) {
+           int64_t ldb, double beta, zval* c, int64_t ldc, zval* ws, int tri = 0) {
   if (M == 0 || N == 0) return;
   using C = GemmMain;
   ensure_smem(ctx, (const void*)bse::zgemm_kernel<C, OPA>, (int)C::SMEM);
@@ -576,6 +576,7 @@ void zgemm(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const zv
   g.K = (int)K;
   g.alpha = alpha;
   g.beta = beta;
+  g.tri = tri;
   const int splits = (K == 0) ? 1 : splitk_for(M, N, K);
   g.ws = ws;
   if (splits > 1 && !ws) throw BseError(BSE_ECUDA, "internal: split-K workspace missing");
@@ -583,7 +584,8 @@ void zgemm(bse_ctx* ctx, int64_t M, int64_t N, int64_t K, double alpha, const zv
   bse::zgemm_kernel<C, OPA><<<grid, C::THREADS, C::SMEM, ctx->stream>>>(g);
   check_launch(ctx);
   if (splits > 1) {
-    bse::zgemm_splitk_reduce<<<grid1d(M * N), 256, 0, ctx->stream>>>(ws, splits, c, ldc, (int)M, (int)N, alpha, beta);
+    bse::zgemm_splitk_reduce<<<grid1d(M * N), 256, 0, ctx->stream>>>(ws, splits, c, ldc, (int)M, (int)N, alpha, beta,
+                                                                     tri);
     check_launch(ctx);
   }
 }
@@ -656,15 +658,20 @@ double defect_to_host(bse_ctx* ctx, const zval* g, int k, double* d_part) {
 // (upper), Q <- Q R^{-1} with R^{-1} from a k x k TRSM and the product on the
 // DMMA GEMM.  gram needs 2 k x k, tmp n x k.  Returns false when the Cholesky
 // factorisation fails (ortho.py:113-119).
+// One CholQR pass: G = Q^H Q (upper triangle only, hermitian by construction -- the reference's
+// (G + G^H)/2, ortho.py:116-117, is then the identity on it), R = chol(G) upper, Q <- Q R^{-1}
+// with the triangular R^{-1} (only the K rows <= column j contribute to column j).  gram holds
+// 3 k x k blocks: [G -> R | R^{-1} | copy of G] (the copy feeds the folded defect check).
 bool cholqr_pass(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, zval* gram, zval* tmp, zval* gws,
                  int* d_info, double shift, double* d_rdiag) {
-  zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
-  bse::hermitize_kernel<<<grid1d(k * k), 256, 0, ctx->stream>>>(gram, (int)k);
+  zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws, bse::GEMM_UPPER);
+  bse::herm_upper_kernel<<<grid1d(k * k), 256, 0, ctx->stream>>>(gram, (int)k);
   check_launch(ctx);
   if (shift != 0.0) {
     bse::add_diag_kernel<<<(int)((k + 255) / 256), 256, 0, ctx->stream>>>(gram, (int)k, shift);
     check_launch(ctx);
   }
+  CUDA_OK(cudaMemcpyAsync(gram + 2 * k * k, gram, (size_t)k * k * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
   const int info = potrf(ctx, gram, (int)k, CUBLAS_FILL_MODE_UPPER, d_info);
   if (info != 0) return false;
   if (d_rdiag) {
@@ -679,14 +686,26 @@ bool cholqr_pass(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, zval*
                       (int)k, &z1, cz(gram), (int)k, cz(rinv), (int)k));
   CUDA_OK(cudaMemcpy2DAsync(tmp, sizeof(zval) * n, q, sizeof(zval) * ldq, sizeof(zval) * n, (size_t)k,
                             cudaMemcpyDeviceToDevice, ctx->stream));
-  zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, tmp, n, rinv, k, 0.0, q, ldq, gws);
+  zgemm<bse::OPA_N>(ctx, n, k, k, 1.0, tmp, n, rinv, k, 0.0, q, ldq, gws, bse::GEMM_B_UPPER);
   return true;
 }
 
+// Orthogonality defect max|Q^H Q - I| of the Q a CholQR pass produced, folded into that pass:
+// Q^H Q = R^{-H} G R^{-1} with G the pass's own (exact) Gram (gram + 2 k^2) and R^{-1}
+// (gram + k^2): two k x k x k products instead of a third n x k x k Gram (ortho.py:124).
+double folded_defect(bse_ctx* ctx, zval* gram, int64_t k, zval* gws, double* dpart) {
+  zval* rinv = gram + k * k;
+  zval* g = gram + 2 * k * k;
+  zval* x = gram;  // R is no longer needed
+  zgemm<bse::OPA_N>(ctx, k, k, k, 1.0, g, k, rinv, k, 0.0, x, k, gws, bse::GEMM_B_UPPER);
+  zgemm<bse::OPA_C>(ctx, k, k, k, 1.0, rinv, k, x, k, 0.0, g, k, gws);
+  return defect_to_host(ctx, g, (int)k, dpart);
+}
+
 size_t cholqr_ws_bytes(int64_t n, int64_t k) {
-  return al(2 * k * k * sizeof(zval)) + 2 * al(n * k * sizeof(zval)) +
-         al(std::max(gemm_ws_bytes(k, k, n), gemm_ws_bytes(n, k, k)) + sizeof(zval)) + al(1024 * 8) + al(k * 8) +
-         al(64) + 4096;
+  return al(3 * k * k * sizeof(zval)) + 2 * al(n * k * sizeof(zval)) +
+         al(std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(n, k, k), gemm_ws_bytes(k, k, k)}) + sizeof(zval)) +
+         al(1024 * 8) + al(k * 8) + al(64) + 4096;
 }
 
 // ortho.py:96-129 on device.  Returns method (0 cholqr2, 1 shifted fallback);
@@ -694,9 +713,10 @@ size_t cholqr_ws_bytes(int64_t n, int64_t k) {
 int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scratch& sc) {
   if (k > n) throw BseError(BSE_ERANK, "cannot orthonormalize " + std::to_string(k) + " columns in dimension " +
                                            std::to_string(n));
-  zval* gram = sc.take<zval>(2 * k * k);
+  zval* gram = sc.take<zval>(3 * k * k);
   zval* tmp = sc.take<zval>(n * k);
-  zval* gws = sc.take<zval>(std::max(gemm_ws_bytes(k, k, n), gemm_ws_bytes(n, k, k)) / sizeof(zval) + 1);
+  zval* gws = sc.take<zval>(std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(n, k, k), gemm_ws_bytes(k, k, k)}) /
+                                sizeof(zval) + 1);
   double* dpart = sc.take<double>(1024);
   double* rdiag = sc.take<double>(k);
   int* d_info = sc.take<int>(4);
@@ -711,9 +731,8 @@ int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scra
     tm.mark("cholqr pass", k);
   }
   if (ok) {
-    zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, q, ldq, 0.0, gram, k, gws);
-    const double defect = defect_to_host(ctx, gram, (int)k, dpart);
-    tm.mark("defect", k);
+    const double defect = folded_defect(ctx, gram, k, gws, dpart);
+    tm.mark("defect (folded into pass 2)", k);
     if (defect <= 1e-8) return 0;  // ortho.py:124-126 (NaN fails the test)
   }
   tm.mark("FALLBACK to shifted CholQR3", k);
@@ -775,11 +794,12 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   double* d_w = sc.take<double>(k);
   int* d_perm = sc.take<int>(k);
   int* d_info = sc.take<int>(4);
-  bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(w, (int)k);
+  // W and Q2^H Q2 are hermitian: their upper triangles (GEMM_UPPER) define them
+  bse::herm_upper_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(w, (int)k);
   check_launch(ctx);
   bse::form_m_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(g2, mm, (int)k);
   check_launch(ctx);
-  bse::hermitize_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
+  bse::herm_upper_kernel<<<grid1d(kk), 256, 0, ctx->stream>>>(mm, (int)k);
   check_launch(ctx);
   capture_kk(ctx, 0, w, k);
   capture_kk(ctx, 2, mm, k);
@@ -1210,6 +1230,67 @@ int bse_s_orthonormalize(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t 
   });
 }
 
+// Incrementally maintained orthonormal basis of span(S Y_locked) (SURVEY.md §7 "Locked basis"): the
+// reference re-runs a Householder QR of the whole n x l flipped locked block every iteration
+// (ortho.py:149-150); the span only grows by the newly locked columns, so they alone are
+// S-flipped, projected twice against the existing basis (block classical Gram-Schmidt, BCGS2) and
+// CholQR'd.  Same span, hence the same projector, to rounding.
+int bse_extend_sbasis(bse_ctx* ctx, void* d_basis, int64_t n, int64_t ldb, int64_t l_old, const void* d_ynew,
+                      int64_t ldy, int64_t c) {
+  return guarded(ctx, [&] {
+    if (n % 2) throw BseError(BSE_EVALIDATION, "S needs an even row count");
+    if (c <= 0) return;
+    if (ldb < n || ldy < n || l_old < 0) throw BseError(BSE_EVALIDATION, "bad shapes");
+    zval* basis = static_cast<zval*>(d_basis);
+    zval* bn = basis + l_old * ldb;
+    const int64_t m = n / 2;
+    size_t need = cholqr_ws_bytes(n, c);
+    if (l_old > 0) need += al(l_old * c * sizeof(zval)) + std::max(gemm_ws_bytes(l_old, c, n), gemm_ws_bytes(n, c, l_old)) + 256;
+    Scratch sc(ctx, need);
+    bse::sflip_copy_kernel<<<grid1d(n * c), 256, 0, ctx->stream>>>(static_cast<const zval*>(d_ynew), ldy, bn, ldb, m,
+                                                                     c);
+    check_launch(ctx);
+    if (l_old > 0) {
+      zval* proj = sc.take<zval>(l_old * c);
+      zval* gws = sc.take<zval>(std::max(gemm_ws_bytes(l_old, c, n), gemm_ws_bytes(n, c, l_old)) / sizeof(zval) + 1);
+      for (int pass = 0; pass < 2; ++pass) {
+        zgemm<bse::OPA_C>(ctx, l_old, c, n, 1.0, basis, ldb, bn, ldb, 0.0, proj, l_old, gws);
+        zgemm<bse::OPA_N>(ctx, n, c, l_old, -1.0, basis, ldb, proj, l_old, 1.0, bn, ldb, gws);
+      }
+    }
+    Scratch rest = sc;
+    cholqr_device(ctx, bn, n, c, ldb, rest);
+  });
+}
+
+// ortho.py:132-158 with the locked space given by its orthonormal basis (bse_extend_sbasis):
+// v <- v - basis (basis^H v), CholQR2 (+ shifted fallback), phase convention.
+int bse_s_orthonormalize_basis(bse_ctx* ctx, void* d_v, int64_t n, int64_t k, int64_t ldv, const void* d_basis,
+                               int64_t l, int64_t ldb, int* h_method) {
+  return guarded(ctx, [&] {
+    if (k == 0) {
+      if (h_method) *h_method = 0;
+      return;
+    }
+    zval* v = static_cast<zval*>(d_v);
+    const zval* basis = static_cast<const zval*>(d_basis);
+    size_t need = cholqr_ws_bytes(n, k);
+    if (l > 0) need += al(l * k * sizeof(zval)) + std::max(gemm_ws_bytes(l, k, n), gemm_ws_bytes(n, k, l)) + 256;
+    Scratch sc(ctx, need);
+    if (l > 0) {
+      zval* proj = sc.take<zval>(l * k);
+      zval* gws = sc.take<zval>(std::max(gemm_ws_bytes(l, k, n), gemm_ws_bytes(n, k, l)) / sizeof(zval) + 1);
+      zgemm<bse::OPA_C>(ctx, l, k, n, 1.0, basis, ldb, v, ldv, 0.0, proj, l, gws);
+      zgemm<bse::OPA_N>(ctx, n, k, l, -1.0, basis, ldb, proj, l, 1.0, v, ldv, gws);
+    }
+    Scratch rest = sc;
+    const int method = cholqr_device(ctx, v, n, k, ldv, rest);
+    bse::phase_fix_kernel<<<(int)k, 256, 0, ctx->stream>>>(v, ldv, n);
+    check_launch(ctx);
+    if (h_method) *h_method = method;
+  });
+}
+
 int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda, int64_t m, const void* d_q,
                      int64_t ldq, int64_t k, double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m,
                      double* h_res) {
@@ -1238,9 +1319,9 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t l
     // rayleigh_ritz.py:112-115: T = S H Q ; W = Q^H T ; Q2^H Q2
     apply_h(ctx, d_ab, lda, m, q, ldq, t, n, k, -1.0, d_sd, fold);
     tm.mark("T = S H Q", k);
-    zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws);
-    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws);
-    tm.mark("grams W, Q2^H Q2", k);
+    zgemm<bse::OPA_C>(ctx, k, k, n, 1.0, q, ldq, t, n, 0.0, w, k, gws, bse::GEMM_UPPER);
+    zgemm<bse::OPA_C>(ctx, k, k, m, 1.0, q + m, ldq, q + m, ldq, 0.0, g2, k, gws, bse::GEMM_UPPER);
+    tm.mark("grams W, Q2^H Q2 (upper triangles)", k);
     Scratch rest = sc;
     rr_pencil(ctx, w, g2, k, h_lam, wvec, h_lam_min_m, rest);
     tm.mark("pencil", k);

@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
   constexpr int STAGES = G::stages, STAGE_BYTES = G::stage_bytes, STACK = G::stack;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+      smem_raw + (((1024u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 1023u)) & 1023u));  // stays a shared-space pointer: LDS, not generic LD
   uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]

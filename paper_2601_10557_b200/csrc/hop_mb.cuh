@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB)
   constexpr int NWARPS = C::THREADS / 32;  // consumer warps
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+      smem_raw + (((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u));  // stays a shared-space pointer: LDS, not generic LD
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -72,41 +72,41 @@ struct RsMaps {
   CUtensorMap x[2];  // x and y parts of the input: (2 kc doubles) x k, leading dim 2 ldx
 };
 
-// ROT: 0 -> x, +1 -> i x, -1 -> -i x; TRANS: the plane tile is K-major (see the header)
-template <int ROT, bool TRANS, class C>
-__device__ __forceinline__ void rs_stage_mma(double (&acc)[2][C::WM][C::WN][2], const double* Ps, const zval* Xs, int wm,
+// One k4 slice of a warp's operands: plane fragment (A of DMMA.8x8x4) and the real / imaginary
+// parts of the input fragment (B), the latter already multiplied by rot i (rot = 0, +1, -1; the
+// sign flips are exact, so the products are those of the unrotated form bit for bit).
+template <class C>
+struct RsFrag {
+  double pf[C::WM];
+  double br[C::WN], bi[C::WN];
+};
+
+// TRANS: the plane tile is K-major (see the header)
+template <bool TRANS, class C>
+__device__ __forceinline__ void rs_load_frag(RsFrag<C>& f, const double* Ps, const zval* Xs, int ks, int rot, int wm,
                                              int wn, int g, int t) {
 #pragma unroll
-  for (int ks = 0; ks < C::BK / 4; ++ks) {
-    double pf[C::WM];
-    double br[C::WN], bi[C::WN];
+  for (int i = 0; i < C::WM; ++i) {
+    const int r = wm * (8 * C::WM) + i * 8 + g;
+    f.pf[i] = TRANS ? Ps[r * C::LDK + ks * 4 + t] : Ps[(ks * 4 + t) * C::LDP + r];
+  }
 #pragma unroll
-    for (int i = 0; i < C::WM; ++i) {
-      const int r = wm * (8 * C::WM) + i * 8 + g;
-      pf[i] = TRANS ? Ps[r * C::LDK + ks * 4 + t] : Ps[(ks * 4 + t) * C::LDP + r];
-    }
+  for (int j = 0; j < C::WN; ++j) {
+    const zval xv = lds128(Xs + (wn * (8 * C::WN) + j * 8 + g) * C::LDX + ks * 4 + t);
+    f.br[j] = rot == 0 ? xv.re : (rot > 0 ? -xv.im : xv.im);
+    f.bi[j] = rot == 0 ? xv.im : (rot > 0 ? xv.re : -xv.re);
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void rs_mma(double (&acc)[2][C::WM][C::WN][2], const RsFrag<C>& f) {
+#pragma unroll
+  for (int i = 0; i < C::WM; ++i)
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
-      const zval xv = lds128(Xs + (wn * (8 * C::WN) + j * 8 + g) * C::LDX + ks * 4 + t);
-      if constexpr (ROT > 0) {  // i * x
-        br[j] = -xv.im;
-        bi[j] = xv.re;
-      } else if constexpr (ROT < 0) {  // -i * x
-        br[j] = xv.im;
-        bi[j] = -xv.re;
-      } else {
-        br[j] = xv.re;
-        bi[j] = xv.im;
-      }
+      dmma(acc[0][i][j], f.pf[i], f.br[j]);
+      dmma(acc[1][i][j], f.pf[i], f.bi[j]);
     }
-#pragma unroll
-    for (int i = 0; i < C::WM; ++i)
-#pragma unroll
-      for (int j = 0; j < C::WN; ++j) {
-        dmma(acc[0][i][j], pf[i], br[j]);
-        dmma(acc[1][i][j], pf[i], bi[j]);
-      }
-  }
 }
 
 // grid: x = column tiles (fastest: CTAs sharing a plane strip run together), y = 2 * row tiles
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   constexpr int NWARPS = C::THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base =
-      reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+      smem_raw + (((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u));  // stays a shared-space pointer: LDS, not generic LD
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -178,16 +178,35 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
 #pragma unroll
       for (int j = 0; j < C::WN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
 
+  // Software-pipelined consumer: the fragments of k4 slice ks + 1 are read from shared memory while
+  // the DMMAs of slice ks issue, across stage boundaries too (the next stage's full barrier is
+  // waited for one slice early), so no warp meets a stage edge with an empty operand register set.
+  constexpr int KS = C::BK / 4;
+  const int rot_t = TRANS ? -1 : 1;
+  auto rot_of = [&](int kt) { return ((kt >= nkt_part) == (h == 1)) ? rot_t : 0; };
+  auto stage_p = [&](int s) { return reinterpret_cast<const double*>(base + s * STAGE_BYTES); };
+  auto stage_x = [&](int s) { return reinterpret_cast<const zval*>(base + s * STAGE_BYTES + P_BYTES); };
+  RsFrag<C> cur, nxt;
+  mbar_wait_cta(&full[0], 0);
+  rs_load_frag<TRANS, C>(cur, stage_p(0), stage_x(0), 0, rot_of(0), wm, wn, g, t);
 #pragma unroll 1
   for (int kt = 0; kt < nkt; ++kt) {
     const int s = kt % C::STAGES;
-    mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
-    const double* Ps = reinterpret_cast<const double*>(base + s * STAGE_BYTES);
-    const zval* Xs = reinterpret_cast<const zval*>(base + s * STAGE_BYTES + P_BYTES);
-    if ((kt >= nkt_part) == (h == 1))
-      rs_stage_mma<TRANS ? -1 : 1, TRANS, C>(acc, Ps, Xs, wm, wn, g, t);
-    else
-      rs_stage_mma<0, TRANS, C>(acc, Ps, Xs, wm, wn, g, t);
+    const double* Ps = stage_p(s);
+    const zval* Xs = stage_x(s);
+    const int rot = rot_of(kt);
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      if (ks + 1 < KS) {
+        rs_load_frag<TRANS, C>(nxt, Ps, Xs, ks + 1, rot, wm, wn, g, t);
+      } else if (kt + 1 < nkt) {
+        const int s1 = (kt + 1) % C::STAGES;
+        mbar_wait_cta(&full[s1], ((kt + 1) / C::STAGES) & 1);
+        rs_load_frag<TRANS, C>(nxt, stage_p(s1), stage_x(s1), 0, rot_of(kt + 1), wm, wn, g, t);
+      }
+      rs_mma<C>(acc, cur);
+      cur = nxt;
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);
   }

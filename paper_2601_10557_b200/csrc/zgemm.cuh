@@ -26,7 +26,12 @@ struct GemmArgs {
   int M, N, K;
   double alpha, beta;
   zval* ws;  // split-K partials [z][N][M] (ld = M), used when gridDim.z > 1
+  // structure: GEMM_UPPER -- only tiles touching the upper triangle are computed (a hermitian
+  // result, M == N; the strictly lower part is left undefined for herm_upper_kernel to fill);
+  // GEMM_B_UPPER -- B is upper triangular (K == N), so output column j needs K rows <= j only
+  int tri;
 };
+enum : int { GEMM_UPPER = 1, GEMM_B_UPPER = 2 };
 
 template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
 struct GemmCfg {
@@ -83,9 +88,11 @@ __global__ void __launch_bounds__(C::THREADS) zgemm_kernel(const GemmArgs g) {
   const int gq = lane >> 2, t = lane & 3;
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int i0 = blockIdx.x * C::BM, j0 = blockIdx.y * C::BN;
+  if ((g.tri & GEMM_UPPER) && i0 >= j0 + C::BN) return;  // tile strictly below the diagonal
+  const int K = (g.tri & GEMM_B_UPPER) ? min(g.K, j0 + C::BN) : g.K;
 
   // split-K range
-  const int nkt_all = (g.K + C::BK - 1) / C::BK;
+  const int nkt_all = (K + C::BK - 1) / C::BK;
   const int per = (nkt_all + gridDim.z - 1) / gridDim.z;
   const int kt_begin = blockIdx.z * per;
   const int kt_end = min(nkt_all, kt_begin + per);
@@ -175,11 +182,12 @@ __global__ void __launch_bounds__(C::THREADS) zgemm_kernel(const GemmArgs g) {
 
 // Fixed-order split-K sum: C = alpha * sum_z ws[z] + beta * C
 __global__ void zgemm_splitk_reduce(const zval* __restrict__ ws, int splits, zval* c, int64_t ldc, int M, int N,
-                                    double alpha, double beta) {
+                                    double alpha, double beta, int tri) {
   const int64_t total = (int64_t)M * N;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int row = int(idx % M);
     const int64_t col = idx / M;
+    if ((tri & GEMM_UPPER) && row > col) continue;  // partials of skipped tiles were never written
     double sr = 0.0, si = 0.0;
     for (int z = 0; z < splits; ++z) {
       const zval v = ws[(int64_t)z * total + idx];

@@ -688,8 +688,9 @@ class DistSolver:
         x0 = q_col.clone()
         q = q_col
         ok = True
-        for _ in range(2):
+        for p in range(2):
             gm = self._gram_row(q)
+            g2 = gm.clone() if p == 1 else None  # chol_rinv factors in place
             st.mark("gram + allreduce", q.shape[0])
             rinv, info = self.ops.chol_rinv(gm)
             st.mark("chol_rinv", q.shape[0])
@@ -698,7 +699,9 @@ class DistSolver:
                 break
             q = self.ops.nn(q, rinv)
             st.mark("Q R^-1", q.shape[0])
-        if ok and self.ops.defect(self._gram_row(q)) <= 1e-8:
+        # defect max|Q^H Q - I| folded into pass 2 (ortho.py:124): Q^H Q = R^-H G2 R^-1 from the pass's
+        # own Gram, k x k work and no third Gram + allreduce
+        if ok and self.ops.defect(self.ops.gram(rinv, self.ops.nn(g2, rinv))) <= 1e-8:
             st.mark("defect", q.shape[0])
             return q, "cholqr"
         st.mark("FALLBACK", q.shape[0])
@@ -722,12 +725,25 @@ class DistSolver:
             raise RankDeficiencyError("orthonormalization failed")
         return q, "shifted_cholqr"
 
-    def s_orthonormalize(self, v_col, locked_col):
-        """ortho.py:132-158 distributed: project out span(S Y), then CholQR2 (col layout)."""
+    def extend_sbasis(self, sbasis, l_old: int, y_new) -> None:
+        """sbasis[l_old:l_old + c] <- orthonormal completion of span(S Y_new) against sbasis[:l_old]
+        (col layout; the single-GPU bse_extend_sbasis: BCGS2 then CholQR of the new block only)."""
+        c = y_new.shape[0]
+        if not c:
+            return
+        b = self.ops.sflip(y_new)
+        if l_old:
+            for _ in range(2):
+                proj = self._gram_row(sbasis[:l_old], b)
+                self.ops.nn(sbasis[:l_old], proj, out=b, alpha=-1.0, beta=1.0)
+        q, _ = self.cholqr(b)
+        sbasis[l_old:l_old + c].copy_(q)
+
+    def s_orthonormalize(self, v_col, basis):
+        """ortho.py:132-158 distributed: project out span(S Y) -- given by its orthonormal basis,
+        grown incrementally as pairs lock -- then CholQR2 (col layout)."""
         st = _Steps("s_ortho", self.g.rank)
-        if locked_col is not None and locked_col.shape[0]:
-            basis, _ = self.cholqr(self.ops.sflip(locked_col))
-            st.mark("basis of S Y", locked_col.shape[0])
+        if basis is not None and basis.shape[0]:
             proj = self._gram_row(basis, v_col)  # l x k
             self.ops.nn(basis, proj, out=v_col, alpha=-1.0, beta=1.0)
             st.mark("projection", v_col.shape[0])
@@ -984,6 +1000,7 @@ class DistSolver:
         st.mark("start block", nevex)
         row_buf = self.ops.empty(nevex, 2 * g.nr)
         locked = self.ops.empty(nev, 2 * g.nc)
+        sbasis = self.ops.empty(nev, 2 * g.nc)  # orthonormal basis of span(S Y_locked)
         nlock, lvals, lres, trace = 0, [], [], []
         converged, it_used, current, backups = False, 0, bounds, 0
         from .solver import MIXED_SWITCH, mixed_precision
@@ -1006,7 +1023,7 @@ class DistSolver:
                     self.chebyshev(v, fcfg, row_buf)
             ledger.add_flops("filter", cfg.deg * 8.0 * n * n * k)
             with ledger.timing("ortho"):
-                v, _ = self.s_orthonormalize(v, locked[:nlock] if nlock else None)
+                v, _ = self.s_orthonormalize(v, sbasis[:nlock] if nlock else None)
             if nlock:
                 ledger.add_flops("ortho", 16.0 * n * nlock * k)
             ledger.add_flops("ortho", 2 * (8.0 * n * k * k + 4.0 * n * k * k))
@@ -1024,6 +1041,8 @@ class DistSolver:
             cnt = new.size
             if cnt:
                 locked[nlock:nlock + cnt].copy_(vecs[:cnt])
+                if nlock + cnt < nev:
+                    self.extend_sbasis(sbasis, nlock, locked[nlock:nlock + cnt])
                 nlock += cnt
                 lvals.extend(lam[:cnt].tolist())
                 lres.extend(res[:cnt].tolist())

@@ -81,6 +81,36 @@ def s_orthonormalize_inplace(v, locked_y=None, ledger: PhaseLedger | None = None
     return _METHODS[method.value]
 
 
+def s_orthonormalize_basis_inplace(v, sbasis=None, ledger: PhaseLedger | None = None) -> str:
+    """s_orthonormalize_inplace with the locked space given by its orthonormal basis (n x l,
+    maintained by extend_sbasis): the solver loop's form (the reference's per-iteration QR of S Y
+    is replaced by the incremental basis, same span)."""
+    n, k = v.shape
+    l = 0 if sbasis is None else int(sbasis.shape[1])
+    if k > n:
+        raise RankDeficiencyError(f"cannot orthonormalize {k} columns in dimension {n}")
+    method = ctypes.c_int(0)
+    ctx = _lib.Context.get(v.device.index)
+    bptr = _lib.dptr(sbasis) if l else ctypes.c_void_p(0)
+    ctx.call("bse_s_orthonormalize_basis", _lib.dptr(v), n, k, ld_of(v), bptr, l, ld_of(sbasis) if l else n,
+             ctypes.byref(method))
+    if ledger is not None:
+        if l:
+            ledger.add_flops("ortho", 16.0 * n * l * k)  # ortho.py:154 (the reference's model)
+        ledger.add_flops("ortho", 2 * (8.0 * n * k * k + 4.0 * n * k * k))  # ortho.py:110
+    return _METHODS[method.value]
+
+
+def extend_sbasis(sbasis, l_old: int, y_new) -> None:
+    """sbasis[:, l_old:l_old + c] <- orthonormal completion of span(S Y_new) against sbasis[:, :l_old]."""
+    c = int(y_new.shape[1])
+    if not c:
+        return
+    n = sbasis.shape[0]
+    _lib.Context.get(sbasis.device.index).call("bse_extend_sbasis", _lib.dptr(sbasis), n, ld_of(sbasis), l_old,
+                                               _lib.dptr(y_new), ld_of(y_new), c)
+
+
 def fix_column_phases(q):
     """ortho.py:70-82 on the GPU (first entry >= 1e-8 max|q| made real positive)."""
     dev = _device_for(q)
