@@ -96,30 +96,47 @@ def cmd_solve(args) -> None:
 
 
 def cmd_bench(args) -> None:
-    """Per repetition and phase: rep,phase,seconds,flops,gflops (FORMATS.md bench.csv)."""
+    """Repeat a solve; per repetition and phase seconds, modeled flops, GFLOP/s, then min/avg/max
+    summaries -- bench.csv and manifest.json in the reference's format (cli.py:291-361,
+    FORMATS.md "bench.csv")."""
+    from . import fileio
     from .solver import solve
 
-    ham, _ = _load(args)
+    ham, inputs = _load(args)
     cfg = _config(args)
-    rows = ["rep,phase,seconds,flops,gflops"]
-    per_phase: dict[str, list[float]] = {}
-    for rep in range(args.reps):
+    if args.reps < 1:
+        raise ValueError_(f"reps must be >= 1, got {args.reps}")
+    runs = []
+    for _ in range(args.reps):
         t0 = time.perf_counter()
         res = solve(ham, cfg, keep_on_device=True)
-        wall = time.perf_counter() - t0
-        for ph in ("lanczos", "filter", "ortho", "rr", "residuals"):
-            sec, fl = res.ledger.seconds.get(ph, 0.0), res.ledger.flops.get(ph, 0.0)
-            rows.append(f"{rep},{ph},{sec:.6f},{fl:.0f},{(fl / sec / 1e9) if sec else 0.0:.3f}")
-            per_phase.setdefault(ph, []).append(sec)
-        tf = res.ledger.total_flops()
-        rows.append(f"{rep},total,{wall:.6f},{tf:.0f},{tf / wall / 1e9:.3f}")
-        per_phase.setdefault("total", []).append(wall)
-    for ph, v in per_phase.items():
-        rows.append(f"summary,{ph},{min(v):.6f},{sum(v) / len(v):.6f},{max(v):.6f}")
+        runs.append((res, time.perf_counter() - t0))
     out = Path(args.out)
     out.mkdir(parents=True, exist_ok=True)
+    phases = sorted({ph for r, _ in runs for ph in r.ledger.flops})
+    rows = ["# bsesolve bench v1", "# manifest: manifest.json", f"# input_digest: {'+'.join(inputs[k] for k in sorted(inputs))}",
+            "rep,phase,seconds,flops,gflops"]
+    for rep, (r, wall) in enumerate(runs):
+        led = r.ledger
+        for ph in phases:
+            sec, fl = led.seconds.get(ph, 0.0), led.flops.get(ph, 0.0)
+            rows.append(f"{rep},{ph},{sec:.6f},{fl:.0f},{(fl / sec / 1e9) if sec > 0 else 0.0:.3f}")
+        rows.append(f"{rep},total,{wall:.6f},{led.total_flops():.0f},{led.total_flops() / wall / 1e9:.3f}")
+    echo = []
+    for ph in phases + ["total"]:
+        if ph == "total":
+            secs, fl = [w for _, w in runs], runs[0][0].ledger.total_flops()
+        else:
+            secs, fl = [r.ledger.seconds.get(ph, 0.0) for r, _ in runs], runs[0][0].ledger.flops.get(ph, 0.0)
+        rows.append(f"summary,{ph},{min(secs):.6f}/{sum(secs) / len(secs):.6f}/{max(secs):.6f},{fl:.0f},")
+        echo.append(f"{ph:10s} min/avg/max {min(secs):.4f}/{sum(secs) / len(secs):.4f}/{max(secs):.4f} s, "
+                    f"modeled {fl / 1e9:.3f} GFLOP")
     (out / "bench.csv").write_text("\n".join(rows) + "\n")
-    print("\n".join(rows[-len(per_phase):]))
+    fileio.write_manifest(out / "manifest.json", "bench",
+                          {"nev": cfg.nev, "nex": cfg.nex, "deg": cfg.deg, "tol": cfg.tol, "maxiter": cfg.maxiter,
+                           "rr_variant": cfg.rr_variant, "seed": cfg.seed, "reps": args.reps},
+                          inputs, ["bench.csv"], args.seed)
+    print("\n".join(echo))
 
 
 def _parser() -> argparse.ArgumentParser:
@@ -152,7 +169,7 @@ def _parser() -> argparse.ArgumentParser:
         if name == "solve":
             s.add_argument("--largest", action="store_true")
         else:
-            s.add_argument("--reps", type=int, default=3)
+            s.add_argument("--reps", type=int, default=5)
     return ap
 
 

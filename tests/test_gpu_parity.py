@@ -576,3 +576,47 @@ def test_filter_without_sum_planes_when_hbm_is_short(bse, monkeypatch):
     ds = DistributedSolver((a, b))
     rd = ds.solve(bse.SolverConfig(nev=8, seed=21))
     assert ds.fwd.sd is None and (np.abs(rd.lambdas - g["lambdas"]) / np.abs(g["lambdas"])).max() <= 1e-10
+
+
+def test_complete_spectrum_and_mirror_largest_match_reference(bse):
+    """solver.py:253-299 on the drop-in's own solve, against the reference's outputs for its solve
+    of the same case (tests/golden/post_m32_s4.npz, oracle/make_golden_post.py): values exactly
+    as ordered, vectors per column up to a phase (the Ritz vectors' phase is the eigensolver's)."""
+    a, b = golden_ham(32, 4)
+    g = golden("post_m32_s4.npz")
+    r = bse.solve(bse.BseHamiltonian(a, b), bse.SolverConfig(nev=4, seed=9))
+    assert np.abs(r.lambdas - g["lambdas"]).max() <= 1e-10 * np.abs(g["lambdas"]).max()
+
+    def same_up_to_phase(x, y):
+        ov = np.abs(np.einsum("ij,ij->j", x.conj(), y)) / (np.linalg.norm(x, axis=0) * np.linalg.norm(y, axis=0))
+        return np.abs(ov - 1).max()
+
+    cs = bse.complete_spectrum(r)
+    assert np.abs(cs.values - g["cs_values"]).max() <= 1e-10 * np.abs(g["cs_values"]).max()
+    assert same_up_to_phase(cs.right, g["cs_right"]) <= 1e-10
+    assert same_up_to_phase(cs.left, g["cs_left"]) <= 1e-10
+    # left pairs: u_i^H v_j = 0 for i != j and the sign normalisation u^H v > 0 (solver.py:262-266)
+    d = cs.left.conj().T @ cs.right
+    assert np.abs(d - np.diag(np.diag(d))).max() <= 1e-8 and (np.real(np.diag(d)) > 0).all()
+    ml = bse.mirror_largest(r)
+    assert np.abs(ml.lambdas - g["ml_lambdas"]).max() <= 1e-10 * np.abs(g["ml_lambdas"]).max()
+    assert same_up_to_phase(ml.v, g["ml_v"]) <= 1e-10
+    np.testing.assert_allclose(ml.residual_norms, r.residual_norms[np.argsort(-r.lambdas, kind="stable")])
+
+
+def test_cli_bench_matches_reference_format(bse, tmp_path):
+    """`bench` subcommand (cli.py:291-361): bench.csv with the reference's header, input digest,
+    (rep, phase) rows and modeled flops -- identical to the reference's own bench.csv on the same
+    PCHB (tests/golden/m8_s11_bench.csv) except the measured seconds -- plus manifest.json."""
+    from paper_2601_10557_b200.cli import main
+
+    rc = main(["bench", "--pchb", str(GOLDEN / "m8_s11.pchb"), "--nev", "2", "--tol", "1e-10", "--reps", "2",
+               "--out", str(tmp_path)])
+    assert rc == 0
+    got = (tmp_path / "bench.csv").read_text().splitlines()
+    ref = (GOLDEN / "m8_s11_bench.csv").read_text().splitlines()
+    assert got[:4] == ref[:4] and len(got) == len(ref)
+    for gl, rl in zip(got[4:], ref[4:]):
+        gf, rf = gl.split(","), rl.split(",")
+        assert gf[:2] == rf[:2] and gf[3] == rf[3], (gl, rl)  # rep, phase, modeled flops
+    assert json.loads((tmp_path / "manifest.json").read_text())["command"] == "bench"
