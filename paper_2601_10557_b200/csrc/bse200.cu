@@ -343,10 +343,10 @@ using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
 
 // TRANS: the transposed-tile product on the same planes (hop_rs.cuh header): a.mr output rows
 // = plane columns, a.kc contraction = plane rows; the planes are read through K-major boxes.
-template <class C, bool TRANS = false>
+template <class C, bool TRANS = false, bool GENERIC = false>
 void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   constexpr size_t smem = C::template smem<TRANS>();
-  ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS>, (int)smem);
+  ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS, GENERIC>, (int)smem);
   bse::RsMaps mp;
   for (int q = 0; q < 4; ++q) {
     if (TRANS)
@@ -358,21 +358,23 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
   mp.x[1] = map2d_f64(a.x2, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
   const int nbm = (a.mr + C::BM - 1) / C::BM;
   dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm);
-  bse::hop_rs_tma_kernel<C, TRANS><<<grid, C::THREADS + 32, smem, ctx->stream>>>(a, mp);
+  bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(a, mp);
   check_launch(ctx);
 }
 
 // one real-split product (folded input x1 / x2, output halves y1 / y2) on the tile's planes g
+// 128 x 32 tiles read their fragments through generic loads, 64 x 32 through LDS (the faster of
+// each, profiles/r02/rs_consumer_variants_*.txt; bitwise identical)
 template <bool TRANS = false>
 void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   switch (ctx->filter_cm) {
-    case 92: launch_rs<RsTall, TRANS>(ctx, a, g, ldg); break;
-    case 94: launch_rs<RsNarrow, TRANS>(ctx, a, g, ldg); break;
+    case 92: launch_rs<RsTall, TRANS, true>(ctx, a, g, ldg); break;
+    case 94: launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg); break;
     default:
       if (a.k >= 512)
-        launch_rs<RsTall, TRANS>(ctx, a, g, ldg);
+        launch_rs<RsTall, TRANS, true>(ctx, a, g, ldg);
       else
-        launch_rs<RsNarrow, TRANS>(ctx, a, g, ldg);
+        launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg);
   }
 }
 

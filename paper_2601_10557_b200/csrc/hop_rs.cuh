@@ -81,10 +81,10 @@ struct RsFrag {
   double br[C::WN], bi[C::WN];
 };
 
-// TRANS: the plane tile is K-major (see the header)
-template <bool TRANS, class C>
-__device__ __forceinline__ void rs_load_frag(RsFrag<C>& f, const double* Ps, const zval* Xs, int ks, int rot, int wm,
-                                             int wn, int g, int t) {
+// ROT: 0 -> x, +1 -> i x, -1 -> -i x; TRANS: the plane tile is K-major (see the header)
+template <int ROT, bool TRANS, class C>
+__device__ __forceinline__ void rs_load_frag_t(RsFrag<C>& f, const double* Ps, const zval* Xs, int ks, int wm, int wn,
+                                               int g, int t) {
 #pragma unroll
   for (int i = 0; i < C::WM; ++i) {
     const int r = wm * (8 * C::WM) + i * 8 + g;
@@ -93,8 +93,16 @@ __device__ __forceinline__ void rs_load_frag(RsFrag<C>& f, const double* Ps, con
 #pragma unroll
   for (int j = 0; j < C::WN; ++j) {
     const zval xv = lds128(Xs + (wn * (8 * C::WN) + j * 8 + g) * C::LDX + ks * 4 + t);
-    f.br[j] = rot == 0 ? xv.re : (rot > 0 ? -xv.im : xv.im);
-    f.bi[j] = rot == 0 ? xv.im : (rot > 0 ? xv.re : -xv.re);
+    if constexpr (ROT > 0) {
+      f.br[j] = -xv.im;
+      f.bi[j] = xv.re;
+    } else if constexpr (ROT < 0) {
+      f.br[j] = xv.im;
+      f.bi[j] = -xv.re;
+    } else {
+      f.br[j] = xv.re;
+      f.bi[j] = xv.im;
+    }
   }
 }
 
@@ -116,7 +124,10 @@ __device__ __forceinline__ int rs_plane(int h, int part) {
   return TRANS ? (h ? (part ? 0 : 2) : (part ? 1 : 3)) : 2 * h + part;
 }
 
-template <class C, bool TRANS = false>
+// GENERIC: fragment loads through a generic pointer (LD) instead of shared-space LDS -- measured
+// faster for the 128 x 32 tile, slower for the 64 x 32 one (profiles/r02/rs_consumer_variants_*.txt;
+// a slice-ahead software-pipelined consumer measured 3-9% slower than both and was dropped)
+template <class C, bool TRANS = false, bool GENERIC = false>
 __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(const HopArgs a,
                                                                               const __grid_constant__ RsMaps maps) {
   constexpr int P_BYTES = C::template p_bytes<TRANS>();
@@ -124,7 +135,8 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   constexpr int NWARPS = C::THREADS / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base =
-      smem_raw + (((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u));  // stays a shared-space pointer: LDS, not generic LD
+      GENERIC ? reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127))
+             : smem_raw + (((128u - (static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) & 127u)) & 127u));
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -178,34 +190,28 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
 #pragma unroll
       for (int j = 0; j < C::WN; ++j) acc[q][i][j][0] = acc[q][i][j][1] = 0.0;
 
-  // Software-pipelined consumer: the fragments of k4 slice ks + 1 are read from shared memory while
-  // the DMMAs of slice ks issue, across stage boundaries too (the next stage's full barrier is
-  // waited for one slice early), so no warp meets a stage edge with an empty operand register set.
   constexpr int KS = C::BK / 4;
-  const int rot_t = TRANS ? -1 : 1;
-  auto rot_of = [&](int kt) { return ((kt >= nkt_part) == (h == 1)) ? rot_t : 0; };
   auto stage_p = [&](int s) { return reinterpret_cast<const double*>(base + s * STAGE_BYTES); };
   auto stage_x = [&](int s) { return reinterpret_cast<const zval*>(base + s * STAGE_BYTES + P_BYTES); };
-  RsFrag<C> cur, nxt;
-  mbar_wait_cta(&full[0], 0);
-  rs_load_frag<TRANS, C>(cur, stage_p(0), stage_x(0), 0, rot_of(0), wm, wn, g, t);
 #pragma unroll 1
   for (int kt = 0; kt < nkt; ++kt) {
     const int s = kt % C::STAGES;
+    mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
     const double* Ps = stage_p(s);
     const zval* Xs = stage_x(s);
-    const int rot = rot_of(kt);
+    RsFrag<C> f;
+    if ((kt >= nkt_part) == (h == 1)) {  // the i (forward) / -i (transposed) part of this half
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      if (ks + 1 < KS) {
-        rs_load_frag<TRANS, C>(nxt, Ps, Xs, ks + 1, rot, wm, wn, g, t);
-      } else if (kt + 1 < nkt) {
-        const int s1 = (kt + 1) % C::STAGES;
-        mbar_wait_cta(&full[s1], ((kt + 1) / C::STAGES) & 1);
-        rs_load_frag<TRANS, C>(nxt, stage_p(s1), stage_x(s1), 0, rot_of(kt + 1), wm, wn, g, t);
+      for (int ks = 0; ks < KS; ++ks) {
+        rs_load_frag_t<TRANS ? -1 : 1, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
+        rs_mma<C>(acc, f);
       }
-      rs_mma<C>(acc, cur);
-      cur = nxt;
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        rs_load_frag_t<0, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
+        rs_mma<C>(acc, f);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);

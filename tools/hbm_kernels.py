@@ -1,6 +1,7 @@
 """Achieved HBM bandwidth of the memory-bound kernels on the solve path (north star: "achieved HBM
 GB/s for the QR, residual and axpby kernels"), at C3 shapes (m = 20000, n = 40000, k = 1200),
-timed with CUDA events on the library's stream (torch's current stream), inputs > L2.
+timed with CUDA events on the library's stream (torch's current stream), L2 flushed before
+every timed call, against MEASURED_PEAKS.json's HBM figure.
 
 The axpby of the Chebyshev recurrence and the S-flip of the RR product are fused into the GEMM
 epilogues (no standalone pass); the standalone HBM-bound kernels are the ones below.
@@ -20,16 +21,26 @@ PEAK = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").
     if (Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").exists() else 6553.9
 
 
+_FLUSH = None
+
+
 def timed(fn, reps=10):
+    """Median of reps CUDA-event timings, the 126 MB L2 flushed (a 512 MB write) before each."""
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(64 << 20, dtype=torch.float64, device="cuda")
     fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
+    ts = []
     for _ in range(reps):
+        _FLUSH.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sorted(ts)[len(ts) // 2]
 
 
 def main(m=20000, k=1200):

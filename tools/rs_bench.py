@@ -2,7 +2,7 @@
 (bse_chebyshev_filter_rs, per step) and the grid's transposed product (bse_hop_tile_rs_t) on the
 same planes; executed TF/s (4 n^2 k per step) against the measured 37.1 TF/s DMMA peak.
 
-    python tools/rs_bench.py [m] [k,k,...]
+    python tools/rs_bench.py [m] [k,k,...] [code,code,...]   (bse_set_filter_algorithm codes)
 """
 import json
 import sys
@@ -19,6 +19,7 @@ from paper_2601_10557_b200.hamiltonian import colmajor_empty, ld_of
 PEAK = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())["dmma_tflops"]
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 ks = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else [1200, 300, 100]
+codes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [90]
 dev = torch.device("cuda", 0)
 ops = CudaOps(dev)
 ctx = ops.ctx
@@ -48,20 +49,30 @@ def timed(fn, reps):
 
 out = []
 for k in ks:
-    v = colmajor_empty(n, k, dev)
-    v.real.normal_()
-    v.imag.normal_()
+    v0 = colmajor_empty(n, k, dev)
+    v0.real.normal_()
+    v0.imag.normal_()
     work = torch.empty(2 * n * k, dtype=torch.complex128, device=dev)
-    deg = 4
-    ms_f = timed(lambda: ctx.call("bse_chebyshev_filter_rs", fwd.g.data_ptr(), fwd.ldg, m, _lib.dptr(v), n, k, deg,
-                                  0.0, 1.0, -1.5, _lib.dptr(work)), 2) / deg
     x = torch.empty((k, n), dtype=torch.complex128, device=dev)
     x.real.normal_()
     x.imag.normal_()
     y = torch.empty_like(x)
-    ms_t = timed(lambda: ops.hop(trn, x, y, alpha=0.5, shift=0.1, shift_rows=(0, m), s_off=0, filter=True, rs=True), 4)
-    ex = 4.0 * n * n * k / 1e12
-    row = {"m": m, "k": k, "fwd_ms": ms_f, "fwd_tflops": ex / ms_f * 1e3, "fwd_frac": ex / ms_f * 1e3 / PEAK,
-           "trans_ms": ms_t, "trans_tflops": ex / ms_t * 1e3, "trans_frac": ex / ms_t * 1e3 / PEAK}
-    out.append(row)
-    print(json.dumps({kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in row.items()}), flush=True)
+    deg = 4
+    ref = None
+    for code in codes:
+        ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
+        v = v0.clone()
+        ms_f = timed(lambda: ctx.call("bse_chebyshev_filter_rs", fwd.g.data_ptr(), fwd.ldg, m, _lib.dptr(v), n, k, deg,
+                                      0.0, 1.0, -1.5, _lib.dptr(work)), 2) / deg
+        ms_t = timed(lambda: ops.hop(trn, x, y, alpha=0.5, shift=0.1, shift_rows=(0, m), s_off=0, filter=True,
+                                     rs=True), 4)
+        yy = y.clone()
+        same = None if ref is None else bool(torch.equal(ref, yy))
+        ref = yy if ref is None else ref
+        ex = 4.0 * n * n * k / 1e12
+        row = {"m": m, "k": k, "code": code, "fwd_ms": ms_f, "fwd_tflops": ex / ms_f * 1e3,
+               "fwd_frac": ex / ms_f * 1e3 / PEAK, "trans_ms": ms_t, "trans_tflops": ex / ms_t * 1e3,
+               "trans_frac": ex / ms_t * 1e3 / PEAK, "bitwise_as_first_code": same}
+        out.append(row)
+        print(json.dumps({kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in row.items()}), flush=True)
+ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 90))
