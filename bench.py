@@ -375,6 +375,9 @@ def run_ours(args, world, rank, local):
     launches = ctx.launches - launches0
     step_s = e0.elapsed_time(e1) / 1e3 / args.steps
     step_s = max_over_ranks(step_s, world)
+    # device memory: this rank's operator storage and the peak allocation of the timed solves
+    op_bytes = ds.operator_bytes() if world > 1 else None
+    peak_gb = max_over_ranks(torch.cuda.max_memory_allocated(dev) / 1e9, world)
     fms, ffl = filter_stats()
     res = results[-1]
     if world == 1:
@@ -485,6 +488,10 @@ def run_ours(args, world, rank, local):
                       "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},
             "parity_vs_reference": parity,
             "is_definite": defin,
+            "memory": {"operator_gb_per_gpu": round(op_bytes / 1e9, 3) if op_bytes else None,
+                       "peak_allocated_gb_max_over_ranks": round(peak_gb, 2),
+                       "note": "operator = one tile's real-split planes, 32 m^2/(p q) bytes (N > 1); "
+                               "peak includes the generator's full instance on each rank"},
             "clocks": clk.summary(),
         }
         if cpu is not None:

@@ -101,7 +101,9 @@ int bse_make_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t mr, 
 /* Register real-split planes d_g (bse_make_rs_planes, mr = kc = m) of the operator d_ab on the
  * context: while registered, the T = (S) H Q products of bse_rr_hermitian / bse_rr_backup with
  * this d_ab run on the real-split kernel (fold Q, product, unfold with the S-flip).  d_g = NULL
- * clears the registration (the Python layer scopes it to one RR call).                          */
+ * clears the registration (the Python layer scopes it to one RR call).  d_ab may be NULL for an
+ * operator held as planes only (one GPU at n = 100k: the planes replace [A|B]); the RR calls
+ * then take d_ab = NULL too and every product, k = 1 included, runs on the planes.             */
 int bse_set_rs_planes(bse_ctx* ctx, const void* d_ab, int64_t m, const void* d_g, int64_t ldg);
 /* Register a device buffer of 4 k^2 complex128 + k doubles that the next bse_rr_hermitian /
  * bse_rr_backup calls fill with their reduced problem (rayleigh_ritz.py:41-51, 140-143, 176-179):

@@ -459,7 +459,8 @@ bool rs_active(const bse_ctx* ctx, const void* d_ab, int64_t m) {
 void apply_h(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, const zval* x, int64_t ldx, zval* y, int64_t ldy,
              int64_t k, double low_sign, const void* d_sd = nullptr, zval* fold = nullptr) {
   if (k == 0 || m == 0) return;
-  if (k > 1 && fold && rs_active(ctx, d_ab, m)) {
+  // k == 1 takes the GEMV on [A|B] unless the operator is held as planes only (d_ab == NULL)
+  if ((k > 1 || !d_ab) && fold && rs_active(ctx, d_ab, m)) {
     const int fb = grid1d(m * k, 256, 148 * 16);
     // fold x into the buffer, the product into y's halves, then unfold y in place (with the S-flip)
     bse::rs_fold_kernel<<<fb, 256, 0, ctx->stream>>>(x, fold, ldx, 2 * m, m, k, 1.0, 1.0);
@@ -1298,12 +1299,14 @@ int bse_rr_hermitian(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t l
                      double* h_res) {
   return guarded(ctx, [&] {
     if (k == 0) return;
+    if (!d_ab && !rs_active(ctx, d_ab, m))
+      throw BseError(BSE_EVALIDATION, "null operator: a planes-only operator needs bse_set_rs_planes(ctx, NULL, m, g, ldg)");
     const int64_t n = 2 * m;
     const zval* q = static_cast<const zval*>(d_q);
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
     const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
-    const bool rs = k > 1 && rs_active(ctx, d_ab, m);
+    const bool rs = (k > 1 || !d_ab) && rs_active(ctx, d_ab, m);
     Scratch sc(ctx, (h_res ? 2 : 1) * al(n * k * sizeof(zval)) + 3 * al(kk * sizeof(zval)) + 4 * al(k * 8) + gwsb +
                         pencil_ws_bytes(k) + 4096 + (rs ? al(n * k * sizeof(zval)) : 0));
     zval* t = sc.take<zval>(n * k);
@@ -1431,12 +1434,14 @@ int bse_rr_backup(bse_ctx* ctx, const void* d_ab, const void* d_sd, int64_t lda,
                   int64_t ldq, int64_t k, double* h_lam, void* d_vout, int64_t ldvout, double* h_lam_min_m) {
   return guarded(ctx, [&] {
     if (k == 0) return;
+    if (!d_ab && !rs_active(ctx, d_ab, m))
+      throw BseError(BSE_EVALIDATION, "null operator: a planes-only operator needs bse_set_rs_planes(ctx, NULL, m, g, ldg)");
     const int64_t n = 2 * m;
     const zval* q = static_cast<const zval*>(d_q);
     zval* vout = static_cast<zval*>(d_vout);
     const size_t kk = (size_t)k * k;
     const size_t gwsb = std::max({gemm_ws_bytes(k, k, n), gemm_ws_bytes(k, k, m), gemm_ws_bytes(n, k, k)});
-    const bool rs = k > 1 && rs_active(ctx, d_ab, m);
+    const bool rs = (k > 1 || !d_ab) && rs_active(ctx, d_ab, m);
     Scratch sc(ctx, al(n * k * sizeof(zval)) + 4 * al(kk * sizeof(zval)) + al(k * 8) + gwsb + backup_ws_bytes(k) +
                         (rs ? al(n * k * sizeof(zval)) : 0));
     zval* t = sc.take<zval>(n * k);
@@ -1478,13 +1483,16 @@ int bse_lanczos_sweep(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, co
   return guarded(ctx, [&] {
     const int64_t n = 2 * m;
     const int nb = grid1d(n, 256, 296);
-    Scratch sc(ctx, 6 * al(n * sizeof(zval)) + al((nb + 2) * 8) + al(64));
+    if (!d_ab && !rs_active(ctx, d_ab, m))
+      throw BseError(BSE_EVALIDATION, "null operator: a planes-only operator needs bse_set_rs_planes(ctx, NULL, m, g, ldg)");
+    Scratch sc(ctx, 7 * al(n * sizeof(zval)) + al((nb + 2) * 8) + al(64));
     zval* start = sc.take<zval>(n);
     zval* q = sc.take<zval>(n);
     zval* qold = sc.take<zval>(n);
     zval* z = sc.take<zval>(n);
     zval* w = sc.take<zval>(n);
     zval* gv = sc.take<zval>(n);
+    zval* fold = d_ab ? nullptr : sc.take<zval>(n);  // planes-only operator: the matvec on the planes
     double* part = sc.take<double>(nb + 2);
     to_device(ctx, reinterpret_cast<double*>(start), static_cast<const double*>(h_start), 2 * n);
     auto sdot = [&](const zval* x, const zval* y) {
@@ -1504,7 +1512,7 @@ int bse_lanczos_sweep(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, co
       check_launch(ctx);
     };
     // lanczos.py:58-66
-    apply_h(ctx, d_ab, lda, m, start, n, gv, n, 1, 1.0);
+    apply_h(ctx, d_ab, lda, m, start, n, gv, n, 1, 1.0, nullptr, fold);
     const double norm2 = sdot(gv, start);
     if (!(norm2 > 0))
       throw BseError(BSE_EINDEFINITE, "start vector has non-positive S*H norm; matrix is not definite");
@@ -1521,7 +1529,7 @@ int bse_lanczos_sweep(bse_ctx* ctx, const void* d_ab, int64_t lda, int64_t m, co
       if (j == steps - 1) break;
       bse::lincomb3_kernel<<<grid1d(n), 256, 0, ctx->stream>>>(w, z, 1.0, q, -alpha, qold, -beta_prev, n);
       check_launch(ctx);
-      apply_h(ctx, d_ab, lda, m, w, n, gv, n, 1, 1.0);
+      apply_h(ctx, d_ab, lda, m, w, n, gv, n, 1, 1.0, nullptr, fold);
       const double beta2 = sdot(gv, w);
       const double running = std::max({1.0, amax, beta_prev});
       if (beta2 <= (1e-14 * running) * (1e-14 * running)) break;  // lanczos.py:79-81

@@ -134,12 +134,17 @@ class BseHamiltonian:
         return ham
 
     def device_blocks(self, device=None):
+        """The [A | B] device buffer; None on a device where the operator is held as real-split
+        planes only (planes_only / drop_blocks_for_planes)."""
         torch = _torch()
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         device = torch.device(device)
         if device.type == "cuda" and device.index is None:
             device = torch.device("cuda", torch.cuda.current_device())
+        if device in self.__dict__.get("_planes_only", ()):
+            _lib.Context.get(device.index).set_ham_flags(self.flags)
+            return None
         ab = self._dev.get(device)
         if ab is None:
             if self.a is None:
@@ -243,13 +248,54 @@ class BseHamiltonian:
             cache[device] = pl
         return pl
 
+    def planes_only(self, device) -> bool:
+        return _torch().device(device) in self.__dict__.get("_planes_only", ())
+
+    def drop_blocks_for_planes(self, device) -> bool:
+        """Hold the operator on `device` as its real-split planes only: build them (they carry the
+        same 32 m^2 bytes of information) and free [A | B].  For n = 100k on one GPU, where [A | B]
+        (80 GB) and the planes (80 GB) do not both fit beside the solve's vectors, so the
+        real-split kernel runs every product (filter, RR, Lanczos) instead of 3M.  False when
+        there is no room to build the planes even transiently, or B == 0."""
+        torch = _torch()
+        device = torch.device(device)
+        if self.planes_only(device):
+            return True
+        if self.b_is_zero or not _lib.uses_rs_planes():
+            return False
+        self.flags  # noqa: B018 -- B == 0 is decided while the blocks still exist
+        torch.cuda.empty_cache()
+        if self.device_rs_planes(device) is None:
+            return False
+        self._dev.pop(device, None)
+        self.__dict__.get("_sd", {}).pop(device, None)
+        self.__dict__.get("_p64", {}).pop(device, None)
+        self.__dict__.setdefault("_planes_only", set()).add(device)
+        torch.cuda.empty_cache()
+        return True
+
     def release_device(self) -> None:
         for cache in ("_sd", "_p64", "_rs"):
             self.__dict__.get(cache, {}).clear()
         if self.a is not None:
             self._dev.clear()
+            self.__dict__.get("_planes_only", set()).clear()
 
     def host_blocks(self) -> tuple[np.ndarray, np.ndarray]:
+        if self.a is None and not self._dev and self.__dict__.get("_planes_only"):
+            # held as planes only: A, B back from Z, V, U, W (Ar = (V + U)/2, Br = (U - V)/2,
+            # Ai = (Z + W)/2, Bi = (Z - W)/2) -- equal to the original blocks to rounding
+            dev = next(iter(self._planes_only))
+            g = self._rs[dev]
+            m = self.m
+            gm = g[:m]
+            z, v, u, w = (gm[:, q * m:(q + 1) * m] for q in range(4))
+            a = _torch().complex((v + u) * 0.5, (z + w) * 0.5)
+            b = _torch().complex((u - v) * 0.5, (z - w) * 0.5)
+            self.a = np.asfortranarray(a.T.contiguous().cpu().numpy().T)
+            self.b = np.asfortranarray(b.T.contiguous().cpu().numpy().T)
+            self.a.flags.writeable = False
+            self.b.flags.writeable = False
         if self.a is None:
             ab = next(iter(self._dev.values()))
             m = self.m

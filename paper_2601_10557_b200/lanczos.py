@@ -48,9 +48,16 @@ def _sweep(ham: BseHamiltonian, start: np.ndarray, steps: int, ledger):
     betas = np.zeros(max(steps - 1, 1))
     count = ctypes.c_int(0)
     st = np.ascontiguousarray(start, dtype=np.complex128)
-    _lib.Context.get(dev.index).call(
-        "bse_lanczos_sweep", _lib.dptr(ab), ld_of(ab), ham.m, st.ctypes.data_as(ctypes.c_void_p), steps,
-        _lib.hptr(alphas), _lib.hptr(betas), ctypes.byref(count))
+    ctx = _lib.Context.get(dev.index)
+    g = ham.device_rs_planes(dev) if ab is None else None  # planes-only operator: matvecs on the planes
+    try:
+        if g is not None:
+            ctx.call("bse_set_rs_planes", None, ham.m, _lib.dptr(g), g.stride(1))
+        ctx.call("bse_lanczos_sweep", _lib.dptr(ab), ld_of(ab) if ab is not None else ham.m, ham.m,
+                 st.ctypes.data_as(ctypes.c_void_p), steps, _lib.hptr(alphas), _lib.hptr(betas), ctypes.byref(count))
+    finally:
+        if g is not None:
+            ctx.call("bse_set_rs_planes", None, 0, None, 0)
     na = count.value
     # one H product for the start plus one per completed step (lanczos.py:58, 76)
     if ledger is not None:

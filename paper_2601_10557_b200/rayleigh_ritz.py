@@ -78,10 +78,10 @@ def _rr(entry: str, variant: str, ham: BseHamiltonian, q, ledger, fused_residual
         cap = torch.zeros(4 * k * k + (k + 1) // 2, dtype=torch.complex128, device=q.device)
         ctx.call("bse_set_rr_capture", _lib.dptr(cap))
     try:
-        if g is not None:
+        if g is not None:  # ab is None when the operator is held as planes only
             ctx.call("bse_set_rs_planes", _lib.dptr(ab), ham.m, _lib.dptr(g), g.stride(1))
-        ctx.call(entry, _lib.dptr(ab), sd, ld_of(ab), ham.m, _lib.dptr(q), ld_of(q), k, _lib.hptr(lam), _lib.dptr(vout),
-                 ld_of(vout), ctypes.byref(lmm), *extra)
+        ctx.call(entry, _lib.dptr(ab), sd, ld_of(ab) if ab is not None else ham.m, ham.m, _lib.dptr(q), ld_of(q), k,
+                 _lib.hptr(lam), _lib.dptr(vout), ld_of(vout), ctypes.byref(lmm), *extra)
     finally:
         if g is not None:
             ctx.call("bse_set_rs_planes", None, 0, None, 0)
@@ -140,6 +140,9 @@ def residuals_device(ham: BseHamiltonian, values: np.ndarray, vectors, ledger=No
     out = np.zeros(k)
     lam = np.ascontiguousarray(values, dtype=np.float64)
     ab = ham.device_blocks(vectors.device)
+    if ab is None:
+        raise ValidationError("explicit residuals need the [A|B] blocks; a planes-only operator takes the fused "
+                              "residuals of the RR (BSE200_RESIDUALS=fused)")
     _lib.Context.get(vectors.device.index).call(
         "bse_residuals", _lib.dptr(ab), ld_of(ab), ham.m, _lib.dptr(vectors), ld_of(vectors), k, _lib.hptr(lam),
         _lib.hptr(out))

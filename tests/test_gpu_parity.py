@@ -620,3 +620,30 @@ def test_cli_bench_matches_reference_format(bse, tmp_path):
         gf, rf = gl.split(","), rl.split(",")
         assert gf[:2] == rf[:2] and gf[3] == rf[3], (gl, rl)  # rep, phase, modeled flops
     assert json.loads((tmp_path / "manifest.json").read_text())["command"] == "bench"
+
+
+def test_planes_only_operator_solve(bse):
+    """The operator held as its real-split planes only (drop_blocks_for_planes: n = 100k on one GPU,
+    where [A|B] and the planes do not both fit): Lanczos (k = 1 matvecs), filter, RR and fused
+    residuals all on the planes; same results as with [A|B] kept, and A, B recoverable from the
+    planes to rounding."""
+    import torch
+
+    a, b = golden_ham(64, 21)
+    g = golden("solve_m64_s21.npz")
+    ham = bse.BseHamiltonian(a, b)
+    dev = torch.device("cuda", 0)
+    ham.device_blocks(dev)
+    assert ham.drop_blocks_for_planes(dev) and ham.planes_only(dev) and ham.device_blocks(dev) is None
+    r = bse.solve(ham, bse.SolverConfig(nev=8, seed=21, rel_res=True, tol=1e-12))
+    ref = bse.solve(bse.BseHamiltonian(a, b), bse.SolverConfig(nev=8, seed=21, rel_res=True, tol=1e-12))
+    assert r.iterations_used == ref.iterations_used
+    assert [t.locked for t in r.trace] == [t.locked for t in ref.trace]
+    assert np.abs(r.lambdas - ref.lambdas).max() <= 1e-12 * np.abs(ref.lambdas).max()
+    assert np.abs(r.lambdas - g["dense_lambdas"][:8]).max() <= 1e-10 * np.abs(g["dense_lambdas"][:8]).max()
+    born = bse.generate(bse.GeneratorSpec(m=64, seed=21))  # device-born: A, B come back from the planes
+    ga, gb = born.host_blocks()
+    born2 = bse.generate(bse.GeneratorSpec(m=64, seed=21))
+    assert born2.drop_blocks_for_planes(dev)
+    ra, rb = born2.host_blocks()
+    assert _rel(ra, ga) <= 1e-15 and _rel(rb, gb) <= 1e-15
