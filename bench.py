@@ -50,7 +50,7 @@ PRECISION = {"c3c64": "c64"}
 COUPLING = {"c3b0": 0.0}
 METRIC = "time-to-solution, nev eigenpairs @ n=40k; filter FP64 TFLOP/s as % of peak"
 FP64_PEAK_FILE = ROOT / "profiles" / "fp64_peak.json"
-TRAFFIC_FILE = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+TRAFFIC_FILE = ROOT / "profiles" / "r02" / "ncu_traffic.json"
 
 
 def ncu_traffic(algo: str):
@@ -203,11 +203,11 @@ def solve_trace(cfg_name: str):
 
 def cpu_reference_time(cfg_name: str, blocks=None, quick: bool = False, samples: int = 0):
     """Reference CPU time-to-solution from timed reference-path phases (oracle/cpu_model.py):
-    every phase of the reference code path timed once at the full n on this host's cores, the
-    solve's per-iteration (k, l) applied to those timings; ``samples`` further per-step samples
-    of the H application rescale the filter rate (median reported).  ``quick`` (our arm's
-    cpu_baseline leg, ~30 s): narrower calibration widths unless the reference arm cached a full
-    calibration on this host."""
+    every phase of the reference code path timed at the full n and the solve's own widths on this
+    host's cores (median of 3), the solve's per-iteration (k, l) applied to those timings;
+    ``samples`` further per-step samples of the H application rescale the filter rate (median
+    reported).  ``quick`` (our arm's cpu_baseline leg): the reference arm's cached calibration on
+    this host when present, else the same calibration with one run per timing (~1 min at C3)."""
     from oracle import cpu_model
 
     m, nev, nex, deg, tol, rel = CONFIGS[cfg_name]
@@ -226,8 +226,8 @@ def cpu_reference_time(cfg_name: str, blocks=None, quick: bool = False, samples:
         blocks = cpu_model.timing_instance(m)
     a, b = blocks
     if cal is None:
-        k_hi, k_lo, l_hi = (min(nevex, 512), 64, min(nev, 256)) if quick else (nevex, max(min(tk), 32), nev)
-        cal = cpu_model.calibrate(a, b, k_hi, k_lo, l_hi)
+        # the same widths either way (the solve's own k range); quick = one run per timing
+        cal = cpu_model.calibrate(a, b, nevex, max(min(tk), 32), nev, reps=1 if quick else None)
         cal["sample_k"] = 64
         cal["sample_s"] = cpu_model.sample_step(a, b, 64)
         cal["quick"] = quick
@@ -365,12 +365,17 @@ def run_ours(args, world, rank, local):
     barrier(world)
     torch.cuda.synchronize()
     launches0 = ctx.launches
+    profile_range = os.environ.get("BSE200_PROFILE_RANGE") == "1"  # ncu --profile-from-start off
     with ClockSampler(local) as clk:
+        if profile_range:
+            torch.cuda.profiler.start()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         results = [one_solve() for _ in range(args.steps)]
         e1.record()
         torch.cuda.synchronize()
+        if profile_range:
+            torch.cuda.profiler.stop()
         barrier(world)
     launches = ctx.launches - launches0
     step_s = e0.elapsed_time(e1) / 1e3 / args.steps

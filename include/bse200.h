@@ -57,12 +57,12 @@ const char* bse_version(void);
 /* Kernel of the Chebyshev-filter products (and of H products given sum planes): 4 = 4M split
  * (8 real DMMA per complex block pair; the context default); 3M / Gauss (6 DMMA, 25% fewer FP64
  * tensor ops, error bound ~eps (|Re|+|Im|)^2): 88 = TMA-fed producer-warp kernel
- * (the 3M default), 82 / 86 its narrow / wide tiles, 72 = cp.async + mbarrier rings,
- * 65 = cp.async + CTA barrier, 3 = sums in registers.  65-88 need the sum planes (else 3 runs);
- * all 3M codes give bitwise-identical results.  90-96: the real-split kernel (csrc/hop_rs.cuh,
- * 4 n^2 k flops per step) for bse_chebyshev_filter_rs / bse_hop_tile_rs / registered RR planes,
- * 90 = tile by block width (the Python default), 91-96 fixed tiles (bitwise identical); every
- * other product runs code 88 under them.  BSE_EVALIDATION for other codes.                     */
+ * (the 3M default), 82 / 86 its narrow / wide tiles; without the sum planes the same kernel forms
+ * the operand sums in registers (same bits).  90 / 92 / 94: the real-split kernel
+ * (csrc/hop_rs.cuh, 4 n^2 k flops per step) for bse_chebyshev_filter_rs, bse_hop_tile_rs(_t) and
+ * registered RR planes, 90 = tile by block width (the Python default), 92 / 94 fixed tiles
+ * (bitwise identical); complex-operand products run code 88 under them.  BSE_EVALIDATION for
+ * other codes.                                                                                 */
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults);
 /* Properties of the Hamiltonian the following operator calls on this context act on
  * (BSE_HAM_* flags); the Python layer sets them before every operator call.                     */

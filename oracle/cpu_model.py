@@ -82,13 +82,24 @@ def _orthonormal(n, k, seed):
     return q
 
 
-def calibrate(a, b, k_hi: int, k_lo: int, l_hi: int, *, bounds=(-1.0, 0.5, 1.0)) -> dict:
-    """Time every reference phase at the workload's full n (a, b: host blocks, F-order)."""
+def calibrate(a, b, k_hi: int, k_lo: int, l_hi: int, *, bounds=(-1.0, 0.5, 1.0), reps: int | None = None) -> dict:
+    """Time every reference phase at the workload's full n (a, b: host blocks, F-order); each timing
+    is the median of `reps` (default REPS) runs."""
+    global REPS
+    saved = REPS
+    REPS = reps or REPS
+    try:
+        return _calibrate(a, b, k_hi, k_lo, l_hi, bounds)
+    finally:
+        REPS = saved
+
+
+def _calibrate(a, b, k_hi, k_lo, l_hi, bounds):
     m = a.shape[0]
     n = 2 * m
     mu_1, cut, mu_n = bounds
     c, e = (mu_n + cut) / 2.0, (mu_n - cut) / 2.0
-    t = {"n": n, "k_hi": k_hi, "k_lo": k_lo, "l_hi": l_hi, "cores": _cores(),
+    t = {"n": n, "k_hi": k_hi, "k_lo": k_lo, "l_hi": l_hi, "cores": _cores(), "reps": REPS,
          "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS")}
     o.h_times(a, b, _block(1, n, min(k_lo, 64)))  # BLAS threads and buffers up at the full size
     t0 = _now()

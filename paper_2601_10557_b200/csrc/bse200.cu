@@ -300,8 +300,9 @@ using Hop3MWide = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 using Hop3MNarrowNP = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 0>;
 using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 
-// 90: the real-split filter (hop_rs.cuh) for bse_chebyshev_filter_rs; every other product
-// (RR's S H Q, the distributed tiles) runs code 88 under it
+// 90 (92 / 94): the real-split kernel (hop_rs.cuh) -- bse_chebyshev_filter_rs, the RR's S H Q
+// on registered planes, the grid's tile products (bse_hop_tile_rs / _rs_t); the complex-operand
+// products that remain (B = 0, no planes) run code 88 under it
 bool filter_code_needs_planes(int code) { return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94; }
 bool filter_code_valid(int code) { return code == 4 || filter_code_needs_planes(code); }
 
