@@ -18,11 +18,13 @@ The scheme of PAPER.md:723-740 (not shipped by the reference):
   term is added by one designated member, so the summed partials ARE
   Y_{j+1}: the whole recurrence is one fused DMMA GEMM + one allreduce per
   step, with two buffers (one per layout) and no copies.
-* CholQR Grams, the projection against the locked vectors, W = Q^H S H Q,
-  Q2^H Q2 and the residual norms are local partial products plus ONE
-  allreduce each; the replicas of a layout split the rows between them.  The k x k pencil (solved redundantly in PAPER.md:725) is
-  split into its two independent halves on ranks 0 and 1.  Q is allgathered
-  once per iteration for the RR; the backup projection reuses the same T.
+* CholQR Grams, the projection against the locked vectors, [W | Q2^H Q2] and
+  [column norms | residual norms] are local partial products plus ONE
+  allreduce each; the replicas of a layout split the rows between them.  The
+  k x k pencil (solved redundantly in PAPER.md:725) is split into its two
+  independent halves on ranks 0 and 1.  Q is redistributed once per iteration
+  from the col to the row layout (point-to-point inside the row group); the
+  backup projection reuses the same T.
 * The complex64 filter (configs[4]) runs the same recurrence on the tcgen05
   tile kernel: raw fp32 partials, an fp32 allreduce, then the hi/lo split.
 
@@ -520,6 +522,47 @@ class DistSolver:
             full[:, g.m + a:g.m + b] = part[:, mx:mx + b - a]
         return full
 
+    def col_to_row(self, x_col):
+        """Redistribute a col-layout block (rows C_J of both halves) to the row layout (rows R_I) --
+        ChASE's row/column redistribution: inside the row group, member j owns the
+        piece C_j ∩ R_I and sends it to the others by point-to-point NCCL, so each GPU receives
+        (m/p - |C_J ∩ R_I|) rows of each half instead of allgathering all m."""
+        g, torch = self.g, self.torch
+        k = x_col.shape[0]
+        out = torch.empty((k, 2 * g.nr), dtype=x_col.dtype, device=x_col.device)
+
+        def piece(j):  # C_j ∩ R_I in global rows
+            return max(g.ce[j], g.r0), min(g.ce[j + 1], g.r1)
+
+        lo, hi = piece(g.J)
+        mine = None
+        if hi > lo:  # my own piece: local copy, packed [upper | lower] for the sends
+            mine = torch.cat([x_col[:, lo - g.c0:hi - g.c0], x_col[:, g.nc + lo - g.c0:g.nc + hi - g.c0]], dim=1)
+            out[:, lo - g.r0:hi - g.r0] = mine[:, :hi - lo]
+            out[:, g.nr + lo - g.r0:g.nr + hi - g.r0] = mine[:, hi - lo:]
+        if g.q == 1:
+            return out
+        dist = self.c.dist
+        ops, recvs = [], []
+        for j in range(g.q):
+            if j == g.J:
+                continue
+            peer = g.I * g.q + j
+            if mine is not None:
+                ops.append(dist.P2POp(dist.isend, self.c._real(mine), peer))
+            plo, phi = piece(j)
+            if phi > plo:
+                buf = torch.empty((k, 2 * (phi - plo)), dtype=x_col.dtype, device=x_col.device)
+                ops.append(dist.P2POp(dist.irecv, self.c._real(buf), peer))
+                recvs.append((plo, phi, buf))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for plo, phi, buf in recvs:
+            out[:, plo - g.r0:phi - g.r0] = buf[:, :phi - plo]
+            out[:, g.nr + plo - g.r0:g.nr + phi - g.r0] = buf[:, phi - plo:]
+        return out
+
     def row_rows(self, full_storage):
         g, m = self.g, self.g.m
         return self.torch.cat([full_storage[:, g.r0:g.r1], full_storage[:, m + g.r0:m + g.r1]], dim=1).contiguous()
@@ -801,9 +844,8 @@ class DistSolver:
         else:
             self.forward(q_col, t_row, low_sign=-1.0, filter=True)  # T = S H Q (rows R_I), filter kernel
         st.mark("T = S H Q", k)
-        q_full = self.assemble_from_col(q_col)
-        st.mark("allgather Q", k)
-        q_rows = self.row_rows(q_full)
+        q_rows = self.col_to_row(q_col)
+        st.mark("redistribute Q (col -> row layout)", k)
         rlo, rhi = self._share(nr, "row")  # this replica's share of the rows of each half
         clo, chi = self._share(self.g.nc, "col")
         nc = self.g.nc
