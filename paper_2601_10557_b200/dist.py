@@ -1038,7 +1038,7 @@ class DistSolver:
             bounds = self.lanczos(nevex, cfg.lanczos_steps, rng.substream(cfg.seed, TAG_LANCZOS), ledger)
         st.mark("lanczos", nevex)
         normalizer = abs(bounds.mu_1) if cfg.rel_res else 1.0
-        v = start_block_col(rng.substream(cfg.seed, TAG_SUBSPACE), n, nevex, g, self.ops)
+        v = start_block_col(rng.substream(cfg.seed, TAG_SUBSPACE), n, nevex, g, self.ops, self.c)
         st.mark("start block", nevex)
         row_buf = self.ops.empty(nevex, 2 * g.nr)
         locked = self.ops.empty(nev, 2 * g.nc)
@@ -1120,20 +1120,32 @@ class DistSolver:
         return out
 
 
-def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops):
+def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops, comm: "Comm | None" = None):
     """Rows C_J of both halves of the reference start block complex_normal_matrix(seed, n, cols)
-    (solver.py:139-141): drawn bit-exactly on the host for just this rank's rows when m <=
-    EXACT_LIMIT, else the whole block on the device (generate.py's policy; bit-exact words,
-    Box-Muller within ~1 ulp) and this rank's rows sliced out (the host draw of every rank
-    competes for the same host cores: 0.77 s of a 12.8 s C3 solve at N = 4)."""
+    (solver.py:139-141), (cols, 2 nc) storage.  m <= EXACT_LIMIT: drawn bit-exactly on the host --
+    the p replicas of a column group each draw a 1/p share of the columns (two contiguous counter
+    ranges per column) and allgather them over the column communicator, so the whole grid draws the
+    block exactly once (every rank drawing its full column slice made the N = 4 C3 solve pay 0.8 s
+    of contended host time).  Above EXACT_LIMIT: the device rng (generate.py's policy)."""
     torch = ops.torch
     m = grid.m
     if m > EXACT_LIMIT and hasattr(ops, "ctx"):
         full = rng.device_complex_normal_matrix(seed, n, cols, ops.device).T  # (cols, n) storage rows
         return torch.cat([full[:, grid.c0:grid.c1], full[:, m + grid.c0:m + grid.c1]], dim=1).contiguous()
-    rows = np.concatenate([np.arange(grid.c0, grid.c1), m + np.arange(grid.c0, grid.c1)])
-    index = np.arange(cols, dtype=np.int64)[:, None] * n + rows[None, :]  # column-major fill (rng.py:78-81)
-    return torch.from_numpy(rng.complex_normals_at(seed, index)).to(ops.device)
+    share = comm is not None and grid.p > 1
+    edges = split(cols, grid.p) if share else [0, cols]
+    lo, hi = (edges[grid.I], edges[grid.I + 1]) if share else (0, cols)
+    span = -(-cols // grid.p) if share else cols  # padded share for the equal-size allgather
+    col = np.arange(lo, hi, dtype=np.int64) * n  # column-major fill (rng.py:78-81)
+    part = np.zeros((span, 2 * grid.nc), dtype=np.complex128)
+    if hi > lo and grid.nc:
+        part[:hi - lo, :grid.nc] = rng.complex_normals_segments(seed, col + grid.c0, grid.nc)
+        part[:hi - lo, grid.nc:] = rng.complex_normals_segments(seed, col + m + grid.c0, grid.nc)
+    mine = torch.from_numpy(part).to(ops.device)
+    if not share:
+        return mine[:cols].contiguous() if span != cols else mine
+    parts = comm.gather(mine, "col")
+    return torch.cat([pt[:edges[i + 1] - edges[i]] for i, pt in enumerate(parts)], dim=0).contiguous()
 
 
 class DistributedSolver:

@@ -78,6 +78,29 @@ def complex_normals(seed: int, count: int, start_index: int = 0, threads: int | 
     return out
 
 
+def complex_normals_segments(seed: int, starts, length: int, threads: int | None = None) -> np.ndarray:
+    """Row r = normals starts[r] .. starts[r] + length - 1 (equal-length contiguous counter ranges,
+    e.g. a row block of a column-major matrix): bit-identical to complex_normals there, computed
+    range by range on all host cores (no per-element index arithmetic)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    starts = [int(x) for x in np.ravel(starts)]
+    out = np.empty((len(starts), length), dtype=np.complex128)
+    if not starts or not length:
+        return out
+    per = max(1, _CHUNK // length)  # segments per task: ~_CHUNK normals of work each
+
+    def work(a):
+        for r in range(a, min(a + per, len(starts))):
+            out[r] = _normals_serial(seed, length, starts[r])
+
+    nt = threads or min(64, os.cpu_count() or 1)
+    with ThreadPoolExecutor(nt) as ex:
+        list(ex.map(work, range(0, len(starts), per)))
+    return out
+
+
 def _normals_at(seed: int, index: np.ndarray) -> np.ndarray:
     """Normals with arbitrary (int64) indices: the same counter arithmetic element by element."""
     ctr = np.empty(2 * index.size, dtype=_U64)
