@@ -115,3 +115,15 @@ def test_c2_parity_grid_path_against_reference(bse):
                            seed=int(g["seed"]), rel_res=bool(g["rel_res"]))
     res = ds.solve(cfg)
     check_result(res, g)
+
+
+def test_c3_parity_against_reference(bse):
+    """C3 (BASELINE.json configs[2], the headline): n = 40k, nev 1000, nex 200 on 1 GPU, against the
+    reference's own C3 solve (hours on the build container's 8 cores)."""
+    g = _load("c3")
+    ham = bse.generate(bse.GeneratorSpec(m=int(g["m"]), seed=0))
+    check_instance(ham, g)
+    cfg = bse.SolverConfig(nev=int(g["nev"]), nex=int(g["nex"]), deg=int(g["deg"]), tol=float(g["tol"]),
+                           seed=int(g["seed"]), rel_res=bool(g["rel_res"]))
+    res = bse.solve(ham, cfg)
+    check_result(res, g)
