@@ -58,6 +58,17 @@ struct bse_ctx {
   unsigned ham_flags = 0;  // BSE_HAM_B_ZERO: operator calls skip the B half of the contraction
   void* gv = nullptr;  // split-K GEMV partials
   size_t gv_bytes = 0;
+  // second stream + cuSOLVER handle: the RR pencil's eigenvalues of M run beside chol(W) -> eigh(G)
+  cudaStream_t aux = nullptr;
+  cusolverDnHandle_t aux_solver = nullptr;
+  cusolverDnParams_t aux_params = nullptr;
+  void* aux_dws = nullptr;
+  size_t aux_dws_bytes = 0;
+  void* aux_hws = nullptr;
+  size_t aux_hws_bytes = 0;
+  double* aux_pinned = nullptr;
+  size_t aux_pinned_count = 0;
+  cudaEvent_t aux_ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -774,6 +785,59 @@ int cholqr_device(bse_ctx* ctx, zval* q, int64_t n, int64_t k, int64_t ldq, Scra
   return 1;
 }
 
+// Eigenvalues (no vectors) of the hermitian k x k `src`, computed on the context's second stream
+// after the main stream reaches this point; the values and info land in pinned host memory.
+// aux_eigvalsh_wait() joins and returns them.
+void aux_eigvalsh_start(bse_ctx* ctx, const zval* src, zval* a, double* d_w, int* d_info, int k) {
+  if (!ctx->aux) {
+    CUDA_OK(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    SOLVER_OK(cusolverDnCreate(&ctx->aux_solver));
+    SOLVER_OK(cusolverDnCreateParams(&ctx->aux_params));
+    SOLVER_OK(cusolverDnSetStream(ctx->aux_solver, ctx->aux));
+    for (cudaEvent_t& e : ctx->aux_ev) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  CUDA_OK(cudaEventRecord(ctx->aux_ev[0], ctx->stream));
+  CUDA_OK(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0));
+  CUDA_OK(cudaMemcpyAsync(a, src, (size_t)k * k * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->aux));
+  size_t dws = 0, hws = 0;
+  SOLVER_OK(cusolverDnXsyevd_bufferSize(ctx->aux_solver, ctx->aux_params, CUSOLVER_EIG_MODE_NOVECTOR,
+                                        CUBLAS_FILL_MODE_LOWER, k, CUDA_C_64F, a, k, CUDA_R_64F, d_w, CUDA_C_64F, &dws,
+                                        &hws));
+  dws = std::max<size_t>(dws, 256);
+  if (ctx->aux_dws_bytes < dws) {
+    CUDA_OK(cudaStreamSynchronize(ctx->aux));
+    if (ctx->aux_dws) CUDA_OK(cudaFree(ctx->aux_dws));
+    CUDA_OK(cudaMalloc(&ctx->aux_dws, dws));
+    ctx->aux_dws_bytes = dws;
+  }
+  if (ctx->aux_hws_bytes < std::max<size_t>(hws, 16)) {
+    free(ctx->aux_hws);
+    ctx->aux_hws = malloc(std::max<size_t>(hws, 16));
+    ctx->aux_hws_bytes = std::max<size_t>(hws, 16);
+  }
+  if (ctx->aux_pinned_count < (size_t)k + 1) {
+    if (ctx->aux_pinned) CUDA_OK(cudaFreeHost(ctx->aux_pinned));
+    ctx->aux_pinned = nullptr;
+    CUDA_OK(cudaMallocHost(&ctx->aux_pinned, (k + 1) * sizeof(double)));
+    ctx->aux_pinned_count = k + 1;
+  }
+  SOLVER_OK(cusolverDnXsyevd(ctx->aux_solver, ctx->aux_params, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_LOWER, k,
+                             CUDA_C_64F, a, k, CUDA_R_64F, d_w, CUDA_C_64F, ctx->aux_dws, dws, ctx->aux_hws, hws,
+                             d_info));
+  CUDA_OK(cudaMemcpyAsync(ctx->aux_pinned, d_w, k * sizeof(double), cudaMemcpyDeviceToHost, ctx->aux));
+  CUDA_OK(cudaMemcpyAsync(ctx->aux_pinned + k, d_info, sizeof(int), cudaMemcpyDeviceToHost, ctx->aux));
+  CUDA_OK(cudaEventRecord(ctx->aux_ev[1], ctx->aux));
+}
+
+void aux_eigvalsh_wait(bse_ctx* ctx, std::vector<double>& w, int k) {
+  CUDA_OK(cudaEventSynchronize(ctx->aux_ev[1]));
+  CUDA_OK(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0));  // scratch reuse stays ordered
+  int info = 0;
+  std::memcpy(&info, ctx->aux_pinned + k, sizeof(int));
+  if (info != 0) throw BseError(BSE_ENUMERICAL, "hermitian eigensolver failed (info " + std::to_string(info) + ")");
+  w.assign(ctx->aux_pinned, ctx->aux_pinned + k);
+}
+
 // copy one k x k factor into slot `slot` of the registered capture buffer (no-op when none)
 void capture_kk(bse_ctx* ctx, int slot, const zval* src, int64_t k) {
   if (!ctx->rr_capture) return;
@@ -781,7 +845,7 @@ void capture_kk(bse_ctx* ctx, int slot, const zval* src, int64_t k) {
                           cudaMemcpyDeviceToDevice, ctx->stream));
 }
 
-size_t pencil_ws_bytes(int64_t k) { return 3 * al((size_t)k * k * sizeof(zval)) + al(k * 8) + al(k * 4) + al(64); }
+size_t pencil_ws_bytes(int64_t k) { return 3 * al((size_t)k * k * sizeof(zval)) + 2 * al(k * 8) + al(k * 4) + al(64); }
 
 // Small hermitian pencil of the oblique RR (rayleigh_ritz.py:113-137) on k x k device data:
 // w = Q^H S H Q and g2 = Q2^H Q2 (raw sums, overwritten).  Returns ascending Ritz values on the
@@ -808,22 +872,38 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   capture_kk(ctx, 0, w, k);
   capture_kk(ctx, 2, mm, k);
   std::vector<double> hw(k);
-  if (mode != 2) {
-    // :116-120  |lambda|_min(M) >= 1e-8
-    CUDA_OK(cudaMemcpyAsync(tmp, mm, kk * sizeof(zval), cudaMemcpyDeviceToDevice, ctx->stream));
-    heevd(ctx, tmp, (int)k, d_w, false, d_info);
-    to_host(ctx, hw.data(), d_w, k);
-    tm.mark("eigvalsh(M)", k);
+  // :116-120  |lambda|_min(M) >= 1e-8 -- the eigenvalues of M run on the second stream while this
+  // one factors W and solves G; the checks below keep the reference's order (M first, then the
+  // Cholesky of W, then theta ~ 0), so the same error is raised for the same input
+  bool m_pending = false;
+  auto check_m = [&]() {
+    if (!m_pending) return;
+    m_pending = false;
+    std::vector<double> wm;
+    aux_eigvalsh_wait(ctx, wm, (int)k);
     double lmm = INFINITY;
-    for (double v : hw) lmm = std::min(lmm, std::fabs(v));
+    for (double v : wm) lmm = std::min(lmm, std::fabs(v));
     if (h_lam_min_m) *h_lam_min_m = lmm;
+    tm.mark("eigvalsh(M) joined", k);
     if (mode == 1) return;
     if (!(lmm >= 1e-8))
       throw BseError(BSE_EHERMITIAN_RQ, "|lambda_min(Q*SQ)| = " + std::to_string(lmm) + " below 1e-8");
+  };
+  if (mode != 2) {
+    int* m_info = d_info + 1;
+    aux_eigvalsh_start(ctx, mm, tmp, d_w + 0, m_info, (int)k);
+    m_pending = true;
+    if (mode == 1) {
+      check_m();
+      return;
+    }
   }
+  double* d_wg = sc.take<double>(k);  // eigenvalues of G (d_w belongs to the second stream)
   // :121-126  L = chol(W)
-  if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0)
+  if (potrf(ctx, w, (int)k, CUBLAS_FILL_MODE_LOWER, d_info) != 0) {
+    check_m();
     throw BseError(BSE_EHERMITIAN_RQ, "Cholesky of Q*SHQ failed; S*H is not definite on the subspace");
+  }
   capture_kk(ctx, 1, w, k);  // L in the lower triangle (the caller drops the upper)
   // :127-129  G = L^{-1} M L^{-H}, hermitised
   const cuDoubleComplex z1 = make_cuDoubleComplex(1.0, 0.0);
@@ -837,9 +917,10 @@ void rr_pencil(bse_ctx* ctx, zval* w, zval* g2, int64_t k, double* h_lam, zval* 
   capture_kk(ctx, 3, g, k);
   tm.mark("chol(W), G = L^-1 M L^-H", k);
   // :130-133  theta, y = eigh(G); lambda = 1/theta
-  heevd(ctx, g, (int)k, d_w, true, d_info);
-  to_host(ctx, hw.data(), d_w, k);
+  heevd(ctx, g, (int)k, d_wg, true, d_info);
+  to_host(ctx, hw.data(), d_wg, k);
   tm.mark("eigh(G)", k);
+  check_m();
   double tmin = INFINITY;
   for (double v : hw) tmin = std::min(tmin, std::fabs(v));
   if (tmin < 2.220446049250313e-16) throw BseError(BSE_EHERMITIAN_RQ, "reduced spectrum touches zero; cannot invert");
@@ -1000,6 +1081,17 @@ void bse_ctx_destroy(bse_ctx* ctx) {
   if (ctx->gv) cudaFree(ctx->gv);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   free(ctx->hws);
+  if (ctx->aux) {
+    cudaStreamSynchronize(ctx->aux);
+    if (ctx->aux_dws) cudaFree(ctx->aux_dws);
+    if (ctx->aux_pinned) cudaFreeHost(ctx->aux_pinned);
+    free(ctx->aux_hws);
+    for (cudaEvent_t e : ctx->aux_ev)
+      if (e) cudaEventDestroy(e);
+    if (ctx->aux_params) cusolverDnDestroyParams(ctx->aux_params);
+    if (ctx->aux_solver) cusolverDnDestroy(ctx->aux_solver);
+    cudaStreamDestroy(ctx->aux);
+  }
   if (ctx->params) cusolverDnDestroyParams(ctx->params);
   if (ctx->solver) cusolverDnDestroy(ctx->solver);
   if (ctx->blas) cublasDestroy(ctx->blas);
@@ -1013,7 +1105,7 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     if (!filter_code_valid(complex_mults))
-      throw BseError(BSE_EVALIDATION, "filter algorithm must be 3, 4, 65, 72, 82, 86, 88 or 90-96 (include/bse200.h)");
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92 or 94 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }
