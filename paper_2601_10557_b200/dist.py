@@ -477,6 +477,8 @@ class DistSolver:
     # more (4 GPUs: filter 13.0 s chunked vs 12.5 s with the first kernels, 10.97 s vs 10.74 s with the
     # TMA kernel, profiles/r01/); BSE200_CHUNK_MIN enables it.
     CHUNK_MIN = int(__import__("os").environ.get("BSE200_CHUNK_MIN", str(1 << 30)))
+    # the start block is drawn (and the first filter run) in two column halves from this width on
+    START_SPLIT_MIN = 64
 
     def __init__(self, grid: Grid, comm: Comm, ops, fwd: Tile, trn: Tile):
         self.g, self.c, self.ops, self.fwd, self.trn = grid, comm, ops, fwd, trn
@@ -1034,11 +1036,28 @@ class DistSolver:
         cfg.validate(n)
         ledger = PhaseLedger()
         st = _Steps("solve", g.rank)
+        seed3 = rng.substream(cfg.seed, TAG_SUBSPACE)
+        host_draw = g.m <= EXACT_LIMIT or not hasattr(self.ops, "ctx")
+        pool = second = None
+        k1 = nevex
+        if host_draw:
+            # bit-exact host draw in two column halves on a helper thread: the first during the
+            # Lanczos sweep, the second during the first half's filter (columns are independent)
+            from concurrent.futures import ThreadPoolExecutor
+
+            k1 = nevex // 2 if nevex >= self.START_SPLIT_MIN else nevex
+            pool = ThreadPoolExecutor(1)
+            first = pool.submit(start_block_host, seed3, n, 0, k1, g, self.c)
+            second = pool.submit(start_block_host, seed3, n, k1, nevex, g, self.c) if k1 < nevex else None
         with ledger.timing("lanczos"):
             bounds = self.lanczos(nevex, cfg.lanczos_steps, rng.substream(cfg.seed, TAG_LANCZOS), ledger)
         st.mark("lanczos", nevex)
         normalizer = abs(bounds.mu_1) if cfg.rel_res else 1.0
-        v = start_block_col(rng.substream(cfg.seed, TAG_SUBSPACE), n, nevex, g, self.ops, self.c)
+        if host_draw:
+            v = self.ops.empty(nevex, 2 * g.nc)
+            v[:k1] = start_block_finish(first.result(), 0, k1, g, self.ops, self.c)
+        else:
+            v = start_block_col(seed3, n, nevex, g, self.ops, self.c)
         st.mark("start block", nevex)
         row_buf = self.ops.empty(nevex, 2 * g.nr)
         locked = self.ops.empty(nev, 2 * g.nc)
@@ -1059,7 +1078,13 @@ class DistSolver:
                 mixed and (not trace or trace[-1].min_res_unlocked > MIXED_SWITCH * abs(bounds.mu_1)))
             filter_precisions.append("c64" if use_c64 else "c128")
             with ledger.timing("filter"):
-                if use_c64:
+                if second is not None:  # first iteration: the start block's second half arrives meanwhile
+                    filt = self.chebyshev_c64 if use_c64 else (lambda x, f: self.chebyshev(x, f, row_buf))
+                    filt(v[:k1], fcfg)
+                    v[k1:] = start_block_finish(second.result(), k1, nevex, g, self.ops, self.c)
+                    filt(v[k1:], fcfg)
+                    second = None
+                elif use_c64:
                     self.chebyshev_c64(v, fcfg)
                 else:
                     self.chebyshev(v, fcfg, row_buf)
@@ -1084,7 +1109,8 @@ class DistSolver:
             if cnt:
                 locked[nlock:nlock + cnt].copy_(vecs[:cnt])
                 if nlock + cnt < nev:
-                    self.extend_sbasis(sbasis, nlock, locked[nlock:nlock + cnt])
+                    with ledger.timing("ortho"):  # the reference's QR of S Y_locked is ortho time
+                        self.extend_sbasis(sbasis, nlock, locked[nlock:nlock + cnt])
                 nlock += cnt
                 lvals.extend(lam[:cnt].tolist())
                 lres.extend(res[:cnt].tolist())
@@ -1110,6 +1136,8 @@ class DistSolver:
             vals = np.concatenate([lvals, lam[act][:miss]])
             blocks = torch.cat([locked[:nlock], vecs[torch.as_tensor(act[:miss], device=vecs.device)]], dim=0)
             resid = np.concatenate([lres, res[act][:miss]])
+        if pool is not None:
+            pool.shutdown(wait=False)
         st.mark("iterations", nev)
         order = np.argsort(vals, kind="stable")[:nev]
         full = self.assemble_from_col(blocks[torch.as_tensor(order, device=blocks.device)].contiguous())
@@ -1120,32 +1148,55 @@ class DistSolver:
         return out
 
 
+def _start_share(grid: Grid, c_lo: int, c_hi: int, comm) -> tuple[list, int]:
+    """Column edges of the p replicas' shares of columns [c_lo, c_hi) and the padded share width."""
+    share = comm is not None and grid.p > 1
+    edges = [c_lo + e for e in split(c_hi - c_lo, grid.p)] if share else [c_lo, c_hi]
+    span = -(-(c_hi - c_lo) // grid.p) if share else c_hi - c_lo
+    return edges, span
+
+
+def start_block_host(seed: int, n: int, c_lo: int, c_hi: int, grid: Grid, comm=None) -> np.ndarray:
+    """Host part of start_block_cols: this replica's share of columns [c_lo, c_hi), rows C_J of both
+    halves, bit-exact (two contiguous counter ranges per column, rng.py:78-81), padded to the
+    share width.  Pure numpy: safe to run on a helper thread while the GPU works."""
+    edges, span = _start_share(grid, c_lo, c_hi, comm)
+    me = grid.I if len(edges) > 2 else 0
+    lo, hi = edges[me], edges[me + 1]
+    m = grid.m
+    col = np.arange(lo, hi, dtype=np.int64) * n
+    part = np.zeros((span, 2 * grid.nc), dtype=np.complex128)
+    if hi > lo and grid.nc:
+        part[:hi - lo, :grid.nc] = rng.complex_normals_segments(seed, col + grid.c0, grid.nc)
+        part[:hi - lo, grid.nc:] = rng.complex_normals_segments(seed, col + m + grid.c0, grid.nc)
+    return part
+
+
+def start_block_finish(part: np.ndarray, c_lo: int, c_hi: int, grid: Grid, ops, comm=None):
+    """Device part: upload this replica's share and allgather the shares over the column
+    communicator (a collective: every rank calls it in the same order) -> (c_hi - c_lo, 2 nc)."""
+    torch = ops.torch
+    edges, span = _start_share(grid, c_lo, c_hi, comm)
+    mine = torch.from_numpy(part).to(ops.device)
+    if len(edges) == 2:
+        return mine[:c_hi - c_lo].contiguous() if span != c_hi - c_lo else mine
+    parts = comm.gather(mine, "col")
+    return torch.cat([pt[:edges[i + 1] - edges[i]] for i, pt in enumerate(parts)], dim=0).contiguous()
+
+
 def start_block_col(seed: int, n: int, cols: int, grid: Grid, ops, comm: "Comm | None" = None):
     """Rows C_J of both halves of the reference start block complex_normal_matrix(seed, n, cols)
     (solver.py:139-141), (cols, 2 nc) storage.  m <= EXACT_LIMIT: drawn bit-exactly on the host --
-    the p replicas of a column group each draw a 1/p share of the columns (two contiguous counter
-    ranges per column) and allgather them over the column communicator, so the whole grid draws the
-    block exactly once (every rank drawing its full column slice made the N = 4 C3 solve pay 0.8 s
-    of contended host time).  Above EXACT_LIMIT: the device rng (generate.py's policy)."""
+    the p replicas of a column group each draw a 1/p share of the columns and allgather them over the
+    column communicator, so the grid draws the block exactly once (every rank drawing its full column
+    slice made the N = 4 C3 solve pay 0.8 s of contended host time).  Above EXACT_LIMIT: the device
+    rng (generate.py's policy)."""
     torch = ops.torch
     m = grid.m
     if m > EXACT_LIMIT and hasattr(ops, "ctx"):
         full = rng.device_complex_normal_matrix(seed, n, cols, ops.device).T  # (cols, n) storage rows
         return torch.cat([full[:, grid.c0:grid.c1], full[:, m + grid.c0:m + grid.c1]], dim=1).contiguous()
-    share = comm is not None and grid.p > 1
-    edges = split(cols, grid.p) if share else [0, cols]
-    lo, hi = (edges[grid.I], edges[grid.I + 1]) if share else (0, cols)
-    span = -(-cols // grid.p) if share else cols  # padded share for the equal-size allgather
-    col = np.arange(lo, hi, dtype=np.int64) * n  # column-major fill (rng.py:78-81)
-    part = np.zeros((span, 2 * grid.nc), dtype=np.complex128)
-    if hi > lo and grid.nc:
-        part[:hi - lo, :grid.nc] = rng.complex_normals_segments(seed, col + grid.c0, grid.nc)
-        part[:hi - lo, grid.nc:] = rng.complex_normals_segments(seed, col + m + grid.c0, grid.nc)
-    mine = torch.from_numpy(part).to(ops.device)
-    if not share:
-        return mine[:cols].contiguous() if span != cols else mine
-    parts = comm.gather(mine, "col")
-    return torch.cat([pt[:edges[i + 1] - edges[i]] for i, pt in enumerate(parts)], dim=0).contiguous()
+    return start_block_finish(start_block_host(seed, n, 0, cols, grid, comm), 0, cols, grid, ops, comm)
 
 
 class DistributedSolver:

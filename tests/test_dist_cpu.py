@@ -38,6 +38,7 @@ def _worker(rank, world, port, key, pq, out, planes=None):
     from paper_2601_10557_b200.dist import DistSolver
 
     DistSolver.CHUNK_MIN = 4  # exercise the column-chunked filter pipeline on the small cases
+    DistSolver.START_SPLIT_MIN = 4  # and the two-half start block / first filter
     from paper_2601_10557_b200.dist import DistributedSolver as DS
 
     ds = DS((a, b), device=torch.device("cpu"), grid=grid, ops=TorchOps(), planes=planes)

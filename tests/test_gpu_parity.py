@@ -647,3 +647,18 @@ def test_planes_only_operator_solve(bse):
     assert born2.drop_blocks_for_planes(dev)
     ra, rb = born2.host_blocks()
     assert _rel(ra, ga) <= 1e-15 and _rel(rb, gb) <= 1e-15
+
+
+def test_split_start_block_and_first_filter_change_no_bit(bse, monkeypatch):
+    """The start block drawn in two column halves with the first filter run per half (solver.py;
+    the host draws the second half while the GPU filters the first) gives bitwise the same solve."""
+    import paper_2601_10557_b200.solver as solver_mod
+
+    a, b = golden_ham(64, 21)
+    cfg = bse.SolverConfig(nev=8, seed=21)
+    monkeypatch.setattr(solver_mod, "START_SPLIT_MIN", 1 << 30)
+    whole = bse.solve(bse.BseHamiltonian(a, b), cfg)
+    monkeypatch.setattr(solver_mod, "START_SPLIT_MIN", 4)
+    split = bse.solve(bse.BseHamiltonian(a, b), cfg)
+    assert np.array_equal(whole.lambdas, split.lambdas) and np.array_equal(whole.v, split.v)
+    assert [t.locked for t in whole.trace] == [t.locked for t in split.trace]
