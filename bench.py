@@ -309,7 +309,24 @@ def run_ours(args, world, rank, local):
     m, nev, nex, deg, tol, rel = CONFIGS[args.config]
     n = 2 * m
     t0 = time.perf_counter()
-    ham = bse.generate(bse.GeneratorSpec(m=m, seed=0, coupling_ratio=COUPLING.get(args.config, 0.5)), device=dev)
+    spec = bse.GeneratorSpec(m=m, seed=0, coupling_ratio=COUPLING.get(args.config, 0.5))
+    if world == 1 or os.environ.get("BSE200_DIST_BACKEND", "nccl") == "gloo":
+        ham = bse.generate(spec, device=dev)
+    else:
+        # rank 0 builds the instance (host rng, device GEMM / eigensolvers) and broadcasts [A|B] over
+        # NVLink: the other ranks neither redraw 2 m^2 host normals nor rerun the eigensolvers
+        import torch.distributed as tdist
+
+        from paper_2601_10557_b200.hamiltonian import colmajor_empty
+
+        if rank == 0:
+            ham = bse.generate(spec, device=dev)
+            ab = ham.device_blocks(dev)
+        else:
+            ab = colmajor_empty(m, 2 * m, dev)
+        tdist.broadcast(torch.view_as_real(ab.T), src=0)  # (2m, m) storage: contiguous
+        if rank != 0:
+            ham = BseHamiltonian.from_device(ab, Definiteness.DEFINITE)  # rank 0 ran the certificate
     torch.cuda.synchronize()
     gen_s = time.perf_counter() - t0
     cfg = bse.SolverConfig(nev=nev, nex=nex, deg=deg, tol=tol, seed=0, rel_res=rel)
