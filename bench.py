@@ -207,7 +207,7 @@ def cpu_reference_time(cfg_name: str, blocks=None, quick: bool = False, samples:
     host's cores (median of 3), the solve's per-iteration (k, l) applied to those timings;
     ``samples`` further per-step samples of the H application rescale the filter rate (median
     reported).  ``quick`` (our arm's cpu_baseline leg): the reference arm's cached calibration on
-    this host when present, else the same calibration with one run per timing (~1 min at C3)."""
+    this host when present, else the same calibration (~3 min at C3 on 16 cores)."""
     from oracle import cpu_model
 
     m, nev, nex, deg, tol, rel = CONFIGS[cfg_name]
@@ -226,8 +226,8 @@ def cpu_reference_time(cfg_name: str, blocks=None, quick: bool = False, samples:
         blocks = cpu_model.timing_instance(m)
     a, b = blocks
     if cal is None:
-        # the same widths either way (the solve's own k range); quick = one run per timing
-        cal = cpu_model.calibrate(a, b, nevex, max(min(tk), 32), nev, reps=1 if quick else None)
+        # the same calibration as the reference arm (the solve's own widths, medians of 3)
+        cal = cpu_model.calibrate(a, b, nevex, max(min(tk), 32), nev)
         cal["sample_k"] = 64
         cal["sample_s"] = cpu_model.sample_step(a, b, 64)
         cal["quick"] = quick

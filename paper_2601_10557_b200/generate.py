@@ -144,6 +144,9 @@ def generate(spec: GeneratorSpec, device=None, exact: bool | None = None) -> Bse
             b.copy_(tmp.view(m, m).T)  # column-major B0
             ctx.call("bse_scale_shift", _lib.dptr(b), m, m, float(scale), 0.0, 0)
         del tmp
+        # release the m^2 scratch now: a cached segment later partly reused by small tensors can no
+        # longer be returned, which is what kept n = 100k from building its planes on one GPU
+        torch.cuda.empty_cache()
         if pool is not None:
             pool.shutdown()
         definite = Definiteness.UNKNOWN

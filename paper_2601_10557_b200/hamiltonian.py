@@ -446,6 +446,11 @@ def is_definite(ham: BseHamiltonian) -> Definiteness:
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device())
     ab = ham.device_blocks(dev)
+    if ab is None:  # held as planes only: a temporary [A|B] (host copy, or rebuilt from the planes)
+        a, b = ham.host_blocks()
+        ab = colmajor_empty(ham.m, 2 * ham.m, dev)
+        ab[:, :ham.m].copy_(torch.from_numpy(np.asfortranarray(a)))
+        ab[:, ham.m:].copy_(torch.from_numpy(np.asfortranarray(b)))
     import ctypes
 
     flag = ctypes.c_int(0)
