@@ -1167,8 +1167,13 @@ def start_block_host(seed: int, n: int, c_lo: int, c_hi: int, grid: Grid, comm=N
     col = np.arange(lo, hi, dtype=np.int64) * n
     part = np.zeros((span, 2 * grid.nc), dtype=np.complex128)
     if hi > lo and grid.nc:
-        part[:hi - lo, :grid.nc] = rng.complex_normals_segments(seed, col + grid.c0, grid.nc)
-        part[:hi - lo, grid.nc:] = rng.complex_normals_segments(seed, col + m + grid.c0, grid.nc)
+        # the host's cores are shared by the ranks on this node (and each rank's driving thread)
+        import os
+
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        nt = max(1, (os.cpu_count() or 1) // max(local, 1) - (1 if local > 1 else 0))
+        part[:hi - lo, :grid.nc] = rng.complex_normals_segments(seed, col + grid.c0, grid.nc, threads=nt)
+        part[:hi - lo, grid.nc:] = rng.complex_normals_segments(seed, col + m + grid.c0, grid.nc, threads=nt)
     return part
 
 
