@@ -56,6 +56,7 @@ struct bse_ctx {
   void* sws = nullptr;  // persistent cuSOLVER device workspace (grows, never shrinks)
   size_t sws_bytes = 0;
   unsigned ham_flags = 0;  // BSE_HAM_B_ZERO: operator calls skip the B half of the contraction
+  int rs_group_rows = 0;  // real-split CTA raster (hop_rs.cuh): BSE200_RS_GROUP_ROWS, 0 = columns fastest
   void* gv = nullptr;  // split-K GEMV partials
   size_t gv_bytes = 0;
   // second stream + cuSOLVER handle: the RR pencil's eigenvalues of M run beside chol(W) -> eigh(G)
@@ -370,7 +371,9 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
   mp.x[1] = map2d_f64(a.x2, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
   const int nbm = (a.mr + C::BM - 1) / C::BM;
   dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm);
-  bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(a, mp);
+  bse::HopArgs ar = a;
+  ar.group_rows = ctx->rs_group_rows;
+  bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(ar, mp);
   check_launch(ctx);
 }
 
@@ -1059,6 +1062,7 @@ int bse_ctx_create(int device, bse_ctx** out) {
   *out = nullptr;
   bse_ctx* ctx = new bse_ctx();
   ctx->device = device;
+  if (const char* g = std::getenv("BSE200_RS_GROUP_ROWS")) ctx->rs_group_rows = std::max(0, std::atoi(g));
   try {
     CUDA_OK(cudaSetDevice(device));
     BLAS_OK(cublasCreate(&ctx->blas));

@@ -54,6 +54,7 @@ struct HopArgs {
   // input block shares with its output block in the 2D layout); per-column shifts when set
   int shift_lo, shift_hi;
   const double* shift_col;
+  int group_rows;  // real-split kernel CTA raster (hop_rs.cuh); 0 = column tiles fastest
   // residual mode
   const double* lam;  // per column
   double* partial;    // [gridDim.y][k]

@@ -143,9 +143,22 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % C::WARPS_M, wn = warp / C::WARPS_M;
   const int nbm = (a.mr + C::BM - 1) / C::BM;
-  const int h = blockIdx.y >= nbm;  // output half: 0 -> x', 1 -> y'
-  const int i0 = (blockIdx.y - h * nbm) * C::BM;
-  const int c0 = blockIdx.x * C::BN;
+  // CTA raster: by default column tiles run fastest (the CTAs of one plane strip run together); with
+  // GROUP_ROWS > 0 the launch order walks GROUP_ROWS row tiles per column tile first, so a wave spans
+  // fewer column tiles of X (X is re-streamed once per wave: the bulk of the DRAM traffic)
+  int row_tile = blockIdx.y, col_tile = blockIdx.x;
+  if (a.group_rows > 0) {
+    const int ncol = gridDim.x, nrow = gridDim.y;
+    const int pid = blockIdx.y * ncol + blockIdx.x;
+    const int per_group = a.group_rows * ncol;
+    const int grp = pid / per_group, first = grp * a.group_rows;
+    const int rows_here = min(a.group_rows, nrow - first);
+    row_tile = first + (pid % per_group) % rows_here;
+    col_tile = (pid % per_group) / rows_here;
+  }
+  const int h = row_tile >= nbm;  // output half: 0 -> x', 1 -> y'
+  const int i0 = (row_tile - h * nbm) * C::BM;
+  const int c0 = col_tile * C::BN;
   const int nkt_part = (a.kc + C::BK - 1) / C::BK;
   const int nkt = 2 * nkt_part;
 
