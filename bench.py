@@ -151,9 +151,12 @@ def dist_setup():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # NCCL communicator init lines (rank count, NVLS / P2P transports) go to the log
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        # NCCL communicator init lines (rank count, NVLS / P2P transports) go to the log -- stderr, so
+        # rank 0's stdout carries only the JSON line (an image default of NCCL_DEBUG=VERSION is raised)
+        if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
+            os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if os.environ.get("BSE200_DIST_BACKEND", "nccl") == "gloo":
             # test only: more ranks than GPUs (the 2 x 4 grid of an 8-GPU box on 4 GPUs); not a bench number
             local = local % torch.cuda.device_count()
