@@ -151,12 +151,14 @@ def dist_setup():
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # NCCL communicator init lines (rank count, NVLS / P2P transports) go to the log -- stderr, so
-        # rank 0's stdout carries only the JSON line (an image default of NCCL_DEBUG=VERSION is raised)
+        # NCCL communicator init lines (rank count, transports): NCCL_DEBUG=INFO / SUBSYS=INIT into
+        # per-process files, which rank 0 echoes to stderr (nccl_init_lines) so stdout carries only the
+        # JSON line; an image default of NCCL_DEBUG=VERSION is raised
         if os.environ.get("NCCL_DEBUG", "").upper() not in ("INFO", "TRACE"):
             os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        os.environ.setdefault("NCCL_DEBUG_FILE", str(NCCL_LOG_DIR / "nccl_init.%h.%p.log"))
+        NCCL_LOG_DIR.mkdir(parents=True, exist_ok=True)
         if os.environ.get("BSE200_DIST_BACKEND", "nccl") == "gloo":
             # test only: more ranks than GPUs (the 2 x 4 grid of an 8-GPU box on 4 GPUs); not a bench number
             local = local % torch.cuda.device_count()
@@ -188,6 +190,22 @@ def max_over_ranks(x: float, world: int) -> float:
 
 # ----------------------------------------------------------------------------- CPU arms
 CACHE = ROOT / ".bench_cache"
+NCCL_LOG_DIR = ROOT / ".bench_cache" / "nccl" / (os.environ.get("TORCHELASTIC_RUN_ID", "")
+                                                  + "-" + os.environ.get("MASTER_PORT", ""))
+
+
+def nccl_init_lines(world: int) -> dict | None:
+    """The NCCL communicator init lines of this run's ranks (NCCL_DEBUG_FILE), echoed to stderr."""
+    if world == 1:
+        return None
+    lines = []
+    for p in sorted(NCCL_LOG_DIR.glob("nccl_init.*.log")):
+        lines += [ln.rstrip() for ln in p.read_text(errors="replace").splitlines()
+                  if "Init COMPLETE" in ln or " nRanks " in ln]
+    for ln in lines:
+        print(ln, file=sys.stderr)
+    ranks = sorted({int(x) for ln in lines for x in __import__("re").findall(r"nranks (\d+)", ln)})
+    return {"comm_sizes_seen": ranks, "init_complete_lines": sum("Init COMPLETE" in ln for ln in lines)}
 
 
 def cores() -> int:
@@ -513,6 +531,7 @@ def run_ours(args, world, rank, local):
                       "e2e_max_dlambda_rel": float(np.max(np.abs(r_e2e.lambdas - res.lambdas) / np.abs(res.lambdas)))},
             "parity_vs_reference": parity,
             "is_definite": defin,
+            "nccl": nccl_init_lines(world),
             "memory": {"operator_gb_per_gpu": round(op_bytes / 1e9, 3) if op_bytes else None,
                        "peak_allocated_gb_max_over_ranks": round(peak_gb, 2),
                        "note": "operator = one tile's real-split planes, 32 m^2/(p q) bytes (N > 1); "
