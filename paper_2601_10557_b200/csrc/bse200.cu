@@ -56,7 +56,7 @@ struct bse_ctx {
   void* sws = nullptr;  // persistent cuSOLVER device workspace (grows, never shrinks)
   size_t sws_bytes = 0;
   unsigned ham_flags = 0;  // BSE_HAM_B_ZERO: operator calls skip the B half of the contraction
-  int rs_group_rows = 0;  // real-split CTA raster (hop_rs.cuh): BSE200_RS_GROUP_ROWS, 0 = columns fastest
+  int rs_group_rows = 8;  // real-split CTA raster (hop_rs.cuh): BSE200_RS_GROUP_ROWS, 0 = columns fastest
   void* gv = nullptr;  // split-K GEMV partials
   size_t gv_bytes = 0;
   // second stream + cuSOLVER handle: the RR pencil's eigenvalues of M run beside chol(W) -> eigh(G)
