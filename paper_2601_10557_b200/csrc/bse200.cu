@@ -315,9 +315,7 @@ using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 // 90 (92 / 94): the real-split kernel (hop_rs.cuh) -- bse_chebyshev_filter_rs, the RR's S H Q
 // on registered planes, the grid's tile products (bse_hop_tile_rs / _rs_t); the complex-operand
 // products that remain (B = 0, no planes) run code 88 under it
-bool filter_code_needs_planes(int code) {
-  return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 93 || code == 94 || code == 95;
-}
+bool filter_code_needs_planes(int code) { return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94 || code == 96; }
 bool filter_code_valid(int code) { return code == 4 || filter_code_needs_planes(code); }
 
 // Chebyshev-step products, as selected by bse_set_filter_algorithm
@@ -348,15 +346,14 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
 }
 
 // ---- real-split filter (hop_rs.cuh) ----
-// tiles (codes for bse_set_filter_algorithm; 90 picks 92 from 512 columns, else 94;
-// profiles/r01/tune_rs.txt: 223 / 60 / 24 ms per C3 step at k = 1200 / 300 / 100 vs 346 / 91 / 33 for 3M;
-// the dominated 128 x 64, 64 x 64, BK = 32 and 8-stage tiles of round 1 are retired):
-//   92  128 x 32, 8 consumer warps of 32 x 16, 6 stages
-//   94  64 x 32, 8 consumer warps of 16 x 16, 5 stages, 2 CTAs / SM
+// tiles (codes for bse_set_filter_algorithm; 90 picks 96 from 300 columns, else 94):
+//   96  128 x 32, 4 consumer warps of 32 x 32 (32 DMMA per 8 fragment loads), 3 stages, 2 CTAs / SM
+//       -- 95.3% of the DMMA peak at k = 1200 in both directions (profiles/r02/rs_tall4_*.txt)
+//   92  128 x 32, 8 consumer warps of 32 x 16, 6 stages, 1 CTA / SM (round-1 default: 92.6%)
+//   94  64 x 32, 8 consumer warps of 16 x 16, 5 stages, 2 CTAs / SM (the faster one below ~300 columns)
 using RsTall = bse::RsCfg<128, 32, 16, 4, 2, 6, 1>;
 using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
-// experiment: 4 consumer warps of 32 x 32 (twice the DMMAs per fragment load), 2 CTAs / SM
-using RsTall4 = bse::RsCfg<128, 32, 16, 4, 4, 4, 2>;
+using RsTall4 = bse::RsCfg<128, 32, 16, 4, 4, 3, 2>;
 
 // TRANS: the transposed-tile product on the same planes (hop_rs.cuh header): a.mr output rows
 // = plane columns, a.kc contraction = plane rows; the planes are read through K-major boxes.
@@ -382,18 +379,17 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
 }
 
 // one real-split product (folded input x1 / x2, output halves y1 / y2) on the tile's planes g
-// 128 x 32 tiles read their fragments through generic loads, 64 x 32 through LDS (the faster of
-// each, profiles/r02/rs_consumer_variants_*.txt; bitwise identical)
+// 128 x 32 / 8-warp tiles read their fragments through generic loads, the others through LDS (the
+// faster of each, profiles/r02/rs_consumer_variants_*.txt, rs_tall4_*.txt; all bitwise identical)
 template <bool TRANS = false>
 void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   switch (ctx->filter_cm) {
     case 92: launch_rs<RsTall, TRANS, true>(ctx, a, g, ldg); break;
     case 94: launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg); break;
-    case 93: launch_rs<RsTall4, TRANS, true>(ctx, a, g, ldg); break;
-    case 95: launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg); break;
+    case 96: launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg); break;
     default:
-      if (a.k >= 512)
-        launch_rs<RsTall, TRANS, true>(ctx, a, g, ldg);
+      if (a.k >= 300)
+        launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg);
       else
         launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg);
   }
@@ -1115,7 +1111,7 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     if (!filter_code_valid(complex_mults))
-      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92 or 94 (include/bse200.h)");
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92, 94 or 96 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }
