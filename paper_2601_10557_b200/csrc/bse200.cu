@@ -315,7 +315,9 @@ using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 // 90 (92 / 94): the real-split kernel (hop_rs.cuh) -- bse_chebyshev_filter_rs, the RR's S H Q
 // on registered planes, the grid's tile products (bse_hop_tile_rs / _rs_t); the complex-operand
 // products that remain (B = 0, no planes) run code 88 under it
-bool filter_code_needs_planes(int code) { return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94 || code == 96; }
+bool filter_code_needs_planes(int code) {
+  return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94 || code == 96 || code == 97;
+}
 bool filter_code_valid(int code) { return code == 4 || filter_code_needs_planes(code); }
 
 // Chebyshev-step products, as selected by bse_set_filter_algorithm
@@ -354,6 +356,7 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
 using RsTall = bse::RsCfg<128, 32, 16, 4, 2, 6, 1>;
 using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
 using RsTall4 = bse::RsCfg<128, 32, 16, 4, 4, 3, 2>;
+using RsTall4K32 = bse::RsCfg<128, 32, 32, 4, 4, 2, 2>;  // experiment: BK = 32, double buffered
 
 // TRANS: the transposed-tile product on the same planes (hop_rs.cuh header): a.mr output rows
 // = plane columns, a.kc contraction = plane rows; the planes are read through K-major boxes.
@@ -387,6 +390,7 @@ void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ld
     case 92: launch_rs<RsTall, TRANS, true>(ctx, a, g, ldg); break;
     case 94: launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg); break;
     case 96: launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg); break;
+    case 97: launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg); break;
     default:
       if (a.k >= 300)
         launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg);
