@@ -127,7 +127,7 @@ _lib = None
 _lock = threading.Lock()
 # Chebyshev-filter product kernels (bse_set_filter_algorithm codes)
 _ALGOS = {"4m": 4, "3m": 88, "3m-tma-narrow": 82, "3m-tma-wide": 86, "rs": 90, "rs-tall": 92, "rs-narrow": 94,
-          "rs-tall4": 96}
+          "rs-tall4": 96, "rs-tall4-k32": 97}
 # BSE200_FILTER=3m / 4m select the Gauss 3M / plain 4M complex splits for the filter;
 # default "rs": the real-split filter (csrc/hop_rs.cuh, 4 n^2 k executed flops per step) for every
 # filter product with B != 0 (single GPU and both directions of the 2D grid) and the RR's
@@ -137,7 +137,7 @@ _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "rs").lower()]
 
 def set_filter_algorithm(name: str) -> None:
     """'rs' (default: the real-split planes of csrc/hop_rs.cuh, half the FP64 tensor ops of 4M;
-    fixed tiles 'rs-tall4' / 'rs-tall' / 'rs-narrow', bitwise identical), '3m' (Gauss split, 25% fewer FP64
+    fixed tiles 'rs-tall4-k32' / 'rs-tall4' / 'rs-tall' / 'rs-narrow', bitwise identical), '3m' (Gauss split, 25% fewer FP64
     tensor ops than 4M, operand sums precomputed once, TMA-fed producer-warp kernel; fixed tiles
     '3m-tma-narrow' / '3m-tma-wide', bitwise identical) or '4m'."""
     global _FILTER_CM
@@ -172,8 +172,8 @@ def uses_sum_planes() -> bool:
 
 
 def uses_rs_planes() -> bool:
-    """real-split filter (codes 90, 92, 94, 96; csrc/hop_rs.cuh); B = 0 products run the 3M kernel (88)"""
-    return _FILTER_CM in (90, 92, 94, 96)
+    """real-split filter (codes 90, 92, 94, 96, 97; csrc/hop_rs.cuh); B = 0 products run the 3M kernel (88)"""
+    return _FILTER_CM in (90, 92, 94, 96, 97)
 
 
 def load() -> C.CDLL:

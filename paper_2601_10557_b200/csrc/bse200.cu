@@ -348,15 +348,29 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
 }
 
 // ---- real-split filter (hop_rs.cuh) ----
-// tiles (codes for bse_set_filter_algorithm; 90 picks 96 from 300 columns, else 94):
-//   96  128 x 32, 4 consumer warps of 32 x 32 (32 DMMA per 8 fragment loads), 3 stages, 2 CTAs / SM
-//       -- 95.3% of the DMMA peak at k = 1200 in both directions (profiles/r02/rs_tall4_*.txt)
+// tiles (codes for bse_set_filter_algorithm; 90 picks 97 or 94 by the wave estimate below):
+//   97  128 x 32, 4 consumer warps of 32 x 32, BK = 32 double buffered, 2 CTAs / SM -- 96.8% of the
+//       DMMA peak at m = 20k, k = 1200 in both directions (profiles/r02/rs_tall4_bk32.txt)
+//   96  the same with BK = 16, 3 stages (95.3%)
 //   92  128 x 32, 8 consumer warps of 32 x 16, 6 stages, 1 CTA / SM (round-1 default: 92.6%)
-//   94  64 x 32, 8 consumer warps of 16 x 16, 5 stages, 2 CTAs / SM (the faster one below ~300 columns)
+//   94  64 x 32, 8 consumer warps of 16 x 16, 5 stages, 2 CTAs / SM: twice the CTAs, so the better
+//       one when the 128-row tile leaves a short last wave (small k or small tiles of the 2D grid)
 using RsTall = bse::RsCfg<128, 32, 16, 4, 2, 6, 1>;
 using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
 using RsTall4 = bse::RsCfg<128, 32, 16, 4, 4, 3, 2>;
-using RsTall4K32 = bse::RsCfg<128, 32, 32, 4, 4, 2, 2>;  // experiment: BK = 32, double buffered
+using RsTall4K32 = bse::RsCfg<128, 32, 32, 4, 4, 2, 2>;
+
+// Default tile: the 128-row 4-warp tile runs at ~96.8% of the DMMA peak in full waves, the 64-row
+// tile at ~93.5%; each is discounted by the fill of its last wave (2 resident CTAs per SM)
+bool rs_wide_tile(int64_t rows, int64_t k) {
+  const double slots = 148.0 * 2;
+  const double col = double((k + 31) / 32);
+  auto fill = [&](int64_t bm) {
+    const double waves = col * 2.0 * double((rows + bm - 1) / bm) / slots;
+    return waves / std::ceil(waves);
+  };
+  return 0.968 * fill(128) >= 0.935 * fill(64);
+}
 
 // TRANS: the transposed-tile product on the same planes (hop_rs.cuh header): a.mr output rows
 // = plane columns, a.kc contraction = plane rows; the planes are read through K-major boxes.
@@ -382,8 +396,8 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
 }
 
 // one real-split product (folded input x1 / x2, output halves y1 / y2) on the tile's planes g
-// 128 x 32 / 8-warp tiles read their fragments through generic loads, the others through LDS (the
-// faster of each, profiles/r02/rs_consumer_variants_*.txt, rs_tall4_*.txt; all bitwise identical)
+// the 8-warp 128 x 32 tile reads its fragments through generic loads, the others through LDS (the
+// faster of each, profiles/r02/rs_consumer_variants_*.txt, rs_tall4_*.txt); all bitwise identical
 template <bool TRANS = false>
 void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
   switch (ctx->filter_cm) {
@@ -392,8 +406,8 @@ void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ld
     case 96: launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg); break;
     case 97: launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg); break;
     default:
-      if (a.k >= 300)
-        launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg);
+      if (rs_wide_tile(a.mr, a.k))
+        launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg);
       else
         launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg);
   }
@@ -1115,7 +1129,7 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     if (!filter_code_valid(complex_mults))
-      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92, 94 or 96 (include/bse200.h)");
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92, 94, 96 or 97 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }

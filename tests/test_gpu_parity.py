@@ -324,7 +324,7 @@ def test_c1_parity(bse, c1_instance):
         assert np.abs(ov - 1).max() <= 1e-8
 
 
-@pytest.mark.parametrize("algo", ["3m", "3m-tma-narrow", "3m-tma-wide", "4m", "rs", "rs-tall4", "rs-tall", "rs-narrow"])
+@pytest.mark.parametrize("algo", ["3m", "3m-tma-narrow", "3m-tma-wide", "4m", "rs", "rs-tall4-k32", "rs-tall4", "rs-tall", "rs-narrow"])
 def test_filter_3m_accuracy_and_c1_parity(bse, c1_instance, algo):
     """3M (Gauss) filter products: the filter output within 1e-12 of the 4M result (scaled), and
     the C1 solve (abs tol 1e-10) keeps the reference's iterations +-1 and lambda to 1e-10 relative."""
@@ -414,7 +414,7 @@ def test_filter_rs_matches_3m_and_tiles_bitwise(bse):
             ctx.call("bse_chebyshev_filter", _lib.dptr(ab), _lib.dptr(sd), ld_of(ab), m, _lib.dptr(ref), 2 * m, k, 4,
                      0.5, 2.0, -3.0, _lib.dptr(work))
             outs = {}
-            for algo in ("rs", "rs-tall4", "rs-tall", "rs-narrow"):
+            for algo in ("rs", "rs-tall4-k32", "rs-tall4", "rs-tall", "rs-narrow"):
                 bse.set_filter_algorithm(algo)
                 v = v0.clone()
                 ctx.call("bse_chebyshev_filter_rs", _lib.dptr(gp), ldg, m, _lib.dptr(v), 2 * m, k, 4, 0.5, 2.0, -3.0,
