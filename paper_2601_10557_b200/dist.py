@@ -545,22 +545,28 @@ class DistSolver:
         if g.q == 1:
             return out
         dist = self.c.dist
+        # gloo has no point-to-point transport for CUDA tensors (the 8-ranks-on-4-GPUs test mode):
+        # stage those through host memory
+        staged = x_col.is_cuda and dist.get_backend() == "gloo"
+        dev = torch.device("cpu") if staged else x_col.device
+        send = mine.cpu() if (staged and mine is not None) else mine
         ops, recvs = [], []
         for j in range(g.q):
             if j == g.J:
                 continue
             peer = g.I * g.q + j
-            if mine is not None:
-                ops.append(dist.P2POp(dist.isend, self.c._real(mine), peer))
+            if send is not None:
+                ops.append(dist.P2POp(dist.isend, self.c._real(send), peer))
             plo, phi = piece(j)
             if phi > plo:
-                buf = torch.empty((k, 2 * (phi - plo)), dtype=x_col.dtype, device=x_col.device)
+                buf = torch.empty((k, 2 * (phi - plo)), dtype=x_col.dtype, device=dev)
                 ops.append(dist.P2POp(dist.irecv, self.c._real(buf), peer))
                 recvs.append((plo, phi, buf))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
         for plo, phi, buf in recvs:
+            buf = buf.to(x_col.device)
             out[:, plo - g.r0:phi - g.r0] = buf[:, :phi - plo]
             out[:, g.nr + plo - g.r0:g.nr + phi - g.r0] = buf[:, phi - plo:]
         return out
