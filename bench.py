@@ -494,7 +494,10 @@ def run_ours(args, world, rank, local):
             from paper_2601_10557_b200.dist import grid_shape
 
             p, q = grid_shape(world)
-            cfgd["parallelism"] = f"2D block grid {p}x{q} (one A/B tile per GPU), NCCL row/col allreduce"
+            backend = os.environ.get("BSE200_DIST_BACKEND", "nccl")
+            cfgd["parallelism"] = (f"2D block grid {p}x{q} (one tile of real-split planes per GPU), "
+                                   f"{'NCCL' if backend == 'nccl' else backend + ' (functional test mode)'} "
+                                   f"row/col allreduce")
         line = {
             "metric": METRIC, "value": step_s, "unit": "s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "strong",
