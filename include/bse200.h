@@ -58,11 +58,12 @@ const char* bse_version(void);
  * (8 real DMMA per complex block pair; the context default); 3M / Gauss (6 DMMA, 25% fewer FP64
  * tensor ops, error bound ~eps (|Re|+|Im|)^2): 88 = TMA-fed producer-warp kernel
  * (the 3M default), 82 / 86 its narrow / wide tiles; without the sum planes the same kernel forms
- * the operand sums in registers (same bits).  90 / 92 / 94 / 96 / 97: the real-split kernel
+ * the operand sums in registers (same bits).  90 / 92 / 94 / 96 / 97 / 98: the real-split kernel
  * (csrc/hop_rs.cuh, 4 n^2 k flops per step) for bse_chebyshev_filter_rs, bse_hop_tile_rs(_t) and
- * registered RR planes, 90 = tile by block shape (the Python default), 92 / 94 / 96 / 97 fixed tiles
- * (bitwise identical); complex-operand products run code 88 under them.  BSE_EVALIDATION for
- * other codes.                                                                                 */
+ * registered RR planes, 90 = tile and split-K factor by block shape (the Python default),
+ * 92 / 94 / 96 / 97 fixed unsplit tiles (bitwise identical), 98 = tile 97 with its K range split
+ * over 2 CTAs (env BSE200_RS_KSPLIT overrides the factor; partial sums reduced in a fixed order);
+ * complex-operand products run code 88 under them.  BSE_EVALIDATION for other codes.          */
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults);
 /* Properties of the Hamiltonian the following operator calls on this context act on
  * (BSE_HAM_* flags); the Python layer sets them before every operator call.                     */

@@ -127,7 +127,8 @@ _lib = None
 _lock = threading.Lock()
 # Chebyshev-filter product kernels (bse_set_filter_algorithm codes)
 _ALGOS = {"4m": 4, "3m": 88, "3m-tma-narrow": 82, "3m-tma-wide": 86, "rs": 90, "rs-tall": 92, "rs-narrow": 94,
-          "rs-tall4": 96, "rs-tall4-k32": 97}
+          "rs-tall4": 96, "rs-tall4-k32": 97,
+          "rs-tall4-k32-split": 98}
 # BSE200_FILTER=3m / 4m select the Gauss 3M / plain 4M complex splits for the filter;
 # default "rs": the real-split filter (csrc/hop_rs.cuh, 4 n^2 k executed flops per step) for every
 # filter product with B != 0 (single GPU and both directions of the 2D grid) and the RR's
@@ -172,8 +173,8 @@ def uses_sum_planes() -> bool:
 
 
 def uses_rs_planes() -> bool:
-    """real-split filter (codes 90, 92, 94, 96, 97; csrc/hop_rs.cuh); B = 0 products run the 3M kernel (88)"""
-    return _FILTER_CM in (90, 92, 94, 96, 97)
+    """real-split filter (codes 90, 92, 94, 96, 97, 98; csrc/hop_rs.cuh); B = 0 products run the 3M kernel (88)"""
+    return _FILTER_CM in (90, 92, 94, 96, 97, 98)
 
 
 def load() -> C.CDLL:

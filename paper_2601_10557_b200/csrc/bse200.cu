@@ -57,6 +57,7 @@ struct bse_ctx {
   size_t sws_bytes = 0;
   unsigned ham_flags = 0;  // BSE_HAM_B_ZERO: operator calls skip the B half of the contraction
   int rs_group_rows = 8;  // real-split CTA raster (hop_rs.cuh): BSE200_RS_GROUP_ROWS, 0 = columns fastest
+  int rs_ksplit = 0;      // real-split split-K: BSE200_RS_KSPLIT (0 = planned per product, rs_plan)
   void* gv = nullptr;  // split-K GEMV partials
   size_t gv_bytes = 0;
   // second stream + cuSOLVER handle: the RR pencil's eigenvalues of M run beside chol(W) -> eigh(G)
@@ -316,7 +317,8 @@ using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 // on registered planes, the grid's tile products (bse_hop_tile_rs / _rs_t); the complex-operand
 // products that remain (B = 0, no planes) run code 88 under it
 bool filter_code_needs_planes(int code) {
-  return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94 || code == 96 || code == 97;
+  return code == 82 || code == 86 || code == 88 || code == 90 || code == 92 || code == 94 || code == 96 || code == 97 ||
+         code == 98;
 }
 bool filter_code_valid(int code) { return code == 4 || filter_code_needs_planes(code); }
 
@@ -348,7 +350,7 @@ void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
 }
 
 // ---- real-split filter (hop_rs.cuh) ----
-// tiles (codes for bse_set_filter_algorithm; 90 picks 97 or 94 by the wave estimate below):
+// tiles (codes for bse_set_filter_algorithm; 90 picks 97 or 94, and a split-K factor, by rs_plan below):
 //   97  128 x 32, 4 consumer warps of 32 x 32, BK = 32 double buffered, 2 CTAs / SM -- 96.8% of the
 //       DMMA peak at m = 20k, k = 1200 in both directions (profiles/r02/rs_tall4_bk32.txt)
 //   96  the same with BK = 16, 3 stages (95.3%)
@@ -360,22 +362,61 @@ using RsNarrow = bse::RsCfg<64, 32, 16, 2, 2, 5, 2>;
 using RsTall4 = bse::RsCfg<128, 32, 16, 4, 4, 3, 2>;
 using RsTall4K32 = bse::RsCfg<128, 32, 32, 4, 4, 2, 2>;
 
-// Default tile: the 128-row 4-warp tile runs at ~96.8% of the DMMA peak in full waves, the 64-row
-// tile at ~93.5%; each is discounted by the fill of its last wave (2 resident CTAs per SM)
-bool rs_wide_tile(int64_t rows, int64_t k) {
+// Default plan: the 128-row 4-warp tile runs at ~96.8% of the DMMA peak in full waves, the 64-row
+// tile at ~93.5%; each is discounted by the fill of its last wave (2 resident CTAs per SM).  A short
+// last wave (the 10k-row tiles of a 2 x 2 grid, small k late in the solve) can instead be filled by
+// splitting each tile's K range over ksplit CTAs: the partial sums cost 2 ksplit k rows 16 B of HBM
+// traffic (written once, read once by rs_splitk_epilogue_kernel) plus one extra launch.
+struct RsPlan {
+  bool wide;
+  int ksplit;
+};
+constexpr size_t RS_SPLIT_WS_MAX = size_t(2) << 30;  // cap on the split-K partials (ctx->gv)
+
+RsPlan rs_plan(int64_t rows, int64_t kc, int64_t k, int force_split = 0) {
   const double slots = 148.0 * 2;
   const double col = double((k + 31) / 32);
-  auto fill = [&](int64_t bm) {
-    const double waves = col * 2.0 * double((rows + bm - 1) / bm) / slots;
-    return waves / std::ceil(waves);
-  };
-  return 0.968 * fill(128) >= 0.935 * fill(64);
+  const double flop_s = 16.0 * double(rows) * double(kc) * double(k) / 37.1e12;  // at the DMMA peak
+  RsPlan best{true, 1};
+  double best_t = 1e300;
+  for (int wide = 1; wide >= 0; --wide) {
+    const int64_t bm = wide ? 128 : 64;
+    const double eff = wide ? 0.968 : 0.935;
+    const int64_t nkt = 2 * ((kc + 31) / 32);  // K stages of a tile (BK 32; the 64-row tile's BK 16 doubles it)
+    for (int sp = 1; sp <= 4; ++sp) {
+      if (force_split > 0 && sp != force_split) continue;
+      if (sp > 1 && (nkt / sp < 16 || (size_t)sp * 2 * k * rows * 16 > RS_SPLIT_WS_MAX)) continue;
+      const double waves = col * 2.0 * double((rows + bm - 1) / bm) * sp / slots;
+      double t = flop_s / eff * std::ceil(waves) / waves;
+      if (sp > 1) t += (2.0 * sp * 2.0 * double(k) * double(rows) * 16.0) / 6.0e12 + 4e-6;
+      if (t < best_t * 0.995) {  // prefer the earlier (wider, unsplit) plan on near ties
+        best_t = t;
+        best = RsPlan{wide == 1, sp};
+      }
+    }
+  }
+  return best;
+}
+
+// the split-K partial buffer (shared with launch_gemv: never live at the same time)
+void* ensure_gv(bse_ctx* ctx, size_t need) {
+  if (ctx->gv_bytes < need) {
+    if (ctx->gv) {
+      CUDA_OK(cudaStreamSynchronize(ctx->stream));
+      CUDA_OK(cudaFree(ctx->gv));
+    }
+    ctx->gv = nullptr;
+    ctx->gv_bytes = 0;
+    CUDA_OK(cudaMalloc(&ctx->gv, need));
+    ctx->gv_bytes = need;
+  }
+  return ctx->gv;
 }
 
 // TRANS: the transposed-tile product on the same planes (hop_rs.cuh header): a.mr output rows
 // = plane columns, a.kc contraction = plane rows; the planes are read through K-major boxes.
 template <class C, bool TRANS = false, bool GENERIC = false>
-void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg) {
+void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg, int ksplit = 1) {
   constexpr size_t smem = C::template smem<TRANS>();
   ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS, GENERIC>, (int)smem);
   bse::RsMaps mp;
@@ -388,11 +429,21 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
   mp.x[0] = map2d_f64(a.x1, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
   mp.x[1] = map2d_f64(a.x2, 2 * (uint64_t)a.kc, a.k, a.ldx * 16, 2 * C::LDX, C::BN);
   const int nbm = (a.mr + C::BM - 1) / C::BM;
-  dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm);
+  dim3 grid((a.k + C::BN - 1) / C::BN, 2 * nbm, ksplit);
   bse::HopArgs ar = a;
   ar.group_rows = ctx->rs_group_rows;
+  ar.ksplit = ksplit;
+  ar.part_ws = nullptr;
+  if (ksplit > 1)
+    ar.part_ws = static_cast<zval*>(ensure_gv(ctx, (size_t)ksplit * 2 * a.k * a.mr * sizeof(zval)));
   bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(ar, mp);
   check_launch(ctx);
+  if (ksplit > 1) {
+    const int64_t total = 2 * (int64_t)a.k * a.mr;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    bse::rs_splitk_epilogue_kernel<<<blocks, 256, 0, ctx->stream>>>(ar);
+    check_launch(ctx);
+  }
 }
 
 // one real-split product (folded input x1 / x2, output halves y1 / y2) on the tile's planes g
@@ -405,11 +456,14 @@ void rs_product(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ld
     case 94: launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg); break;
     case 96: launch_rs<RsTall4, TRANS, false>(ctx, a, g, ldg); break;
     case 97: launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg); break;
-    default:
-      if (rs_wide_tile(a.mr, a.k))
-        launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg);
+    case 98: launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg, ctx->rs_ksplit > 1 ? ctx->rs_ksplit : 2); break;
+    default: {
+      const RsPlan p = rs_plan(a.mr, a.kc, a.k, ctx->rs_ksplit);
+      if (p.wide)
+        launch_rs<RsTall4K32, TRANS, false>(ctx, a, g, ldg, p.ksplit);
       else
-        launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg);
+        launch_rs<RsNarrow, TRANS, false>(ctx, a, g, ldg, p.ksplit);
+    }
   }
 }
 
@@ -441,18 +495,7 @@ void launch_gemv(bse_ctx* ctx, const bse::HopArgs& a) {
   int nsplit = std::max(1, std::min(64, (148 * 8 + rb - 1) / rb));
   nsplit = std::min(nsplit, std::max(1, a.kc / 64));
   const int kchunk = (a.kc + nsplit - 1) / nsplit;
-  const size_t need = (size_t)nsplit * 2 * a.mr * sizeof(zval);
-  if (ctx->gv_bytes < need) {
-    if (ctx->gv) {
-      CUDA_OK(cudaStreamSynchronize(ctx->stream));
-      CUDA_OK(cudaFree(ctx->gv));
-    }
-    ctx->gv = nullptr;
-    ctx->gv_bytes = 0;
-    CUDA_OK(cudaMalloc(&ctx->gv, need));
-    ctx->gv_bytes = need;
-  }
-  zval* part = static_cast<zval*>(ctx->gv);
+  zval* part = static_cast<zval*>(ensure_gv(ctx, (size_t)nsplit * 2 * a.mr * sizeof(zval)));
   bse::gemv_partial_kernel<<<dim3(rb, nsplit), bse::GV_THREADS, 0, ctx->stream>>>(
       a.pa, a.pb, a.lda, a.mr, a.kc, a.x1, a.x2, kchunk, part, (ctx->ham_flags & BSE_HAM_B_ZERO) ? 1 : 0);
   check_launch(ctx);
@@ -1083,6 +1126,7 @@ int bse_ctx_create(int device, bse_ctx** out) {
   bse_ctx* ctx = new bse_ctx();
   ctx->device = device;
   if (const char* g = std::getenv("BSE200_RS_GROUP_ROWS")) ctx->rs_group_rows = std::max(0, std::atoi(g));
+  if (const char* g = std::getenv("BSE200_RS_KSPLIT")) ctx->rs_ksplit = std::max(0, std::min(4, std::atoi(g)));
   try {
     CUDA_OK(cudaSetDevice(device));
     BLAS_OK(cublasCreate(&ctx->blas));
@@ -1129,7 +1173,7 @@ int bse_set_hamiltonian_flags(bse_ctx* ctx, unsigned flags) {
 int bse_set_filter_algorithm(bse_ctx* ctx, int complex_mults) {
   return guarded(ctx, [&] {
     if (!filter_code_valid(complex_mults))
-      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92, 94, 96 or 97 (include/bse200.h)");
+      throw BseError(BSE_EVALIDATION, "filter algorithm must be 4, 82, 86, 88, 90, 92, 94, 96, 97 or 98 (include/bse200.h)");
     ctx->filter_cm = complex_mults;
   });
 }

@@ -55,6 +55,10 @@ struct HopArgs {
   int shift_lo, shift_hi;
   const double* shift_col;
   int group_rows;  // real-split kernel CTA raster (hop_rs.cuh); 0 = column tiles fastest
+  // real-split split-K (hop_rs.cuh): ksplit > 1 CTAs share a tile's K range (gridDim.z) and write raw
+  // partial sums to part_ws [z][h][col][row]; rs_splitk_epilogue_kernel sums and finishes them
+  int ksplit;
+  zval* part_ws;
   // residual mode
   const double* lam;  // per column
   double* partial;    // [gridDim.y][k]

@@ -160,7 +160,11 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   const int i0 = (row_tile - h * nbm) * C::BM;
   const int c0 = col_tile * C::BN;
   const int nkt_part = (a.kc + C::BK - 1) / C::BK;
-  const int nkt = 2 * nkt_part;
+  // this CTA's K stages [kt0, kt1) of the 2 nkt_part (all of them unless split-K)
+  const int nsplit = a.ksplit > 1 ? a.ksplit : 1;
+  const int per_split = (2 * nkt_part + nsplit - 1) / nsplit;
+  const int kt0 = min(2 * nkt_part, (int)blockIdx.z * per_split);
+  const int nkt = min(2 * nkt_part, kt0 + per_split) - kt0;
 
   if (threadIdx.x == 0) {
 #pragma unroll
@@ -181,8 +185,9 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
       for (int lkt = 0; lkt < nkt; ++lkt) {
         const int b = lkt % C::STAGES;
         if (lkt >= C::STAGES) mbar_wait_cta(&empty[b], ((lkt - C::STAGES) / C::STAGES) & 1);
-        const int part = lkt >= nkt_part;
-        const int j0 = (lkt - part * nkt_part) * C::BK;
+        const int gkt = kt0 + lkt;
+        const int part = gkt >= nkt_part;
+        const int j0 = (gkt - part * nkt_part) * C::BK;
         unsigned char* st = base + b * STAGE_BYTES;
         tc::mbar_arrive_expect_tx(&full[b], STAGE_BYTES);
         if (TRANS)
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
     const double* Ps = stage_p(s);
     const zval* Xs = stage_x(s);
     RsFrag<C> f;
-    if ((kt >= nkt_part) == (h == 1)) {  // the i (forward) / -i (transposed) part of this half
+    if ((kt0 + kt >= nkt_part) == (h == 1)) {  // the i (forward) / -i (transposed) part of this half
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) {
         rs_load_frag_t<TRANS ? -1 : 1, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
@@ -228,6 +233,23 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(&empty[s]);
+  }
+
+  if (nsplit > 1) {  // raw partial sums; rs_splitk_epilogue_kernel finishes the output
+    zval* w = a.part_ws + ((int64_t)(blockIdx.z * 2 + h) * a.k) * a.mr;
+#pragma unroll
+    for (int i = 0; i < C::WM; ++i) {
+      const int row = i0 + wm * (8 * C::WM) + i * 8 + g;
+      if (row >= a.mr) continue;
+#pragma unroll
+      for (int j = 0; j < C::WN; ++j)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int col = c0 + wn * (8 * C::WN) + j * 8 + 2 * t + hh;
+          if (col < a.k) w[(int64_t)col * a.mr + row] = zval{acc[0][i][j][hh], acc[1][i][j][hh]};
+        }
+    }
+    return;
   }
 
   // epilogue: y_h = alpha (acc - shift s_h) - beta p_h on the output half h
@@ -261,6 +283,36 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
         yh[(int64_t)col * a.ldy + row] = out;
       }
     }
+  }
+}
+
+// split-K finish: y_h = alpha (sum_z part[z][h] - shift s_h) - beta p_h, the partials added in a
+// fixed order (deterministic), the same epilogue arithmetic as hop_rs_tma_kernel's
+__global__ void rs_splitk_epilogue_kernel(const HopArgs a) {
+  const int64_t total = 2 * (int64_t)a.k * a.mr;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int row = int(idx % a.mr);
+    const int64_t rest = idx / a.mr;
+    const int col = int(rest % a.k), h = int(rest / a.k);
+    double vr = 0.0, vi = 0.0;
+    for (int z = 0; z < a.ksplit; ++z) {
+      const zval v = a.part_ws[((int64_t)(z * 2 + h) * a.k + col) * a.mr + row];
+      vr += v.re;
+      vi += v.im;
+    }
+    if ((a.shift != 0.0 || a.shift_col) && row >= a.shift_lo && row < a.shift_hi) {
+      const double sc = a.shift_col ? a.shift_col[col] : a.shift;
+      const zval s = (h ? a.s2 : a.s1)[(int64_t)col * a.lds + row];
+      vr = vr - sc * s.re;
+      vi = vi - sc * s.im;
+    }
+    zval out{a.alpha * vr, a.alpha * vi};
+    if (a.beta != 0.0) {
+      const zval p = (h ? a.p2 : a.p1)[(int64_t)col * a.ldp + row];
+      out.re = out.re - a.beta * p.re;
+      out.im = out.im - a.beta * p.im;
+    }
+    (h ? a.y2 : a.y1)[(int64_t)col * a.ldy + row] = out;
   }
 }
 

@@ -3,6 +3,8 @@
 same planes; executed TF/s (4 n^2 k per step) against the measured 37.1 TF/s DMMA peak.
 
     python tools/rs_bench.py [m] [k,k,...] [code,code,...]   (bse_set_filter_algorithm codes)
+
+BSE200_RS_KSPLIT=s fixes the split-K factor of code 90 (0: planned per product; code 98 = tile 97, split 2).
 """
 import json
 import sys
@@ -68,11 +70,13 @@ for k in ks:
                                      rs=True), 4)
         yy = y.clone()
         same = None if ref is None else bool(torch.equal(ref, yy))
+        rdiff = None if ref is None else float((yy - ref).abs().max() / ref.abs().max())
         ref = yy if ref is None else ref
         ex = 4.0 * n * n * k / 1e12
         row = {"m": m, "k": k, "code": code, "fwd_ms": ms_f, "fwd_tflops": ex / ms_f * 1e3,
                "fwd_frac": ex / ms_f * 1e3 / PEAK, "trans_ms": ms_t, "trans_tflops": ex / ms_t * 1e3,
-               "trans_frac": ex / ms_t * 1e3 / PEAK, "bitwise_as_first_code": same}
+               "trans_frac": ex / ms_t * 1e3 / PEAK, "bitwise_as_first_code": same,
+               "max_rel_diff_vs_first": rdiff}
         out.append(row)
         print(json.dumps({kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in row.items()}), flush=True)
 ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, 90))
