@@ -1,6 +1,7 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle and
 the reference golden fixtures.  Tolerances are written next to each check."""
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -383,6 +384,27 @@ def test_filter_3m_variants_bitwise_identical(bse):
         assert torch.equal(v, outs[("3m", kk)]), (algo, kk)
 
 
+@pytest.mark.parametrize("ksplit", [2, 3, 4])
+def test_rs_split_k(ksplit):
+    """Split-K real-split products (hop_rs.cuh: a tile's contraction over ksplit CTAs, partial sums
+    reduced in fixed order by rs_splitk_epilogue_kernel): filter and transposed-tile product within
+    rounding of the unsplit tile, deterministic run to run; ragged shapes including splits left
+    without K stages (kc = 5 over 3 or 4 CTAs)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, BSE200_RS_KSPLIT=str(ksplit))
+    worker = Path(__file__).resolve().parent / "_splitk_worker.py"
+    r = subprocess.run([sys.executable, str(worker)], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rows = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(rows) == 4
+    for row in rows:
+        assert row["filter_rel"] <= 1e-13 and row["trans_rel"] <= 1e-14, row
+        assert row["repeat_bitwise"], row
+
+
 def test_filter_rs_matches_3m_and_tiles_bitwise(bse):
     """Real-split filter (csrc/hop_rs.cuh: folded basis, four real planes, 4 n^2 k flops per step)
     against the 3M filter at ragged shapes: within 1e-12 of the output scale; its tile variants
@@ -653,7 +675,8 @@ def test_planes_only_operator_solve(bse):
 
 def test_split_start_block_and_first_filter_change_no_bit(bse, monkeypatch):
     """The start block drawn in two column halves with the first filter run per half (solver.py;
-    the host draws the second half while the GPU filters the first) gives bitwise the same solve."""
+    the host draws the second half while the GPU filters the first) gives bitwise the same solve
+    (at sizes where the real-split products of both widths take the same split-K plan, as here)."""
     import paper_2601_10557_b200.solver as solver_mod
 
     a, b = golden_ham(64, 21)
