@@ -1085,14 +1085,15 @@ void c64_step(bse_ctx* ctx, bse::c64::Maps& maps, const C64Step& st) {
   const unsigned nt = (unsigned)((st.k + bse::c64::BN - 1) / bse::c64::BN);
   const unsigned mt = (unsigned)((st.mo + bse::c64::BM - 1) / bse::c64::BM);
   if (c64_pair(st.k)) {
-    // CTA pairs along x over the row tiles (an odd count gets one all-padding CTA)
+    // CTA pairs (clusters along x) over adjacent row tiles, column tiles fastest (c64.cuh; an odd
+    // row-tile count gets one all-padding CTA)
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3((mt + 1) / 2 * 2, nt);
+    cfg.gridDim = dim3(2 * nt, (mt + 1) / 2);
     cfg.blockDim = dim3(bse::c64::THREADS);
     cfg.dynamicSmemBytes = bse::c64::PAIR_SMEM;
     cfg.stream = ctx->stream;

@@ -172,8 +172,13 @@ __global__ void __launch_bounds__(THREADS, 1) step_kernel(const __grid_constant_
   uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // single CTA: grid (column tiles, row tiles); pair: grid (row tiles (even), column tiles)
-  const int c0 = (PAIR ? blockIdx.y : blockIdx.x) * BN, i0 = (PAIR ? blockIdx.x : blockIdx.y) * BM;
+  // column tiles fastest: a wave holds every column tile of a few row strips, so each strip of the
+  // operator planes is fetched from DRAM about once (with row tiles fastest the pair variant
+  // re-streamed the planes once per column tile: 262 GB per step at C3, k = 1200).
+  // single CTA: grid (column tiles, row tiles); pair: grid (2 x column tiles, row-tile pairs), the
+  // cluster (2, 1, 1) pairing row tiles 2y and 2y + 1 of one column tile
+  const int c0 = (PAIR ? blockIdx.x / 2 : blockIdx.x) * BN;
+  const int i0 = (PAIR ? 2 * blockIdx.y + (blockIdx.x & 1) : blockIdx.y) * BM;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;
   const int nk_part = (a.kc + BKE - 1) / BKE;
   const int nk = a.skip_b ? nk_part : 2 * nk_part;

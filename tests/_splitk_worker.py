@@ -40,7 +40,7 @@ def main():
         for code in (97, 98, 98):
             ctx.check(ctx.lib.bse_set_filter_algorithm(ctx.handle, code))
             v = v0.clone()
-            ctx.call("bse_chebyshev_filter_rs", _lib.dptr(gp), ldg, m, _lib.dptr(v), 2 * m, k, 3, 0.5, 2.0, -3.0,
+            ctx.call("bse_chebyshev_filter_rs", _lib.dptr(gp), ldg, m, _lib.dptr(v), 2 * m, k, 4, 0.5, 2.0, -3.0,
                      _lib.dptr(work))
             filt.setdefault(code, []).append(v)
         # transposed product of an m x kc tile (shift rows, beta term)
