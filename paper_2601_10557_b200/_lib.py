@@ -138,7 +138,9 @@ _FILTER_CM = _ALGOS[os.environ.get("BSE200_FILTER", "rs").lower()]
 
 def set_filter_algorithm(name: str) -> None:
     """'rs' (default: the real-split planes of csrc/hop_rs.cuh, half the FP64 tensor ops of 4M;
-    fixed tiles 'rs-tall4-k32' / 'rs-tall4' / 'rs-tall' / 'rs-narrow', bitwise identical), '3m' (Gauss split, 25% fewer FP64
+    tile and split-K factor planned per product; fixed unsplit tiles 'rs-tall4-k32' / 'rs-tall4' /
+    'rs-tall' / 'rs-narrow', bitwise identical; 'rs-tall4-k32-split' = the first with its K range
+    split over 2 CTAs (BSE200_RS_KSPLIT sets the factor)), '3m' (Gauss split, 25% fewer FP64
     tensor ops than 4M, operand sums precomputed once, TMA-fed producer-warp kernel; fixed tiles
     '3m-tma-narrow' / '3m-tma-wide', bitwise identical) or '4m'."""
     global _FILTER_CM

@@ -313,7 +313,7 @@ using Hop3MWide = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 1>;
 using Hop3MNarrowNP = bse::HopCfg<64, 16, 8, 4, 1, 4, 2, 0>;
 using Hop3MWideNP = bse::HopCfg<64, 32, 8, 4, 1, 6, 1, 0>;
 
-// 90 (92 / 94): the real-split kernel (hop_rs.cuh) -- bse_chebyshev_filter_rs, the RR's S H Q
+// 90 (92 / 94 / 96 / 97 / 98): the real-split kernel (hop_rs.cuh) -- bse_chebyshev_filter_rs, the RR's S H Q
 // on registered planes, the grid's tile products (bse_hop_tile_rs / _rs_t); the complex-operand
 // products that remain (B = 0, no planes) run code 88 under it
 bool filter_code_needs_planes(int code) {

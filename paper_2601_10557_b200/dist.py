@@ -430,22 +430,6 @@ def add_sum_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
     return tile
 
 
-def add_rs_planes(ops, tile: Tile, reserve: int = 0) -> Tile:
-    """Attach the tile's real-split planes [Ai + Bi | Ar - Br | Ar + Br | Ai - Bi] (bse_make_rs_planes) for
-    the filter products (CUDA ops only, B != 0), if they leave `reserve` bytes of HBM for the solve."""
-    if not hasattr(ops, "ctx"):
-        return tile
-    ldg = tile.mr + (tile.mr & 1)
-    if not _lib.planes_fit(ldg * 4 * tile.kc * 8, ops.device, reserve):
-        logger.warning("real-split planes of a %d x %d tile do not fit; the filter runs the 3M products",
-                       tile.mr, 2 * tile.kc)
-        return tile
-    g = ops.torch.empty((4 * tile.kc, ldg), dtype=ops.torch.float64, device=ops.device)
-    ops.ctx.call("bse_make_rs_planes", tile.buf.data_ptr(), tile.lda, tile.mr, tile.kc, g.data_ptr(), ldg)
-    tile.g, tile.ldg = g, ldg
-    return tile
-
-
 def tile_from_blocks(ops, a_t, b_t, transpose: bool = False) -> Tile:
     """One column-major [A_t | B_t] device buffer from tile blocks (host numpy or device tensors);
     transpose: the block transpose [A_t^H | B_t^T] instead."""

@@ -15,6 +15,7 @@ def family(name: str) -> str:
                      (r"hop_rs_tma_kernel", "bse::hop_rs_tma_kernel (real-split filter / RR)"),
                      (r"hop3m_tma_kernel", "bse::hop3m_tma_kernel"), (r"zgemm_kernel", "bse::zgemm_kernel (Grams, Q W)"),
                      (r"zgemm_splitk_reduce", "bse::zgemm_splitk_reduce"), (r"rs_fold", "bse::rs_fold_kernel"),
+                     (r"rs_splitk_epilogue", "bse::rs_splitk_epilogue_kernel (split-K finish)"),
                      (r"gemv_partial|sum_reduce|sdot_partial|lincomb3", "bse:: Lanczos GEMV / dots"),
                      (r"phase_fix", "bse::phase_fix_kernel"), (r"bse::", "bse:: other (HBM helpers)"),
                      (r"syevd|sytrd|steqr|laed|stedc|heevd|ormtr|orgtr|zhe|lacpy|larf|potrf|trsm|geqrf|cusolver|cublas",
