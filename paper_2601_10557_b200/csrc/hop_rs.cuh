@@ -34,6 +34,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "hop_mb.cuh"
 #include "tc_common.cuh"
 
@@ -106,12 +108,15 @@ __device__ __forceinline__ void rs_load_frag_t(RsFrag<C>& f, const double* Ps, c
   }
 }
 
-template <class C>
-__device__ __forceinline__ void rs_mma(double (&acc)[2][C::WM][C::WN][2], const RsFrag<C>& f) {
+// PARTIAL: only the first nv 8-column fragments of the warp hold columns < k (the last column
+// tile of a block whose width is not a multiple of BN); the others are skipped (warp-uniform)
+template <class C, bool PARTIAL = false>
+__device__ __forceinline__ void rs_mma(double (&acc)[2][C::WM][C::WN][2], const RsFrag<C>& f, int nv = C::WN) {
 #pragma unroll
   for (int i = 0; i < C::WM; ++i)
 #pragma unroll
     for (int j = 0; j < C::WN; ++j) {
+      if (PARTIAL && j >= nv) continue;
       dmma(acc[0][i][j], f.pf[i], f.br[j]);
       dmma(acc[1][i][j], f.pf[i], f.bi[j]);
     }
@@ -211,29 +216,39 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   constexpr int KS = C::BK / 4;
   auto stage_p = [&](int s) { return reinterpret_cast<const double*>(base + s * STAGE_BYTES); };
   auto stage_x = [&](int s) { return reinterpret_cast<const zval*>(base + s * STAGE_BYTES + P_BYTES); };
+  // 8-column fragments of this warp that hold columns < k: all of them except in the last column
+  // tile of a ragged block, where the rest are skipped (same bits for the valid columns)
+  const int nv = min(C::WN, max(0, (a.k - c0 - wn * 8 * C::WN + 7) / 8));
+  auto consume = [&](auto partial) {
+    constexpr bool PARTIAL = decltype(partial)::value;
 #pragma unroll 1
-  for (int kt = 0; kt < nkt; ++kt) {
-    const int s = kt % C::STAGES;
-    mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
-    const double* Ps = stage_p(s);
-    const zval* Xs = stage_x(s);
-    RsFrag<C> f;
-    if ((kt0 + kt >= nkt_part) == (h == 1)) {  // the i (forward) / -i (transposed) part of this half
+    for (int kt = 0; kt < nkt; ++kt) {
+      const int s = kt % C::STAGES;
+      mbar_wait_cta(&full[s], (kt / C::STAGES) & 1);
+      const double* Ps = stage_p(s);
+      const zval* Xs = stage_x(s);
+      RsFrag<C> f;
+      if ((kt0 + kt >= nkt_part) == (h == 1)) {  // the i (forward) / -i (transposed) part of this half
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        rs_load_frag_t<TRANS ? -1 : 1, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
-        rs_mma<C>(acc, f);
-      }
-    } else {
+        for (int ks = 0; ks < KS; ++ks) {
+          rs_load_frag_t<TRANS ? -1 : 1, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
+          rs_mma<C, PARTIAL>(acc, f, nv);
+        }
+      } else {
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        rs_load_frag_t<0, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
-        rs_mma<C>(acc, f);
+        for (int ks = 0; ks < KS; ++ks) {
+          rs_load_frag_t<0, TRANS, C>(f, Ps, Xs, ks, wm, wn, g, t);
+          rs_mma<C, PARTIAL>(acc, f, nv);
+        }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_cta(&empty[s]);
-  }
+  };
+  if (nv < C::WN)
+    consume(std::true_type{});
+  else
+    consume(std::false_type{});
 
   if (nsplit > 1) {  // raw partial sums; rs_splitk_epilogue_kernel finishes the output
     zval* w = a.part_ws + ((int64_t)(blockIdx.z * 2 + h) * a.k) * a.mr;
