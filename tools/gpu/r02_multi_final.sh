@@ -1,6 +1,5 @@
 #!/bin/bash
-# round 2, call h (4 GPUs): split-K real-split products at N = 4 / 2 (C3, driver step counts) and the
-# A/B against the unsplit plan (BSE200_RS_KSPLIT=1) at N = 4
+# round 2, call h (4 GPUs): final build (split-K + ragged last column tile) at N = 4 / 2 (C3)
 mkdir -p gpurun_out/r02h
 TR4="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29591"
 TR2="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29593"
