@@ -213,6 +213,17 @@ int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* args, const void* d_g
  * of the 2D grid (the same local block, conjugate-transposed), so a grid GPU
  * stores one tile's planes.  Arguments and epilogue as bse_hop_tile_rs.                        */
 int bse_hop_tile_rs_t(bse_ctx* ctx, const bse_hop_tile_args* args, const void* d_g, int64_t ldg);
+/* Fused group reduction of the 2D grid's tile products (dist.py, BSE200_FUSED_REDUCE=1): the next
+ * real-split tile products (bse_hop_tile_rs / _rs_t) store their output tile not to y1 / y2 but to
+ * each of the n (<= 4) base pointers -- this rank's slot in every group member's symmetric
+ * (NVLink peer-mapped) inbox, same layout as y -- from the kernel epilogue, so the transfer
+ * overlaps the product tile by tile; n = 0 restores local output.  Replaces the NCCL allreduce
+ * after the tile product (dist.py sum_row / sum_col; the paper's row / column allreduce,
+ * PAPER.md:723-740).                                                                           */
+int bse_set_push_targets(bse_ctx* ctx, void* const* y_bases, int n);
+/* y[i] = sum_{j < nslot} inbox[j * slot_stride + i], i < count (complex elements), slots added in
+ * order: the second half of the fused group reduction, after a barrier among the group.        */
+int bse_group_sum(bse_ctx* ctx, const void* d_inbox, int64_t slot_stride, int nslot, void* d_y, int64_t count);
 /* (X1, X2) -> (scale (X1 + X2), scale2 (X1 - X2)) for a block of 2 rows x k (ld >= 2 rows; X1 rows
  * [0, rows), X2 rows [rows, 2 rows)); (1, 1) folds, (1/2, 1/2) unfolds, (1/2, -1/2) unfolds with
  * the S-flip; d_dst may equal d_src.                                                           */

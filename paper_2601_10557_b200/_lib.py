@@ -83,6 +83,8 @@ _SIGS = {
     "bse_hop_tile": (C.c_int, [_vp, C.POINTER(HopTileArgs)]),
     "bse_hop_tile_rs": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
     "bse_hop_tile_rs_t": (C.c_int, [_vp, C.POINTER(HopTileArgs), _vp, _i64]),
+    "bse_set_push_targets": (C.c_int, [_vp, C.POINTER(_vp), C.c_int]),
+    "bse_group_sum": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp, _i64]),
     "bse_set_rr_capture": (C.c_int, [_vp, _vp]),
     "bse_extend_sbasis": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64]),
     "bse_s_orthonormalize_basis": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _ip]),

@@ -58,6 +58,8 @@ struct bse_ctx {
   unsigned ham_flags = 0;  // BSE_HAM_B_ZERO: operator calls skip the B half of the contraction
   int rs_group_rows = 8;  // real-split CTA raster (hop_rs.cuh): BSE200_RS_GROUP_ROWS, 0 = columns fastest
   int rs_ksplit = 0;      // real-split split-K: BSE200_RS_KSPLIT (0 = planned per product, rs_plan)
+  int push_n = 0;         // fused group reduction: push targets of the next real-split products
+  zval* push_base[4] = {nullptr, nullptr, nullptr, nullptr};
   void* gv = nullptr;  // split-K GEMV partials
   size_t gv_bytes = 0;
   // second stream + cuSOLVER handle: the RR pencil's eigenvalues of M run beside chol(W) -> eigh(G)
@@ -326,9 +328,9 @@ bool filter_code_valid(int code) { return code == 4 || filter_code_needs_planes(
 void launch_filter_hop(bse_ctx* ctx, const bse::HopArgs& a) {
   int code = ctx->filter_cm >= 90 ? 88 : ctx->filter_cm;
   if (filter_code_needs_planes(code) && (!a.sa || !a.sb))  // no P sum planes: sums in registers
-    code = 98;
+    code = -88;  // internal only (not a bse_set_filter_algorithm code)
   switch (code) {
-    case 98:  // the default's TMA kernel forming the operand sums in registers (same bits)
+    case -88:  // the default's TMA kernel forming the operand sums in registers (same bits)
       if (a.k >= 512)
         launch_hop_tma<Hop3MWideNP>(ctx, a);
       else
@@ -434,6 +436,8 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
   ar.group_rows = ctx->rs_group_rows;
   ar.ksplit = ksplit;
   ar.part_ws = nullptr;
+  ar.npush = ctx->push_n;
+  for (int r = 0; r < 4; ++r) ar.push[r] = ctx->push_base[r];
   if (ksplit > 1)
     ar.part_ws = static_cast<zval*>(ensure_gv(ctx, (size_t)ksplit * 2 * a.k * a.mr * sizeof(zval)));
   bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(ar, mp);
@@ -1782,6 +1786,27 @@ int bse_hop_tile_rs(bse_ctx* ctx, const bse_hop_tile_args* t, const void* d_g, i
       throw BseError(BSE_EVALIDATION, "shift needs s1/s2");
     if (ctx->ham_flags & BSE_HAM_B_ZERO) throw BseError(BSE_EVALIDATION, "the real-split product needs B != 0");
     rs_product(ctx, a, static_cast<const double*>(d_g), ldg);
+  });
+}
+
+int bse_set_push_targets(bse_ctx* ctx, void* const* y_bases, int n) {
+  return guarded(ctx, [&] {
+    if (n < 0 || n > 4 || (n > 0 && !y_bases)) throw BseError(BSE_EVALIDATION, "push targets: 0..4 base pointers");
+    for (int r = 0; r < n; ++r)
+      if (!y_bases[r]) throw BseError(BSE_EVALIDATION, "null push target");
+    ctx->push_n = n;
+    for (int r = 0; r < 4; ++r) ctx->push_base[r] = r < n ? static_cast<zval*>(y_bases[r]) : nullptr;
+  });
+}
+
+int bse_group_sum(bse_ctx* ctx, const void* d_inbox, int64_t slot_stride, int nslot, void* d_y, int64_t count) {
+  return guarded(ctx, [&] {
+    if (count <= 0) return;
+    if (!d_inbox || !d_y || nslot < 1 || slot_stride < count) throw BseError(BSE_EVALIDATION, "group sum arguments");
+    const int blocks = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+    bse::group_sum_kernel<<<blocks, 256, 0, ctx->stream>>>(static_cast<const zval*>(d_inbox), slot_stride, nslot,
+                                                          static_cast<zval*>(d_y), count);
+    check_launch(ctx);
   });
 }
 

@@ -59,6 +59,11 @@ struct HopArgs {
   // partial sums to part_ws [z][h][col][row]; rs_splitk_epilogue_kernel sums and finishes them
   int ksplit;
   zval* part_ws;
+  // fused group reduction (dist.py, 2D grid): npush > 0 -> the real-split output tile is stored to
+  // npush peers' inbox slots (this rank's slot in each group member's symmetric buffer, NVLink
+  // stores from the epilogue) instead of y1 / y2; y2's offset from y1 carries over to each target
+  int npush;
+  zval* push[4];
   // residual mode
   const double* lam;  // per column
   double* partial;    // [gridDim.y][k]

@@ -122,6 +122,17 @@ __device__ __forceinline__ void rs_mma(double (&acc)[2][C::WM][C::WN][2], const 
     }
 }
 
+// output store of half h at element idx = col * ldy + row: local y, or every push target
+__device__ __forceinline__ void rs_store(const HopArgs& a, int h, int64_t idx, const zval& out) {
+  if (a.npush > 0) {
+    const int64_t off = h ? (a.y2 - a.y1) : 0;
+#pragma unroll 1
+    for (int r = 0; r < a.npush; ++r) a.push[r][off + idx] = out;
+  } else {
+    (h ? a.y2 : a.y1)[idx] = out;
+  }
+}
+
 // grid: x = column tiles (fastest: CTAs sharing a plane strip run together), y = 2 * row tiles
 // plane read by output half h for input part (0: x, 1: y): forward Z V | U W, transposed W V | U Z
 template <bool TRANS>
@@ -268,7 +279,6 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   }
 
   // epilogue: y_h = alpha (acc - shift s_h) - beta p_h on the output half h
-  zval* yh = h ? a.y2 : a.y1;
   const zval* sh = h ? a.s2 : a.s1;
   const zval* ph = h ? a.p2 : a.p1;
 #pragma unroll
@@ -295,7 +305,7 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
           out.re = out.re - a.beta * p.re;
           out.im = out.im - a.beta * p.im;
         }
-        yh[(int64_t)col * a.ldy + row] = out;
+        rs_store(a, h, (int64_t)col * a.ldy + row, out);
       }
     }
   }
@@ -327,7 +337,22 @@ __global__ void rs_splitk_epilogue_kernel(const HopArgs a) {
       out.re = out.re - a.beta * p.re;
       out.im = out.im - a.beta * p.im;
     }
-    (h ? a.y2 : a.y1)[(int64_t)col * a.ldy + row] = out;
+    rs_store(a, h, (int64_t)col * a.ldy + row, out);
+  }
+}
+
+// y = sum_j inbox[j] over the nslot slots of a group's symmetric buffer, in slot order (the fused
+// group reduction's second half: every member adds the same partials in the same order)
+__global__ void group_sum_kernel(const zval* __restrict__ inbox, int64_t stride, int nslot, zval* __restrict__ y,
+                                 int64_t count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    zval v = inbox[i];
+    for (int j = 1; j < nslot; ++j) {
+      const zval w = inbox[j * stride + i];
+      v.re += w.re;
+      v.im += w.im;
+    }
+    y[i] = v;
   }
 }
 

@@ -38,6 +38,7 @@ for the collectives.
 from __future__ import annotations
 
 import ctypes
+from functools import partial
 import logging
 import math
 from dataclasses import dataclass
@@ -564,15 +565,74 @@ class DistSolver:
         """col -> row partial product, summed over the row communicator into y_row."""
         g = self.g
         lo, hi = g.diag
-        self.ops.hop(self.fwd, x_col, y_row, shift_rows=(lo - g.r0, hi - g.r0), s_off=g.r0 - g.c0, **kw)
-        self.c.sum_row(y_row)
+        hop = partial(self.ops.hop, self.fwd, x_col, y_row, shift_rows=(lo - g.r0, hi - g.r0), s_off=g.r0 - g.c0,
+                      **kw)
+        if not self._fused_reduce("row", hop, y_row, kw):
+            hop()
+            self.c.sum_row(y_row)
 
     def transposed(self, x_row, y_col, **kw):
         """row -> col partial product (block-transposed tiles), summed over the column communicator."""
         g = self.g
         lo, hi = g.diag
-        self.ops.hop(self.trn, x_row, y_col, shift_rows=(lo - g.c0, hi - g.c0), s_off=g.c0 - g.r0, **kw)
-        self.c.sum_col(y_col)
+        hop = partial(self.ops.hop, self.trn, x_row, y_col, shift_rows=(lo - g.c0, hi - g.c0), s_off=g.c0 - g.r0,
+                      **kw)
+        if not self._fused_reduce("col", hop, y_col, kw):
+            hop()
+            self.c.sum_col(y_col)
+
+    # ---- fused tile product + group reduction over NVLink peer memory (BSE200_FUSED_REDUCE=1) -----
+    FUSED_REDUCE = __import__("os").environ.get("BSE200_FUSED_REDUCE", "0") == "1"
+
+    def _fused_reduce(self, group: str, hop, y, kw) -> bool:
+        """The tile product followed by the group allreduce as ONE real-split kernel whose epilogue
+        stores each output tile into this rank's slot of every group member's symmetric inbox
+        (NVLink stores, overlapping the transfer with the product tile by tile), a barrier among
+        the group, and a local fixed-order sum of the slots (bse_set_push_targets, bse_group_sum).
+        Real-split products on CUDA ops under NCCL only; False -> the caller runs hop + allreduce."""
+        size = self.g.q if group == "row" else self.g.p
+        if not (self.FUSED_REDUCE and size > 1 and size <= 4 and kw.get("rs") and hasattr(self.ops, "ctx")
+                and self.c.dist.get_backend() == "nccl" and y.is_contiguous()):
+            return False
+        k = y.shape[0]
+        t, h, cap, ptrs = self._inbox(group, y.shape[1], k)
+        ctx = self.ops.ctx
+        me = h.rank
+        targets = (ctypes.c_void_p * size)(*[ptrs[j] + me * cap * ZB for j in range(size)])
+        h.barrier(channel=0, timeout_ms=120000)  # every member has summed its inbox from this group's previous product
+        ctx.call("bse_set_push_targets", targets, size)
+        try:
+            hop()
+        finally:
+            ctx.call("bse_set_push_targets", None, 0)
+        h.barrier(channel=0, timeout_ms=120000)  # every member's stores into this inbox are complete
+        ctx.call("bse_group_sum", t.data_ptr(), cap, size, y.data_ptr(), y.numel())
+        return True
+
+    def _inbox(self, group: str, width: int, k: int):
+        """This rank's symmetric inbox for the group: one slot of >= k x width complex per member."""
+        cache = self.__dict__.setdefault("_inboxes", {})
+        need = k * width
+        ent = cache.get(group)
+        if ent is None or ent[2] < need:
+            import torch.distributed._symmetric_memory as symm
+
+            size = self.g.q if group == "row" else self.g.p
+            pg = self.c.row if group == "row" else self.c.col
+            cap = max(need, ent[2] if ent else 0)
+            if ent is not None:
+                # no kernel of this rank may still read the old inbox, and no peer writes into it
+                # outside a product bracketed by the group's barriers: drain, then free
+                self.torch.cuda.synchronize(self.ops.device)
+                ent[1].barrier(channel=0, timeout_ms=120000)
+                self.torch.cuda.synchronize(self.ops.device)
+            cache.pop(group, None)
+            ent = None
+            t = symm.empty(2 * size * cap, dtype=self.torch.float64, device=self.ops.device)
+            h = symm.rendezvous(t, pg)
+            ent = (t, h, cap, list(h.buffer_ptrs))
+            cache[group] = ent
+        return ent
 
     def chebyshev(self, v_col, cfg: FilterConfig, row_buf):
         """p(H) v in place (col layout); row_buf: (k, 2 nr) scratch.  chebyshev.py:58-74.
@@ -1024,6 +1084,12 @@ class DistSolver:
         g = self.g
         n, nevex, nev, tol = 2 * g.m, cfg.nevex, cfg.nev, cfg.tol
         cfg.validate(n)
+        if self.FUSED_REDUCE and self.planes and hasattr(self.ops, "ctx") and g.world > 1:
+            # the fused reductions' symmetric inboxes at full width up front (collective; no regrowth)
+            if g.q > 1:
+                self._inbox("row", 2 * g.nr, nevex)
+            if g.p > 1:
+                self._inbox("col", 2 * g.nc, nevex)
         ledger = PhaseLedger()
         st = _Steps("solve", g.rank)
         seed3 = rng.substream(cfg.seed, TAG_SUBSPACE)
