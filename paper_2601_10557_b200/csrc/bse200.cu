@@ -420,7 +420,13 @@ void* ensure_gv(bse_ctx* ctx, size_t need) {
 template <class C, bool TRANS = false, bool GENERIC = false>
 void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg, int ksplit = 1) {
   constexpr size_t smem = C::template smem<TRANS>();
-  ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS, GENERIC>, (int)smem);
+  // fused group reduction: the PUSH instantiation stores the output tiles to the push targets;
+  // split-K products push from rs_splitk_epilogue_kernel instead
+  const bool push = ctx->push_n > 0 && ksplit == 1;
+  if (push)
+    ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS, GENERIC, true>, (int)smem);
+  else
+    ensure_smem(ctx, (const void*)bse::hop_rs_tma_kernel<C, TRANS, GENERIC>, (int)smem);
   bse::RsMaps mp;
   for (int q = 0; q < 4; ++q) {
     if (TRANS)
@@ -440,7 +446,10 @@ void launch_rs(bse_ctx* ctx, const bse::HopArgs& a, const double* g, int64_t ldg
   for (int r = 0; r < 4; ++r) ar.push[r] = ctx->push_base[r];
   if (ksplit > 1)
     ar.part_ws = static_cast<zval*>(ensure_gv(ctx, (size_t)ksplit * 2 * a.k * a.mr * sizeof(zval)));
-  bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(ar, mp);
+  if (push)
+    bse::hop_rs_tma_kernel<C, TRANS, GENERIC, true><<<grid, C::THREADS + 32, smem, ctx->stream>>>(ar, mp);
+  else
+    bse::hop_rs_tma_kernel<C, TRANS, GENERIC><<<grid, C::THREADS + 32, smem, ctx->stream>>>(ar, mp);
   check_launch(ctx);
   if (ksplit > 1) {
     const int64_t total = 2 * (int64_t)a.k * a.mr;

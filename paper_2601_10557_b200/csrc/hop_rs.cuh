@@ -143,7 +143,9 @@ __device__ __forceinline__ int rs_plane(int h, int part) {
 // GENERIC: fragment loads through a generic pointer (LD) instead of shared-space LDS -- measured
 // faster for the 128 x 32 tile, slower for the 64 x 32 one (profiles/r02/rs_consumer_variants_*.txt;
 // a slice-ahead software-pipelined consumer measured 3-9% slower than both and was dropped)
-template <class C, bool TRANS = false, bool GENERIC = false>
+// PUSH: the fused group reduction's instantiation (stores through rs_store to the push targets);
+// the default one keeps the plain local store, so its code is unchanged by the feature
+template <class C, bool TRANS = false, bool GENERIC = false, bool PUSH = false>
 __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(const HopArgs a,
                                                                               const __grid_constant__ RsMaps maps) {
   constexpr int P_BYTES = C::template p_bytes<TRANS>();
@@ -279,6 +281,7 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
   }
 
   // epilogue: y_h = alpha (acc - shift s_h) - beta p_h on the output half h
+  zval* yh = h ? a.y2 : a.y1;
   const zval* sh = h ? a.s2 : a.s1;
   const zval* ph = h ? a.p2 : a.p1;
 #pragma unroll
@@ -305,7 +308,10 @@ __global__ void __launch_bounds__(C::THREADS + 32, C::MINB) hop_rs_tma_kernel(co
           out.re = out.re - a.beta * p.re;
           out.im = out.im - a.beta * p.im;
         }
-        rs_store(a, h, (int64_t)col * a.ldy + row, out);
+        if constexpr (PUSH)
+          rs_store(a, h, (int64_t)col * a.ldy + row, out);
+        else
+          yh[(int64_t)col * a.ldy + row] = out;
       }
     }
   }

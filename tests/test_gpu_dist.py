@@ -165,3 +165,60 @@ def test_grid_storage_is_one_tile_of_planes():
     ds = DistributedSolver((a, b), device=torch.device("cuda", 0))
     assert ds.planes and ds.fwd.buf is None and ds.trn.buf is None and ds.trn.g is ds.fwd.g
     assert ds.operator_bytes() == 4 * 64 * 64 * 8
+
+
+@pytest.mark.parametrize("algo", ["rs", "rs-tall4-k32-split"])
+@pytest.mark.parametrize("trans", [False, True])
+def test_push_targets_and_group_sum(algo, trans):
+    """The fused group reduction's device half on one GPU (dist.py _fused_reduce, BSE200_FUSED_REDUCE):
+    with two push targets the real-split tile product (unsplit and split-K) stores its output into
+    both inbox slots and not into y; bse_group_sum adds the slots in order.  Two copies of the same
+    partial sum to exactly twice the pushed tile, which is the plain product's output to rounding."""
+    import ctypes
+
+    from paper_2601_10557_b200 import _lib
+    from paper_2601_10557_b200.dist import CudaOps, plane_tiles, tile_from_blocks
+
+    dev = torch.device("cuda", 0)
+    ops = CudaOps(dev)
+    ctx = ops.ctx
+    ctx.set_ham_flags(0)
+    gen = torch.Generator(device=dev).manual_seed(31)
+
+    def rnd(*shape):
+        return torch.complex(torch.randn(*shape, generator=gen, device=dev, dtype=torch.float64),
+                             torch.randn(*shape, generator=gen, device=dev, dtype=torch.float64))
+
+    mr, kc, k = 203, 157, 75
+    fwd, trn = plane_tiles(ops, tile_from_blocks(ops, rnd(mr, kc), rnd(mr, kc)))
+    tile = trn if trans else fwd
+    rows_in, rows_out = (mr, kc) if trans else (kc, mr)
+    x, p = rnd(k, 2 * rows_in), rnd(k, 2 * rows_out)
+    kw = dict(alpha=0.75, shift=3.5, shift_rows=(1, min(mr, kc) - 1), s_off=1, beta=0.25, p=p, filter=True, rs=True)
+    default = _lib.filter_algorithm()
+    try:
+        _lib.set_filter_algorithm(algo)
+        ref = torch.zeros(k, 2 * rows_out, dtype=torch.complex128, device=dev)
+        ops.hop(tile, x, ref, **kw)
+        cap = k * 2 * rows_out + 64  # slot stride larger than the block, as for a full-width inbox
+        inbox = torch.zeros(2 * cap, dtype=torch.complex128, device=dev)
+        untouched = torch.full((k, 2 * rows_out), 7.0, dtype=torch.complex128, device=dev)
+        targets = (ctypes.c_void_p * 2)(inbox.data_ptr(), inbox.data_ptr() + cap * 16)
+        ctx.call("bse_set_push_targets", targets, 2)
+        try:
+            ops.hop(tile, x, untouched, **kw)
+        finally:
+            ctx.call("bse_set_push_targets", None, 0)
+        out = torch.empty_like(ref)
+        ctx.call("bse_group_sum", inbox.data_ptr(), cap, 2, out.data_ptr(), out.numel())
+        torch.cuda.synchronize()
+    finally:
+        _lib.set_filter_algorithm(default)
+    assert torch.equal(untouched, torch.full_like(untouched, 7.0))  # no local store while pushing
+    s0 = inbox[:k * 2 * rows_out].view(k, -1)
+    s1 = inbox[cap:cap + k * 2 * rows_out].view(k, -1)
+    assert torch.equal(s0, s1)  # every target receives the same bits
+    # the pushed tile equals the local-store product to rounding (the compiler may contract the
+    # epilogue's multiply-adds differently on the two store paths)
+    assert (s0 - ref).abs().max().item() <= 4e-16 * ref.abs().max().item()
+    assert torch.equal(out, s0 + s1)
