@@ -385,10 +385,16 @@ RsPlan rs_plan(int64_t rows, int64_t kc, int64_t k, int force_split = 0) {
     const int64_t bm = wide ? 128 : 64;
     const double eff = wide ? 0.968 : 0.935;
     const int64_t nkt = 2 * ((kc + 31) / 32);  // K stages of a tile (BK 32; the 64-row tile's BK 16 doubles it)
+    const double waves1 = col * 2.0 * double((rows + bm - 1) / bm) / slots;
+    const bool can_split = nkt / 2 >= 16 && (size_t)2 * 2 * k * rows * 16 <= RS_SPLIT_WS_MAX;
     for (int sp = 1; sp <= 4; ++sp) {
       if (force_split > 0 && sp != force_split) continue;
       if (sp > 1 && (nkt / sp < 16 || (size_t)sp * 2 * k * rows * 16 > RS_SPLIT_WS_MAX)) continue;
-      const double waves = col * 2.0 * double((rows + bm - 1) / bm) * sp / slots;
+      // under ~20 waves the unsplit grid loses more to the uneven finish of its long CTAs than
+      // the fill estimate shows (m = 10k: k = 810 93.9% unsplit vs 95.1% split 4, k = 266
+      // 86.3% vs 90.7%; profiles/r02/rs_plan_m10k.txt)
+      if (sp == 1 && force_split == 0 && waves1 < 20.0 && can_split) continue;
+      const double waves = waves1 * sp;
       double t = flop_s / eff * std::ceil(waves) / waves;
       if (sp > 1) t += (2.0 * sp * 2.0 * double(k) * double(rows) * 16.0) / 6.0e12 + 4e-6;
       if (t < best_t * 0.995) {  // prefer the earlier (wider, unsplit) plan on near ties
