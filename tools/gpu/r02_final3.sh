@@ -1,5 +1,5 @@
 #!/bin/bash
-# round 2, last 1-GPU validation (PUSH instantiation for the fused reduction, default kernel unchanged): GPU suite,
+# round 2, last 1-GPU validation (final plan: split under 20 waves): GPU suite,
 # smoke, kernel timing at C3 widths, C3 bench
 mkdir -p gpurun_out/r02z3
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02z3/pytest.log 2>&1; echo "pytest rc=$?"; grep -E "passed|failed|FAILED" gpurun_out/r02z3/pytest.log | tail -8
